@@ -1,0 +1,163 @@
+/* kvr_cuda.h — thin C-ABI between the kvrail host C++ and the sm_100a kernels.
+ *
+ * libkvr_cuda.so implements it. It replaces the reference's simulated device
+ * (SimEngine::execute_step, sim_engine.cpp:33-72, and the cost-model "issue"
+ * CostModel::dma_time, sim_engine.hpp:42-44) with a real B200 step: a device
+ * arena of pages, a device page-table mirror of the committed views, a
+ * fixed-shape window ring per slot, and one committed step descriptor per
+ * step consumed by a captured CUDA graph. All structs are POD; offsets in the
+ * descriptor are bytes from its start; every section is 16-byte aligned.
+ * Status codes follow kvrail_c.h (0 ok, KVR_E_CUDA for CUDA failures).
+ */
+#ifndef KVR_CUDA_H
+#define KVR_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { KVR_ELEM_F32 = 0, KVR_ELEM_F16 = 1, KVR_ELEM_BF16 = 2 };
+enum { KVR_PAYLOAD_BYTES = 0, KVR_PAYLOAD_LANES = 1 };
+#define KVR_NO_SLOT 0xffffffffu
+#define KVR_SUMMARY_BASE (1ull << 40) /* summary slots' logical tokens, scenario.cpp:41 */
+
+typedef struct kvr_geometry {
+    int32_t device;
+    int32_t elem_kind;      /* KVR_ELEM_* (attention / lanes interpretation) */
+    uint32_t elem_bytes;    /* PagerConfig::elem_bytes */
+    uint32_t payload_mode;  /* KVR_PAYLOAD_* */
+    uint64_t page_bytes;
+    uint64_t token_bytes;   /* 2 * L * kv_heads * head_dim * elem_bytes */
+    uint32_t arena_pages;
+    uint32_t tokens_per_page;
+    uint32_t layers;
+    uint32_t kv_heads;
+    uint32_t head_dim;
+    uint32_t q_heads;
+    uint32_t n_slots;       /* fixed batch width (Driver concurrency) */
+    uint32_t near_window;   /* W* */
+    uint32_t ring_rows;     /* R >= W*, multiple of 32 */
+    uint32_t far_cap;       /* far slots visible to attention (0 = no far view) */
+    uint32_t chunk_tokens;  /* sv_chunk */
+    uint32_t max_chunks;    /* far rows kept per slot */
+    uint64_t max_tokens;    /* per-slot capacity of the device page table */
+    uint64_t seed;          /* synthetic payload seed (ScenarioConfig::seed) */
+    uint32_t attention;     /* run K-attn each step */
+    uint32_t use_graph;     /* replay the step as a CUDA graph */
+    uint64_t max_desc_bytes;/* capacity of one step descriptor */
+    uint32_t max_scan_descs;/* K-scan capacity (descriptors / spans) */
+    uint32_t max_trains;
+} kvr_geometry;
+
+/* ---- committed step descriptor ------------------------------------------ */
+typedef struct kvr_step_header {
+    uint64_t step;
+    double now;             /* transport clock (stage_time of every descriptor) */
+    uint64_t tau;           /* TransportConfig::merge_threshold */
+    double max_hold;        /* TransportConfig::max_hold */
+    uint32_t merge;
+    uint32_t n_zero, n_cow, n_edit, n_write, n_blob, n_need, n_span, n_prime, n_far_ids;
+    uint64_t write_tokens;  /* sum of kvr_write_op.count over source-0 writes */
+    uint64_t off_zero, off_cow, off_edit, off_write, off_blob_ops, off_blob, off_need, off_span,
+        off_prime, off_far_ids, off_slots;
+    uint64_t total_bytes;
+} kvr_step_header;
+
+typedef struct kvr_zero_op { uint32_t block, slot_begin, slot_count, pad; } kvr_zero_op;
+typedef struct kvr_cow_op { uint32_t src, dst; } kvr_cow_op;
+/* committed view delta: tokens [tok_begin,tok_end) of `slot` -> block/slot_begin
+ * (block == 0xffffffff: unmapped). Tokens >= KVR_SUMMARY_BASE are summary slots. */
+typedef struct kvr_edit_op {
+    uint64_t tok_begin, tok_end;
+    uint32_t slot, block, slot_begin, pad;
+} kvr_edit_op;
+/* payload generated in place: source 0 = synthetic token payload of
+ * (session, token..token+count); source 1 = far summary of chunk tokens
+ * [aux, aux + chunk_tokens) of `dev_slot` written to (block, slot). */
+typedef struct kvr_write_op {
+    uint64_t token;
+    uint64_t aux;
+    uint64_t prefix;        /* exclusive prefix of count over source-0 ops */
+    uint32_t block, slot, count, session;
+    uint32_t dev_slot;      /* KVR_NO_SLOT: arena only */
+    uint32_t source;
+} kvr_write_op;
+/* host payload bytes (Pager::write_tokens) carried in the descriptor blob */
+typedef struct kvr_blob_op {
+    uint64_t blob_offset;
+    uint32_t block, slot, count, pad;
+} kvr_blob_op;
+typedef struct kvr_need_rec {
+    uint32_t slot, session, kind, span_begin, span_count, pad;
+} kvr_need_rec;
+typedef struct kvr_span_rec {
+    uint64_t first_token;   /* logical token of slot_begin */
+    uint32_t block, slot_begin, slot_count, pad;
+} kvr_span_rec;
+typedef struct kvr_prime_op {
+    uint64_t tok_begin, tok_end;
+    uint32_t slot, pad;
+} kvr_prime_op;
+/* one per device slot, always n_slots entries */
+typedef struct kvr_slot_state {
+    uint64_t written;       /* tokens appended (attention length) after this step */
+    uint32_t session;
+    uint32_t live;          /* attention runs for this slot this step */
+    uint32_t far_begin;     /* index into the far-id array */
+    uint32_t far_count;     /* selected far chunks (<= far_cap) */
+} kvr_slot_state;
+
+/* step results (written by the device, read back one step later) */
+typedef struct kvr_step_stats {
+    uint64_t step;
+    double device_ms;
+    uint32_t trains, descriptors, spans, status;
+    uint64_t train_bytes;
+    uint64_t staged_tokens;
+    uint64_t writeback_tokens;
+    uint64_t attn_bytes;
+} kvr_step_stats;
+
+typedef struct kvr_dev kvr_dev;
+
+const char *kvr_dev_last_error(void);
+int kvr_dev_count(int *out);
+int kvr_dev_open(const kvr_geometry *g, kvr_dev **out);
+int kvr_dev_close(kvr_dev *d);
+/* pinned host memory for descriptors (two ring slots of max_desc_bytes) */
+int kvr_dev_desc_buffer(kvr_dev *d, uint32_t ring_slot, void **out);
+/* publish ring slot `ring_slot` (desc_bytes used) and launch the step */
+int kvr_dev_launch(kvr_dev *d, uint32_t ring_slot, uint64_t desc_bytes);
+/* byte-only apply of a descriptor outside a step (zero/cow/writes/edits) */
+int kvr_dev_apply_only(kvr_dev *d, uint32_t ring_slot, uint64_t desc_bytes);
+/* wait for the step launched from `ring_slot` and return its stats */
+int kvr_dev_wait(kvr_dev *d, uint32_t ring_slot, kvr_step_stats *out);
+int kvr_dev_sync(kvr_dev *d);
+
+enum {
+    KVR_BUF_ARENA = 0,   /* bytes */
+    KVR_BUF_RING = 1,    /* [slot][layer][row][2*d_kv] elements */
+    KVR_BUF_TMAP = 2,    /* [slot][max_tokens] u32 global slot index */
+    KVR_BUF_OUT = 3,     /* [slot][layer][q_head][head_dim] f32 */
+    KVR_BUF_QUERY = 4,   /* [slot][layer][q_head][head_dim] f32 */
+    KVR_BUF_FAR = 5,     /* [slot][layer][max_chunks][2*d_kv] elements */
+    KVR_BUF_TRAINS = 6,  /* kvr_train[max_trains] (kvrail_c.h layout) */
+    KVR_BUF_DESCS = 7,   /* kvr_descriptor[max_scan_descs] in train order */
+    KVR_BUF_SCAN = 8,    /* u32 counters: trains, descriptors, spans, status */
+    KVR_BUF_SMAP = 9,    /* [slot][max_chunks] u32 summary-slot map */
+};
+int kvr_dev_read(kvr_dev *d, int buffer, uint64_t offset, uint64_t bytes, void *out);
+int kvr_dev_buffer_bytes(kvr_dev *d, int buffer, uint64_t *out);
+/* time `iters` replays of the last launched step's attention kernel alone
+ * (CUDA events on the launch stream); used by bench.py for the roofline */
+int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms_per_launch);
+int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms_per_launch);
+/* name of the attention kernel variant chosen for this geometry */
+const char *kvr_dev_attention_variant(kvr_dev *d);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KVR_CUDA_H */

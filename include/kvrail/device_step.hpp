@@ -1,0 +1,94 @@
+// kvrail-b200 — the B200 side of one decode step, as seen from host C++.
+//
+// Replaces the reference's fixed-shape device stub SimEngine::execute_step
+// (sim_engine.cpp:33-72) with real work on an sm_100a GPU. Everything the
+// host decided during a step (allocations, copy-on-write, token writes,
+// committed view deltas, staging needs, far-view selections) is sealed into
+// ONE committed step descriptor in pinned host memory, published with one
+// cudaMemcpyAsync and consumed by a captured CUDA graph:
+//
+//   K-apply   zero recycled slots, copy-on-write pages          (arena)
+//   K-write   generate the step's token payloads into the arena and
+//             the per-slot window ring                          (arena, ring)
+//   K-far     far-view chunk summaries into summary slots       (arena)
+//   K-map     apply committed view edits to the device page table
+//   K-prime   fill window rows not covered by this step's writes
+//   K-scan    stage+reduce on device: descriptors and train boundaries
+//   K-gather  move each train's pages into the fixed-shape window
+//   K-attn    fixed-shape window attention for every slot
+//
+// The host never waits for a step before building the next one; it reads the
+// step's small record (counters, device time) one step later.
+#pragma once
+
+#include <cstdint>
+#include <memory>
+#include <span>
+#include <vector>
+
+#include "kvrail/payload_store.hpp"
+#include "kvrail/transport.hpp"
+#include "kvrail_c.h"
+
+namespace kvrail {
+
+struct DeviceStepStats {
+    uint64_t step = 0;
+    double device_ms = 0.0;     // CUDA-event time of the step's device work
+    uint32_t trains = 0;        // computed by K-scan
+    uint32_t descriptors = 0;
+    uint64_t train_bytes = 0;   // sum of train bytes (gather read side)
+    uint64_t writeback_tokens = 0;
+    uint64_t attn_bytes = 0;    // KV bytes the attention read
+    uint32_t scan_status = 0;   // 0 ok; else capacity overflow flags
+};
+
+class DeviceStep {
+public:
+    explicit DeviceStep(const kvr_geometry &geometry);
+    ~DeviceStep();
+    DeviceStep(const DeviceStep &) = delete;
+    DeviceStep &operator=(const DeviceStep &) = delete;
+
+    const kvr_geometry &geometry() const;
+    kvr_dev *handle() const;
+    /// Payload store over the device arena (give it to the Pager).
+    std::shared_ptr<PayloadStore> store();
+
+    /// Mirror session `sid`'s committed view into device slot `slot`.
+    void bind(SessionId sid, uint32_t slot);
+    void unbind(SessionId sid);
+
+    // ---- per-step inputs (cleared by launch) ----
+    void slot_state(uint32_t slot, SessionId sid, uint64_t written, bool live);
+    void need(uint32_t slot, SessionId sid, TrainKind kind, std::span<const StagedSpan> spans,
+              std::span<const uint64_t> first_tokens);
+    void prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end);
+    void far_selection(uint32_t slot, std::span<const uint64_t> chunk_ids);
+
+    /// Seal the step descriptor, publish it and launch the step (async).
+    void launch(uint64_t step, double now, const TransportConfig &tc);
+    /// Stats of `step` (blocks until that step has finished on the device).
+    DeviceStepStats collect(uint64_t step);
+    /// Wait for all launched work.
+    void sync();
+    /// Flush byte ops queued outside a step (Pager API use without a Driver).
+    void flush();
+
+    // ---- parity / inspection (synchronous) ----
+    void read_arena(uint64_t offset, uint64_t bytes, void *out);
+    void read_ring_token(uint32_t slot, uint64_t token, void *out); // token image (tb bytes)
+    void read_page_table(uint32_t slot, uint64_t tok_begin, uint64_t count, uint32_t *out);
+    void read_attention(uint32_t slot, float *out); // [L][Hq][hd]
+    void read_query(uint32_t slot, float *out);     // [L][Hq][hd]
+    void read_far_row(uint32_t slot, uint64_t chunk, void *out); // token image of a far row
+    /// Last K-scan result: trains (desc_begin/count index `descs`).
+    void read_scan(std::vector<kvr_train> &trains, std::vector<kvr_descriptor> &descs);
+
+    struct Impl; // public so the arena-backed PayloadStore can reach it
+
+private:
+    std::unique_ptr<Impl> impl_;
+};
+
+} // namespace kvrail

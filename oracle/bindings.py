@@ -1,0 +1,157 @@
+"""TEST INFRASTRUCTURE (CPU oracle) — never imported by the product path.
+
+ctypes bindings for the two oracles built by oracle/Makefile:
+  * _build/libkvr_oracle.so  — the plain-C restatement (kvr_oracle.h);
+  * _ref/libkvrail_ref.so    — the reference library compiled from its own
+    sources plus a C shim (ref_shim.cpp), symbols prefixed ``kvr_ref_``.
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / reference
+legs use this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import json
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "_build", "libkvr_oracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libkvrail_ref.so")
+
+_oracle = None
+_ref = None
+
+
+def oracle() -> C.CDLL:
+    global _oracle
+    if _oracle is None:
+        lib = C.CDLL(ORACLE_SO)
+        f = C.POINTER(C.c_float)
+        lib.kvo_splitmix64.argtypes = [C.c_uint64]
+        lib.kvo_splitmix64.restype = C.c_uint64
+        lib.kvo_fill_token_payload.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64,
+                                               C.c_uint32, C.c_void_p]
+        lib.kvo_fill_token_lanes.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
+                                             C.c_void_p]
+        lib.kvo_fill_query.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
+                                       C.c_uint32, C.c_int, f]
+        lib.kvo_summarize_chunk.argtypes = [f, C.c_uint32, C.c_uint64, f]
+        lib.kvo_select_chunks.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_uint32,
+                                          C.POINTER(C.c_uint64)]
+        lib.kvo_select_chunks.restype = C.c_uint64
+        lib.kvo_attend_rows.argtypes = [f, C.c_uint64, f, C.c_uint64, C.c_uint64, f, C.c_uint32, f]
+        lib.kvo_attend_window.argtypes = [C.c_void_p, C.c_uint64, f, C.c_uint64, C.c_uint32,
+                                          C.c_uint32, C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
+                                          f, f]
+        lib.kvo_fnv1a.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
+        lib.kvo_fnv1a.restype = C.c_uint64
+        lib.kvo_half_to_float.argtypes = [C.c_uint16]
+        lib.kvo_half_to_float.restype = C.c_float
+        lib.kvo_bf16_to_float.argtypes = [C.c_uint16]
+        lib.kvo_bf16_to_float.restype = C.c_float
+        _oracle = lib
+    return _oracle
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        lib = C.CDLL(REF_SO)
+        cp = C.POINTER(C.c_char_p)
+        lib.kvr_ref_scenario_run.argtypes = [C.c_char_p, C.c_int, cp, cp, cp, C.POINTER(C.c_double)]
+        lib.kvr_ref_scenario_events.argtypes = [C.c_char_p, cp]
+        lib.kvr_ref_free.argtypes = [C.c_char_p]
+        lib.kvr_ref_last_error.restype = C.c_char_p
+        _ref = lib
+    return _ref
+
+
+def ref_api():
+    """The reference pager/transport API bound through the product's Api class."""
+    from paper_2605_09735_b200.kvrail import Api
+    return Api(ref(), "kvr_ref_")
+
+
+def ref_scenario(config: dict, trace: bool = False):
+    """run_scenario of the reference: (steps_csv, report_json, trace, wall_seconds)."""
+    lib = ref()
+    csv, rep, tr = C.c_char_p(), C.c_char_p(), C.c_char_p()
+    wall = C.c_double()
+    rc = lib.kvr_ref_scenario_run(json.dumps(config).encode(), int(trace), C.byref(csv),
+                                  C.byref(rep), C.byref(tr), C.byref(wall))
+    if rc:
+        raise RuntimeError(lib.kvr_ref_last_error().decode())
+    return csv.value.decode(), rep.value.decode(), tr.value.decode(), wall.value
+
+
+# ---- helpers ---------------------------------------------------------------------
+def fill_query(seed, session, step, layer, head, head_dim, elem_kind):
+    out = (C.c_float * head_dim)()
+    oracle().kvo_fill_query(seed, session, step, layer, head, head_dim, elem_kind, out)
+    return list(out)
+
+
+def attend_window(window: bytes, n_near: int, layers: int, kv_heads: int, head_dim: int,
+                  elem_kind: int, layer: int, kv_head: int, query, far_images=None, n_far=0):
+    q = (C.c_float * head_dim)(*query)
+    out = (C.c_float * head_dim)()
+    far = (C.c_float * max(1, len(far_images or [])))(*(far_images or []))
+    oracle().kvo_attend_window(window, n_near, far, n_far, layers, kv_heads, head_dim, elem_kind,
+                               layer, kv_head, q, out)
+    return list(out)
+
+
+def rel_error(got, want) -> float:
+    """max |got - want| / max(|want|, 1e-2 * ||want||_inf) — the 1e-3 parity metric."""
+    scale = max(abs(x) for x in want) if want else 0.0
+    worst = 0.0
+    for g, w in zip(got, want):
+        den = max(abs(w), 1e-2 * scale, 1e-30)
+        worst = max(worst, abs(g - w) / den)
+    return worst
+
+
+def token_bytes_via_view(pager, view, token: int, tb: int) -> bytes:
+    for b, e, blk, sb in view["entries"]:
+        if b <= token < e:
+            return pager.read_slots(blk, sb + (token - b), 1)
+    raise KeyError(token)
+
+
+def check_driver_window_and_attention(driver, far_images_of=None) -> float:
+    """Window ring == arena for every live slot's near window; attention output
+    of the last step within tolerance of the double-precision oracle. Returns the
+    worst attention error (raises AssertionError on a byte mismatch)."""
+    dev = driver.device()
+    g = dev.geometry
+    pager = driver.pager()
+    tb = g.token_bytes
+    group = g.q_heads // g.kv_heads
+    done, _ = driver.progress()
+    step = done - 1
+    worst = 0.0
+    for slot, session, written in driver.live():
+        if pager.session_eos(session):
+            continue  # finished this step: its committed view is already empty
+        view = pager.active_view(session)
+        lo = max(0, written - g.near_window)
+        window = b""
+        for t in range(lo, written):
+            want = token_bytes_via_view(pager, view, t, tb)
+            got = dev.ring_token(slot, t)
+            assert got == want, f"window ring mismatch slot {slot} token {t}"
+            window += want
+        q_dev = dev.query(slot)
+        out = dev.attention(slot)
+        for layer in range(g.layers):
+            for qh in range(g.q_heads):
+                base = (layer * g.q_heads + qh) * g.head_dim
+                q = fill_query(g.seed, session, step, layer, qh, g.head_dim, g.elem_kind)
+                assert q == q_dev[base:base + g.head_dim], "device query differs from the oracle"
+                want = attend_window(window, written - lo, g.layers, g.kv_heads, g.head_dim,
+                                     g.elem_kind, layer, qh // group, q)
+                worst = max(worst, rel_error(out[base:base + g.head_dim], want))
+    return worst

@@ -1,0 +1,287 @@
+// kvrail-b200 byte-level step kernels (HBM-bound integer/byte work).
+//
+//   K-apply : zero recycled page slots, copy-on-write page copies, host blobs
+//   K-write : generate this step's token payloads (reference pattern) into the
+//             arena and the window ring; generate the decode queries
+//   K-far   : far-view chunk summaries (double accumulation, bit-exact)
+//   K-map   : committed view edits -> device page table
+//   K-prime : window rows not produced by this step's writes
+//
+// All loops are grid-stride with 16-byte vector accesses; grids are multiples
+// of the SM count and sized for the worst case so the step graph never changes.
+#include "kvr_internal.cuh"
+
+namespace kvr {
+
+namespace {
+
+__device__ inline void zero16(uint8_t *p) { *reinterpret_cast<int4 *>(p) = make_int4(0, 0, 0, 0); }
+
+// ---------------------------------------------------------------------------
+// K-apply: zero ops, then COW copies, then host blobs (three launches: a
+// recycled page may be a COW source in the same step).
+
+__global__ void k_zero(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_zero_op *ops = section<kvr_zero_op>(c, h->off_zero);
+    for (uint32_t i = blockIdx.x; i < h->n_zero; i += gridDim.x) {
+        const kvr_zero_op op = ops[i];
+        uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot_begin) * c.token_bytes;
+        const uint64_t n16 = uint64_t(op.slot_count) * c.token_bytes / 16;
+        for (uint64_t k = threadIdx.x; k < n16; k += blockDim.x)
+            zero16(dst + 16 * k);
+    }
+}
+
+__global__ void k_cow(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_cow_op *ops = section<kvr_cow_op>(c, h->off_cow);
+    for (uint32_t i = blockIdx.x; i < h->n_cow; i += gridDim.x) {
+        const int4 *src = reinterpret_cast<const int4 *>(c.arena + uint64_t(ops[i].src) * c.page_bytes);
+        int4 *dst = reinterpret_cast<int4 *>(c.arena + uint64_t(ops[i].dst) * c.page_bytes);
+        for (uint64_t k = threadIdx.x; k < c.page_bytes / 16; k += blockDim.x)
+            dst[k] = src[k];
+    }
+}
+
+__global__ void k_blob(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_blob_op *ops = section<kvr_blob_op>(c, h->off_blob_ops);
+    const uint8_t *blob = c.desc + h->off_blob;
+    for (uint32_t i = blockIdx.x; i < h->n_blob; i += gridDim.x) {
+        const kvr_blob_op op = ops[i];
+        uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot) * c.token_bytes;
+        const uint8_t *src = blob + op.blob_offset;
+        const uint64_t n = uint64_t(op.count) * c.token_bytes;
+        for (uint64_t k = threadIdx.x; k < n; k += blockDim.x)
+            dst[k] = src[k];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-write: one CTA per written token (grid-stride), 16 bytes per thread-step.
+
+template <int ESZ> struct Pack16;
+
+__device__ inline uint16_t f2h_bits(float v) { return __half_as_ushort(__float2half_rn(v)); }
+__device__ inline uint16_t f2b_bits(float v) { return __bfloat16_as_ushort(__float2bfloat16_rn(v)); }
+
+// 16 payload bytes starting at byte `b0` of token `tok` of session `sid`.
+__device__ inline int4 payload16(const DevCtx &c, uint32_t sid, uint64_t tok, uint64_t b0) {
+    const uint64_t base = c.seed ^ (uint64_t(sid) << 32) ^ (tok << 8);
+    uint32_t w[4];
+    if (c.esz == 4) { // float lanes (reference pattern for elem_bytes == 4)
+        const uint64_t lane0 = b0 / 4;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+            w[i] = __float_as_uint(lane_value(splitmix64(base ^ (lane0 + i))));
+    } else if (c.payload_mode == KVR_PAYLOAD_LANES) { // 2-byte lanes: pattern rounded
+        const uint64_t lane0 = b0 / 2;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const float a = lane_value(splitmix64(base ^ (lane0 + 2 * i)));
+            const float b = lane_value(splitmix64(base ^ (lane0 + 2 * i + 1)));
+            const uint32_t lo = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(a) : f2h_bits(a);
+            const uint32_t hi = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(b) : f2h_bits(b);
+            w[i] = lo | (hi << 16);
+        }
+    } else { // reference byte pattern: one splitmix per byte
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            uint32_t v = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                v |= uint32_t(splitmix64(base ^ (b0 + 4 * i + k)) & 0xff) << (8 * k);
+            w[i] = v;
+        }
+    }
+    return make_int4(int(w[0]), int(w[1]), int(w[2]), int(w[3]));
+}
+
+__global__ void __launch_bounds__(256) k_write(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint32_t n = h->n_write;
+    const uint64_t total = h->write_tokens;
+    const uint64_t chunks = c.token_bytes / 16;
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    for (uint64_t j = blockIdx.x; j < total; j += gridDim.x) {
+        // op holding token j: last op with prefix <= j (source-0 ops only carry prefixes)
+        uint32_t lo = 0, hi = n;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (ops[mid].prefix <= j)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const kvr_write_op op = ops[lo];
+        if (op.source != 0)
+            continue;
+        const uint64_t k = j - op.prefix;
+        const uint64_t tok = op.token + k;
+        uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + (op.slot + k) * c.token_bytes;
+        uint8_t *ring = nullptr;
+        if (op.dev_slot != KVR_NO_SLOT) {
+            const uint64_t w = slots[op.dev_slot].written;
+            if (tok < w && tok + c.W >= w) // inside the live window after this step
+                ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
+        }
+        for (uint64_t q = threadIdx.x; q < chunks; q += blockDim.x) {
+            const int4 v = payload16(c, op.session, tok, 16 * q);
+            *reinterpret_cast<int4 *>(dst + 16 * q) = v;
+            if (ring) {
+                const uint64_t byte = 16 * q;
+                const uint64_t l = byte / row_bytes, within = byte % row_bytes;
+                *reinterpret_cast<int4 *>(ring + l * uint64_t(c.R) * row_bytes + within) = v;
+            }
+        }
+    }
+}
+
+// Decode queries for live slots: [slot][L][Hq][hd], rounded to the KV element
+// type (kvo_fill_query in the oracle).
+__global__ void k_query(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint64_t per_slot = uint64_t(c.L) * c.Hq * c.hd;
+    const uint64_t total = per_slot * c.n_slots;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        const uint32_t s = uint32_t(i / per_slot);
+        if (!slots[s].live)
+            continue;
+        const uint64_t r = i % per_slot;
+        const uint32_t d = uint32_t(r % c.hd), head = uint32_t((r / c.hd) % c.Hq),
+                       l = uint32_t(r / (uint64_t(c.hd) * c.Hq));
+        const uint64_t hsh = splitmix64(c.seed ^ (0x51ull << 56) ^ (uint64_t(slots[s].session) << 32) ^
+                                        (h->step << 20) ^ (uint64_t(l) << 12) ^ (uint64_t(head) << 8) ^ d);
+        float v = lane_value(hsh);
+        if (c.elem_kind == KVR_ELEM_F16)
+            v = __half2float(__float2half_rn(v));
+        else if (c.elem_kind == KVR_ELEM_BF16)
+            v = __bfloat162float(__float2bfloat16_rn(v));
+        c.q[i] = v;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-far: summary of chunk [aux, aux + chunk_tokens) of a slot, one thread per
+// lane, double accumulation in token order, float(acc * (1/count)) (bit-exact
+// with far_view.cpp:36-46 for fp32 lanes; fp16/bf16 lanes round to nearest even).
+
+__device__ inline double load_lane(const DevCtx &c, const uint8_t *p, uint64_t lane) {
+    if (c.esz == 4)
+        return double(reinterpret_cast<const float *>(p)[lane]);
+    const uint16_t b = reinterpret_cast<const uint16_t *>(p)[lane];
+    return c.elem_kind == KVR_ELEM_BF16 ? double(__bfloat162float(__ushort_as_bfloat16(b)))
+                                        : double(__half2float(__ushort_as_half(b)));
+}
+
+__global__ void k_far(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write);
+    const uint64_t lanes = c.token_bytes / c.esz;
+    const uint64_t lane_blocks = (lanes + blockDim.x - 1) / blockDim.x;
+    const uint64_t work = uint64_t(h->n_write) * lane_blocks;
+    for (uint64_t u = blockIdx.x; u < work; u += gridDim.x) {
+        const kvr_write_op op = ops[u / lane_blocks];
+        if (op.source != 1)
+            continue;
+        const uint64_t lane = (u % lane_blocks) * blockDim.x + threadIdx.x;
+        if (lane >= lanes)
+            continue;
+        double acc = 0.0;
+        const uint32_t *tm = c.tmap + uint64_t(op.dev_slot) * c.max_tokens;
+        for (uint32_t k = 0; k < c.chunk_tokens; ++k) {
+            const uint64_t tok = op.aux + k;
+            const uint32_t gs = tok < c.max_tokens ? tm[tok] : kNoMap;
+            if (gs == kNoMap)
+                continue; // unmapped source: contributes zeros (host validated coverage)
+            acc += load_lane(c, c.arena + gslot_offset(c, gs), lane);
+        }
+        const float mean = float(acc * (1.0 / double(c.chunk_tokens)));
+        uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot) * c.token_bytes;
+        if (c.esz == 4)
+            reinterpret_cast<float *>(dst)[lane] = mean;
+        else
+            reinterpret_cast<uint16_t *>(dst)[lane] =
+                c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(mean) : f2h_bits(mean);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-map: committed view edits into the page table (token granularity, so
+// mid-block aliases and tail extensions need no special case).
+
+__global__ void k_map(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_edit_op *ops = section<kvr_edit_op>(c, h->off_edit);
+    for (uint32_t i = blockIdx.x; i < h->n_edit; i += gridDim.x) {
+        const kvr_edit_op e = ops[i];
+        if (e.slot >= c.n_slots)
+            continue;
+        const bool summary = e.tok_begin >= KVR_SUMMARY_BASE;
+        uint32_t *table = summary ? c.smap + uint64_t(e.slot) * c.smap_cap
+                                  : c.tmap + uint64_t(e.slot) * c.max_tokens;
+        const uint64_t base = summary ? KVR_SUMMARY_BASE : 0;
+        const uint64_t cap = summary ? c.smap_cap : c.max_tokens;
+        for (uint64_t t = e.tok_begin + threadIdx.x; t < e.tok_end; t += blockDim.x) {
+            const uint64_t idx = t - base;
+            if (idx >= cap)
+                break;
+            table[idx] = e.block == kNoMap ? kNoMap
+                                           : e.block * c.tpp + e.slot_begin + uint32_t(t - e.tok_begin);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-prime: ring rows for tokens of [tok_begin, tok_end) from the arena via the
+// (updated) page table; one CTA per (op, token).
+
+__global__ void k_prime(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_prime_op *ops = section<kvr_prime_op>(c, h->off_prime);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    for (uint32_t i = 0; i < h->n_prime; ++i) {
+        const kvr_prime_op op = ops[i];
+        const uint64_t w = slots[op.slot].written;
+        for (uint64_t tok = op.tok_begin + blockIdx.x; tok < op.tok_end; tok += gridDim.x) {
+            if (!(tok < w && tok + c.W >= w) || tok >= c.max_tokens)
+                continue;
+            const uint32_t gs = c.tmap[uint64_t(op.slot) * c.max_tokens + tok];
+            if (gs == kNoMap)
+                continue;
+            const uint8_t *src = c.arena + gslot_offset(c, gs);
+            uint8_t *ring = c.ring + ring_row(c, op.slot, 0, uint32_t(tok % c.R)) * c.esz;
+            for (uint64_t q = threadIdx.x; q < c.token_bytes / 16; q += blockDim.x) {
+                const uint64_t byte = 16 * q;
+                const uint64_t l = byte / row_bytes, within = byte % row_bytes;
+                *reinterpret_cast<int4 *>(ring + l * uint64_t(c.R) * row_bytes + within) =
+                    *reinterpret_cast<const int4 *>(src + byte);
+            }
+        }
+    }
+}
+
+} // namespace
+
+void launch_apply(const DevCtx &c, cudaStream_t s, int sms) {
+    k_zero<<<sms * 4, 256, 0, s>>>(c);
+    k_cow<<<sms * 4, 256, 0, s>>>(c);
+    k_blob<<<sms, 256, 0, s>>>(c);
+}
+
+void launch_write(const DevCtx &c, cudaStream_t s, int sms) {
+    k_write<<<sms * 8, 256, 0, s>>>(c);
+    k_query<<<sms * 2, 256, 0, s>>>(c);
+}
+
+void launch_far(const DevCtx &c, cudaStream_t s, int sms) { k_far<<<sms * 2, 256, 0, s>>>(c); }
+void launch_map(const DevCtx &c, cudaStream_t s, int sms) { k_map<<<sms * 2, 256, 0, s>>>(c); }
+void launch_prime(const DevCtx &c, cudaStream_t s, int sms) { k_prime<<<sms * 4, 256, 0, s>>>(c); }
+
+} // namespace kvr

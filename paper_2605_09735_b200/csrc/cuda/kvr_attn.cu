@@ -1,0 +1,405 @@
+// kvrail-b200 K-attn: fixed-shape window attention for every slot.
+//
+// Shape never changes: the grid covers (slot, layer, kv-head group) work items
+// for all n_slots slots; a slot's visible set is its last min(written, W*)
+// tokens (window ring) plus its selected far summaries, everything else is
+// masked. Definition: attend() of far_view.cpp:113-155 per (layer, q-head)
+// with GQA q-head j -> kv-head j / group, fp32 accumulation (1e-3 rel. bound).
+//
+// Per CTA: one producer warp streams 32-token x G-head K and V tiles out of the
+// ring with 4-D TMA tensor loads (cp.async.bulk.tensor, mbarrier completion)
+// into a multi-stage shared-memory ring; G consumer warps (one per kv head)
+// compute. QK^T: lane <-> token, each lane walks the head dimension with a
+// lane-rotated column order (bank-conflict free on the unpadded TMA tile) and
+// reuses every K element for all `group` q-heads. PV: lane <-> output dims,
+// probabilities broadcast by shuffles. Online softmax in base 2. Decode
+// attention with g <= 8 is far below the tensor-core ridge (g flop/byte), so
+// this is a warp GEMV; a tcgen05 path for large GQA groups is DESIGN.md §6.
+#include <algorithm>
+#include <cstdio>
+#include <cudaTypedefs.h>
+
+#include "kvr_internal.cuh"
+
+namespace kvr {
+
+namespace {
+
+constexpr int kTile = 32; // tokens per tile (one per lane)
+constexpr int kMaxG = 4;  // kv heads per CTA (one consumer warp each)
+
+__device__ inline uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ inline void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ inline void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ inline void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ inline void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "W_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W_%=;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(parity)
+                 : "memory");
+}
+__device__ inline void tma_load_4d(void *dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                   uint64_t *bar) {
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(smem_u32(dst)),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+                 : "memory");
+}
+
+template <typename T> struct Pair;
+template <> struct Pair<__half> {
+    using V = __half2;
+    static __device__ float2 f2(uint32_t u) { return __half22float2(*reinterpret_cast<const __half2 *>(&u)); }
+    static __device__ uint32_t pack(float a, float b) {
+        __half2 h = __floats2half2_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+};
+template <> struct Pair<__nv_bfloat16> {
+    static __device__ float2 f2(uint32_t u) {
+        return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u));
+    }
+    static __device__ uint32_t pack(float a, float b) {
+        __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        return *reinterpret_cast<uint32_t *>(&h);
+    }
+};
+
+// Element-pair access for the three element types (fp32 pairs are 8 bytes).
+template <typename T> __device__ inline float2 load_pair(const T *p) {
+    return Pair<T>::f2(*reinterpret_cast<const uint32_t *>(p));
+}
+template <> __device__ inline float2 load_pair<float>(const float *p) {
+    return *reinterpret_cast<const float2 *>(p);
+}
+
+__device__ inline float warp_max(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ inline float warp_sum(float v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1)
+        v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+template <typename T, int HD, int QG> struct Acc {
+    static constexpr int DPL = HD / 32; // output dims per lane
+    float m[QG], lsum[QG], acc[QG][DPL];
+    __device__ void init() {
+#pragma unroll
+        for (int q = 0; q < QG; ++q) {
+            m[q] = -INFINITY;
+            lsum[q] = 0.f;
+#pragma unroll
+            for (int k = 0; k < DPL; ++k)
+                acc[q][k] = 0.f;
+        }
+    }
+    // One 32-row block: lane r scores row r (krow, nullptr when masked) and the
+    // warp then accumulates rows' V (vrow of row r fetched via shuffle).
+    __device__ void block(const T *krow, const T *vrow_lane, bool valid, const T *qs, float scale_log2) {
+        const int lane = threadIdx.x & 31;
+        float s[QG];
+#pragma unroll
+        for (int q = 0; q < QG; ++q)
+            s[q] = 0.f;
+        if (valid) {
+            float s2[QG];
+#pragma unroll
+            for (int q = 0; q < QG; ++q)
+                s2[q] = 0.f;
+#pragma unroll 8
+            for (int cc = 0; cc < HD / 2; ++cc) {
+                const int d = 2 * ((cc + lane) & (HD / 2 - 1)); // rotated: conflict-free banks
+                const float2 k = load_pair<T>(krow + d);
+#pragma unroll
+                for (int q = 0; q < QG; ++q) {
+                    const float2 qq = load_pair<T>(qs + q * HD + d);
+                    s[q] = fmaf(k.x, qq.x, s[q]);
+                    s2[q] = fmaf(k.y, qq.y, s2[q]);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < QG; ++q)
+                s[q] = (s[q] + s2[q]) * scale_log2;
+        }
+        float p[QG];
+#pragma unroll
+        for (int q = 0; q < QG; ++q) {
+            const float sv = valid ? s[q] : -INFINITY;
+            const float mt = warp_max(sv);
+            const float mn = fmaxf(m[q], mt);
+            const float alpha = mn == -INFINITY ? 1.f : exp2f(m[q] - mn);
+            p[q] = valid ? exp2f(sv - mn) : 0.f;
+            lsum[q] = lsum[q] * alpha + p[q];
+            m[q] = mn;
+#pragma unroll
+            for (int k = 0; k < DPL; ++k)
+                acc[q][k] *= alpha;
+        }
+        const uint64_t vaddr = reinterpret_cast<uint64_t>(vrow_lane);
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+            const T *vr = reinterpret_cast<const T *>(__shfl_sync(0xffffffffu, vaddr, r));
+            if (!vr) // masked row (warp-uniform)
+                continue;
+            float v[DPL];
+#pragma unroll
+            for (int k = 0; k < DPL; k += 2) {
+                if constexpr (DPL == 1) {
+                    v[0] = float(vr[lane]);
+                } else {
+                    const float2 x = load_pair<T>(vr + DPL * lane + k);
+                    v[k] = x.x;
+                    v[k + 1] = x.y;
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < QG; ++q) {
+                const float pr = __shfl_sync(0xffffffffu, p[q], r);
+#pragma unroll
+                for (int k = 0; k < DPL; ++k)
+                    acc[q][k] = fmaf(pr, v[k], acc[q][k]);
+            }
+        }
+    }
+};
+
+template <typename T, int HD, int QG>
+__global__ void __launch_bounds__(32 * (kMaxG + 1), 1)
+    k_attn(DevCtx c, const __grid_constant__ CUtensorMap ring_map, uint32_t G, uint32_t stages) {
+    extern __shared__ __align__(128) uint8_t smem[];
+    const uint32_t tile_elems = kTile * G * HD;
+    T *tiles = reinterpret_cast<T *>(smem);                       // [stages][K|V][32][G][HD]
+    T *qsm = tiles + size_t(stages) * 2 * tile_elems;             // [kMaxG][QG][HD]
+    uint64_t *full = reinterpret_cast<uint64_t *>(qsm + kMaxG * QG * HD);
+    uint64_t *empty = full + stages;
+
+    const kvr_step_header *h = hdr(c);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint32_t *far_ids = section<uint32_t>(c, h->off_far_ids);
+    const uint32_t groups = c.Hkv / G;
+    const uint32_t n_items = c.n_slots * c.L * groups;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (uint32_t s = 0; s < stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], G);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    auto window = [&](uint32_t slot, uint64_t &lo, uint64_t &t0, uint32_t &n_tiles) {
+        const uint64_t w = slots[slot].written;
+        lo = w > c.W ? w - c.W : 0;
+        t0 = lo & ~uint64_t(kTile - 1);
+        n_tiles = w > t0 ? uint32_t((w - t0 + kTile - 1) / kTile) : 0;
+    };
+
+    if (warp == kMaxG) { // ---------------- producer ----------------
+        if (lane != 0)
+            return;
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
+        uint32_t s = 0, phase = 0;
+        const uint32_t bytes = 2 * tile_elems * sizeof(T);
+        for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+            const uint32_t hg = it % groups, l = (it / groups) % c.L, slot = it / (groups * c.L);
+            if (!slots[slot].live)
+                continue;
+            uint64_t lo, t0;
+            uint32_t n_tiles;
+            window(slot, lo, t0, n_tiles);
+            for (uint32_t k = 0; k < n_tiles; ++k) {
+                mbar_wait(&empty[s], phase ^ 1);
+                const int row0 = int((t0 + uint64_t(k) * kTile) % c.R);
+                T *kt = tiles + size_t(s) * 2 * tile_elems;
+                mbar_expect_tx(&full[s], bytes);
+                tma_load_4d(kt, &ring_map, 0, int(hg * G), row0, int(slot * c.L + l), &full[s]);
+                tma_load_4d(kt + tile_elems, &ring_map, 0, int(c.Hkv + hg * G), row0, int(slot * c.L + l),
+                            &full[s]);
+                if (++s == stages) {
+                    s = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+        return;
+    }
+    if (uint32_t(warp) >= G)
+        return;
+
+    // ---------------- consumers: warp `warp` owns kv head hg*G + warp ----------------
+    const float scale_log2 = 1.4426950408889634f / sqrtf(float(HD));
+    T *qs = qsm + warp * QG * HD;
+    uint32_t s = 0, phase = 0;
+    for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+        const uint32_t hg = it % groups, l = (it / groups) % c.L, slot = it / (groups * c.L);
+        const kvr_slot_state st = slots[slot];
+        if (!st.live)
+            continue;
+        const uint32_t kvh = hg * G + warp;
+        uint64_t lo, t0;
+        uint32_t n_tiles;
+        window(slot, lo, t0, n_tiles);
+        const uint64_t w = st.written;
+        // queries of this kv head's group, rounded to T (exact: they were rounded already)
+        const float *qg = c.q + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD;
+        for (int i = lane; i < QG * HD / 2; i += 32) {
+            const float a = qg[2 * i], b = qg[2 * i + 1];
+            if constexpr (sizeof(T) == 4) {
+                reinterpret_cast<float2 *>(qs)[i] = make_float2(a, b);
+            } else {
+                reinterpret_cast<uint32_t *>(qs)[i] = Pair<T>::pack(a, b);
+            }
+        }
+        __syncwarp();
+        Acc<T, HD, QG> acc;
+        acc.init();
+        // far summaries (few rows; read straight from global)
+        const T *far_base = reinterpret_cast<const T *>(c.far) +
+                            (uint64_t(slot) * c.L + l) * c.max_chunks * c.row_elems + uint64_t(kvh) * HD;
+        for (uint32_t f0 = 0; f0 < st.far_count; f0 += 32) {
+            const bool valid = f0 + lane < st.far_count;
+            const T *krow = nullptr, *vrow = nullptr;
+            if (valid) {
+                krow = far_base + uint64_t(far_ids[st.far_begin + f0 + lane]) * c.row_elems;
+                vrow = krow + c.d_kv;
+            }
+            acc.block(krow, vrow, valid, qs, scale_log2);
+        }
+        // near window tiles from the TMA pipeline
+        for (uint32_t k = 0; k < n_tiles; ++k) {
+            mbar_wait(&full[s], phase);
+            const T *kt = tiles + size_t(s) * 2 * tile_elems;
+            const uint64_t tok = t0 + uint64_t(k) * kTile + lane;
+            const bool valid = tok >= lo && tok < w;
+            const T *krow = kt + (size_t(lane) * G + warp) * HD;
+            acc.block(krow, valid ? krow + tile_elems : nullptr, valid, qs, scale_log2);
+            __syncwarp();
+            if (lane == 0)
+                mbar_arrive(&empty[s]);
+            if (++s == stages) {
+                s = 0;
+                phase ^= 1;
+            }
+        }
+        // finalize
+        float *o = c.out + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD;
+#pragma unroll
+        for (int q = 0; q < QG; ++q) {
+            const float z = warp_sum(acc.lsum[q]);
+            const float inv = z > 0.f ? 1.f / z : 0.f;
+#pragma unroll
+            for (int k = 0; k < Acc<T, HD, QG>::DPL; ++k)
+                o[q * HD + Acc<T, HD, QG>::DPL * lane + k] = acc.acc[q][k] * inv;
+        }
+        __syncwarp();
+    }
+}
+
+using AttnFn = void (*)(DevCtx, const CUtensorMap, uint32_t, uint32_t);
+
+template <typename T, int HD> AttnFn pick_group(uint32_t g) {
+    switch (g) {
+    case 1: return k_attn<T, HD, 1>;
+    case 2: return k_attn<T, HD, 2>;
+    case 4: return k_attn<T, HD, 4>;
+    case 8: return k_attn<T, HD, 8>;
+    default: return nullptr;
+    }
+}
+template <typename T> AttnFn pick_hd(uint32_t hd, uint32_t g) {
+    switch (hd) {
+    case 32: return pick_group<T, 32>(g);
+    case 64: return pick_group<T, 64>(g);
+    case 128: return pick_group<T, 128>(g);
+    default: return nullptr;
+    }
+}
+
+} // namespace
+
+struct AttnPlan {
+    AttnFn fn = nullptr;
+    CUtensorMap map{};
+    uint32_t G = 1, stages = 2, grid = 1;
+    size_t smem = 0;
+    char name[96] = {0};
+};
+
+AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device) {
+    auto *p = new AttnPlan();
+    switch (c.elem_kind) {
+    case KVR_ELEM_F16: p->fn = pick_hd<__half>(c.hd, c.group); break;
+    case KVR_ELEM_BF16: p->fn = pick_hd<__nv_bfloat16>(c.hd, c.group); break;
+    default: p->fn = pick_hd<float>(c.hd, c.group); break;
+    }
+    if (!p->fn) {
+        delete p;
+        return nullptr;
+    }
+    // kv heads per CTA: largest G <= 4 dividing Hkv with a <= 64 KiB stage
+    const size_t row = size_t(c.hd) * c.esz;
+    for (uint32_t g : {4u, 2u, 1u})
+        if (c.Hkv % g == 0 && 2 * kTile * g * row <= (64u << 10)) {
+            p->G = g;
+            break;
+        }
+    const size_t stage = 2 * kTile * p->G * row;
+    p->stages = stage * 3 <= (200u << 10) ? 3 : 2;
+    p->smem = p->stages * stage + size_t(kMaxG) * c.group * c.hd * c.esz + 2 * p->stages * 8 + 16;
+    p->grid = uint32_t(sms);
+    cudaFuncSetAttribute(p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem));
+
+    // 4-D view of the ring: (head_dim, 2*Hkv heads, R rows, L*n_slots)
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void **>(&encode),
+                            cudaEnableDefault, &q);
+    if (!encode) {
+        delete p;
+        return nullptr;
+    }
+    const cuuint64_t dims[4] = {c.hd, 2ull * c.Hkv, c.R, uint64_t(c.L) * c.n_slots};
+    const cuuint64_t strides[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
+    const cuuint32_t box[4] = {c.hd, p->G, uint32_t(kTile), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    const CUtensorMapDataType dt =
+        c.esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
+    const CUresult r = encode(&p->map, dt, 4, c.ring, dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        delete p;
+        return nullptr;
+    }
+    std::snprintf(p->name, sizeof(p->name), "k_attn<%s,hd%u,g%u> G=%u stages=%u",
+                  c.elem_kind == KVR_ELEM_F16 ? "f16" : c.elem_kind == KVR_ELEM_BF16 ? "bf16" : "f32",
+                  c.hd, c.group, p->G, p->stages);
+    (void)device;
+    return p;
+}
+
+void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s) {
+    p->fn<<<p->grid, 32 * (kMaxG + 1), p->smem, s>>>(c, p->map, p->G, p->stages);
+}
+
+void free_attn_plan(AttnPlan *p) { delete p; }
+const char *attn_variant(const AttnPlan *p) { return p ? p->name : "none"; }
+
+} // namespace kvr

@@ -1,0 +1,420 @@
+// kvrail-b200 device context: HBM layout, step publication and graph replay.
+// Implements include/kvr_cuda.h.
+//
+// HBM layout (per GPU):
+//   arena  arena_pages x page_bytes        token-major pages, identical to the
+//                                          reference layout (pager.cpp:705)
+//   ring   [slot][layer][R][2*d_kv]        the fixed-shape window; layer-major so
+//                                          one (slot, layer) window is contiguous
+//   tmap   [slot][max_tokens] u32          device page table: token -> block*tpp+slot
+//   smap   [slot][max_chunks+tpp] u32      summary-slot page table
+//   far    [slot][layer][max_chunks][2*d_kv] far-view summary rows
+//   q/out  [slot][layer][q_head][head_dim] f32
+//   desc   3 x max_desc_bytes               step descriptors (2 ring slots + apply-only)
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <vector>
+#include <stdexcept>
+#include <string>
+
+#include "kvr_internal.cuh"
+
+namespace kvr {
+size_t scan_dynamic_smem(uint32_t cap);
+void prepare_scan(uint32_t cap);
+void prepare_gather(const DevCtx &c);
+} // namespace kvr
+
+using namespace kvr;
+
+struct kvr_dev {
+    kvr_geometry g{};
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+    DevCtx base{};
+    uint8_t *d_desc[3] = {nullptr, nullptr, nullptr};
+    void *h_desc[3] = {nullptr, nullptr, nullptr};
+    ScanCounters *h_scan[2] = {nullptr, nullptr};
+    cudaEvent_t ev_start[2] = {}, ev_stop[2] = {}, ev_attn[2] = {};
+    cudaGraphExec_t graph[2] = {nullptr, nullptr};
+    AttnPlan *attn = nullptr;
+    uint64_t launched[2] = {0, 0};
+    bool in_flight[2] = {false, false};
+    uint64_t pending_write_tokens[2] = {0, 0};
+    std::vector<void *> allocs;
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+struct CudaFail : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+
+void ck(cudaError_t e, const char *what) {
+    if (e != cudaSuccess)
+        throw CudaFail(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+template <typename Fn> int guard(Fn &&fn) {
+    try {
+        fn();
+        return KVR_OK;
+    } catch (const CudaFail &e) {
+        g_err = e.what();
+        return KVR_E_CUDA;
+    } catch (const std::exception &e) {
+        g_err = e.what();
+        return KVR_E_BAD_CONFIG;
+    }
+}
+
+void *dalloc(kvr_dev *d, size_t bytes, const char *what) {
+    void *p = nullptr;
+    ck(cudaMalloc(&p, bytes ? bytes : 16), what);
+    d->allocs.push_back(p);
+    return p;
+}
+
+DevCtx ctx_for(const kvr_dev *d, int slot) {
+    DevCtx c = d->base;
+    c.desc = d->d_desc[slot];
+    return c;
+}
+
+void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step) {
+    cudaStream_t s = d->stream;
+    launch_apply(c, s, d->sms);
+    launch_write(c, s, d->sms);
+    launch_far(c, s, d->sms);
+    launch_map(c, s, d->sms);
+    launch_prime(c, s, d->sms);
+    if (!full_step)
+        return;
+    launch_scan(c, s);
+    launch_gather(c, s, d->sms);
+    if (d->g.attention && d->attn)
+        launch_attn(d->attn, c, s);
+}
+
+} // namespace
+
+extern "C" {
+
+const char *kvr_dev_last_error(void) { return g_err.c_str(); }
+
+int kvr_dev_count(int *out) {
+    return guard([&] {
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess)
+            n = 0;
+        *out = n;
+    });
+}
+
+int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
+    auto d = std::make_unique<kvr_dev>();
+    const int rc = guard([&] {
+        kvr_geometry g = *geo;
+        if (g.token_bytes % 16 || (2ull * g.kv_heads * g.head_dim * g.elem_bytes) % 16)
+            throw std::runtime_error("token and layer rows must be multiples of 16 bytes");
+        if (g.kv_heads == 0 || g.q_heads % g.kv_heads)
+            throw std::runtime_error("q_heads must be a multiple of kv_heads");
+        if (g.ring_rows % 32 || g.ring_rows < g.near_window)
+            throw std::runtime_error("ring_rows must be a multiple of 32 and >= W*");
+        if (!g.max_desc_bytes)
+            g.max_desc_bytes = 16ull << 20;
+        if (!g.max_scan_descs)
+            g.max_scan_descs = 2048;
+        if (!g.max_trains)
+            g.max_trains = 2048;
+        if (g.max_scan_descs & (g.max_scan_descs - 1))
+            throw std::runtime_error("max_scan_descs must be a power of two");
+        d->g = g;
+        ck(cudaSetDevice(g.device), "cudaSetDevice");
+        cudaDeviceProp prop;
+        ck(cudaGetDeviceProperties(&prop, g.device), "cudaGetDeviceProperties");
+        d->sms = prop.multiProcessorCount;
+        ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
+        for (int i = 0; i < 2; ++i) {
+            ck(cudaEventCreate(&d->ev_start[i]), "event");
+            ck(cudaEventCreate(&d->ev_stop[i]), "event");
+            ck(cudaEventCreate(&d->ev_attn[i]), "event");
+        }
+        DevCtx &c = d->base;
+        c.page_bytes = g.page_bytes;
+        c.token_bytes = g.token_bytes;
+        c.max_tokens = g.max_tokens;
+        c.seed = g.seed;
+        c.tpp = g.tokens_per_page;
+        c.arena_pages = g.arena_pages;
+        c.L = g.layers;
+        c.Hkv = g.kv_heads;
+        c.hd = g.head_dim;
+        c.Hq = g.q_heads;
+        c.group = g.q_heads / g.kv_heads;
+        c.d_kv = g.kv_heads * g.head_dim;
+        c.row_elems = 2 * c.d_kv;
+        c.esz = g.elem_bytes;
+        c.elem_kind = uint32_t(g.elem_kind);
+        c.payload_mode = g.payload_mode;
+        c.n_slots = g.n_slots;
+        c.W = g.near_window;
+        c.R = g.ring_rows;
+        c.far_cap = g.far_cap;
+        c.chunk_tokens = g.chunk_tokens;
+        c.max_chunks = g.max_chunks ? g.max_chunks : 1;
+        c.smap_cap = c.max_chunks + g.tokens_per_page;
+        c.max_scan = g.max_scan_descs;
+        c.max_trains = g.max_trains;
+        if (uint64_t(c.L) * c.d_kv * 2 * c.esz != g.token_bytes)
+            throw std::runtime_error("token_bytes != 2 * layers * kv_heads * head_dim * elem_bytes");
+
+        const uint64_t arena_bytes = uint64_t(g.arena_pages) * g.page_bytes;
+        c.arena = static_cast<uint8_t *>(dalloc(d.get(), arena_bytes, "arena"));
+        ck(cudaMemsetAsync(c.arena, 0, arena_bytes, d->stream), "arena zero");
+        const uint64_t ring_elems = uint64_t(c.n_slots) * c.L * c.R * c.row_elems;
+        c.ring = static_cast<uint8_t *>(dalloc(d.get(), ring_elems * c.esz, "ring"));
+        ck(cudaMemsetAsync(c.ring, 0, ring_elems * c.esz, d->stream), "ring zero");
+        const uint64_t tmap_n = uint64_t(c.n_slots) * c.max_tokens;
+        c.tmap = static_cast<uint32_t *>(dalloc(d.get(), tmap_n * 4, "tmap"));
+        ck(cudaMemsetAsync(c.tmap, 0xff, tmap_n * 4, d->stream), "tmap init");
+        const uint64_t smap_n = uint64_t(c.n_slots) * c.smap_cap;
+        c.smap = static_cast<uint32_t *>(dalloc(d.get(), smap_n * 4, "smap"));
+        ck(cudaMemsetAsync(c.smap, 0xff, smap_n * 4, d->stream), "smap init");
+        const uint64_t far_elems = uint64_t(c.n_slots) * c.L * c.max_chunks * c.row_elems;
+        c.far = static_cast<uint8_t *>(dalloc(d.get(), far_elems * c.esz, "far"));
+        ck(cudaMemsetAsync(c.far, 0, far_elems * c.esz, d->stream), "far zero");
+        const uint64_t qn = uint64_t(c.n_slots) * c.L * c.Hq * c.hd;
+        c.q = static_cast<float *>(dalloc(d.get(), qn * 4, "q"));
+        c.out = static_cast<float *>(dalloc(d.get(), qn * 4, "out"));
+        ck(cudaMemsetAsync(c.q, 0, qn * 4, d->stream), "q zero");
+        ck(cudaMemsetAsync(c.out, 0, qn * 4, d->stream), "out zero");
+        c.trains = static_cast<kvr_train *>(dalloc(d.get(), sizeof(kvr_train) * c.max_trains, "trains"));
+        c.descs = static_cast<kvr_descriptor *>(dalloc(d.get(), sizeof(kvr_descriptor) * c.max_scan, "descs"));
+        c.gspans = static_cast<GSpan *>(dalloc(d.get(), sizeof(GSpan) * c.max_scan, "gspans"));
+        c.scan = static_cast<ScanCounters *>(dalloc(d.get(), sizeof(ScanCounters), "scan"));
+        ck(cudaMemsetAsync(c.scan, 0, sizeof(ScanCounters), d->stream), "scan zero");
+        for (int i = 0; i < 3; ++i) {
+            d->d_desc[i] = static_cast<uint8_t *>(dalloc(d.get(), g.max_desc_bytes, "desc"));
+            ck(cudaMallocHost(&d->h_desc[i], g.max_desc_bytes), "pinned desc");
+            std::memset(d->h_desc[i], 0, sizeof(kvr_step_header));
+        }
+        for (int i = 0; i < 2; ++i) {
+            void *p;
+            ck(cudaMallocHost(&p, sizeof(ScanCounters)), "pinned stats");
+            d->h_scan[i] = static_cast<ScanCounters *>(p);
+        }
+        prepare_scan(c.max_scan);
+        prepare_gather(c);
+        if (g.attention) {
+            d->attn = make_attn_plan(c, d->sms, g.device);
+            if (!d->attn)
+                throw std::runtime_error("no attention kernel for this head_dim/group/dtype");
+        }
+        ck(cudaStreamSynchronize(d->stream), "open sync");
+    });
+    if (rc != KVR_OK) {
+        kvr_dev_close(d.release());
+        return rc;
+    }
+    *out = d.release();
+    return KVR_OK;
+}
+
+int kvr_dev_close(kvr_dev *d) {
+    if (!d)
+        return KVR_OK;
+    if (d->stream)
+        cudaStreamSynchronize(d->stream);
+    for (int i = 0; i < 2; ++i) {
+        if (d->graph[i])
+            cudaGraphExecDestroy(d->graph[i]);
+        if (d->ev_start[i])
+            cudaEventDestroy(d->ev_start[i]);
+        if (d->ev_stop[i])
+            cudaEventDestroy(d->ev_stop[i]);
+        if (d->ev_attn[i])
+            cudaEventDestroy(d->ev_attn[i]);
+        if (d->h_scan[i])
+            cudaFreeHost(d->h_scan[i]);
+    }
+    for (int i = 0; i < 3; ++i)
+        if (d->h_desc[i])
+            cudaFreeHost(d->h_desc[i]);
+    for (void *p : d->allocs)
+        cudaFree(p);
+    if (d->attn)
+        free_attn_plan(d->attn);
+    if (d->stream)
+        cudaStreamDestroy(d->stream);
+    delete d;
+    return KVR_OK;
+}
+
+int kvr_dev_desc_buffer(kvr_dev *d, uint32_t ring_slot, void **out) {
+    return guard([&] {
+        if (ring_slot > 2)
+            throw std::runtime_error("ring slot out of range");
+        *out = d->h_desc[ring_slot];
+    });
+}
+
+int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
+    return guard([&] {
+        if (k > 1)
+            throw std::runtime_error("step ring slot must be 0 or 1");
+        if (desc_bytes > d->g.max_desc_bytes)
+            throw std::runtime_error("step descriptor exceeds max_desc_bytes");
+        const auto *h = static_cast<const kvr_step_header *>(d->h_desc[k]);
+        const DevCtx c = ctx_for(d, int(k));
+        ck(cudaEventRecord(d->ev_start[k], d->stream), "event");
+        ck(cudaMemcpyAsync(d->d_desc[k], d->h_desc[k], desc_bytes, cudaMemcpyHostToDevice, d->stream),
+           "descriptor H2D");
+        if (d->g.use_graph) {
+            if (!d->graph[k]) {
+                cudaGraph_t graph;
+                ck(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal), "capture");
+                run_step_kernels(d, c, true);
+                ck(cudaStreamEndCapture(d->stream, &graph), "capture end");
+                ck(cudaGraphInstantiate(&d->graph[k], graph, 0), "graph instantiate");
+                cudaGraphDestroy(graph);
+            }
+            ck(cudaGraphLaunch(d->graph[k], d->stream), "graph launch");
+        } else {
+            run_step_kernels(d, c, true);
+            ck(cudaGetLastError(), "step launch");
+        }
+        ck(cudaMemcpyAsync(d->h_scan[k], c.scan, sizeof(ScanCounters), cudaMemcpyDeviceToHost, d->stream),
+           "stats D2H");
+        ck(cudaEventRecord(d->ev_stop[k], d->stream), "event");
+        d->launched[k] = h->step;
+        d->in_flight[k] = true;
+        d->pending_write_tokens[k] = h->write_tokens;
+    });
+}
+
+int kvr_dev_apply_only(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
+    return guard([&] {
+        if (desc_bytes > d->g.max_desc_bytes)
+            throw std::runtime_error("descriptor exceeds max_desc_bytes");
+        DevCtx c = d->base;
+        c.desc = d->d_desc[2];
+        ck(cudaMemcpyAsync(d->d_desc[2], d->h_desc[2], desc_bytes, cudaMemcpyHostToDevice, d->stream),
+           "apply H2D");
+        run_step_kernels(d, c, false);
+        ck(cudaGetLastError(), "apply launch");
+        ck(cudaStreamSynchronize(d->stream), "apply sync");
+        (void)k;
+    });
+}
+
+int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
+    return guard([&] {
+        if (k > 1)
+            throw std::runtime_error("step ring slot must be 0 or 1");
+        std::memset(out, 0, sizeof(*out));
+        if (!d->in_flight[k])
+            return;
+        ck(cudaEventSynchronize(d->ev_stop[k]), "step wait");
+        float ms = 0.f;
+        ck(cudaEventElapsedTime(&ms, d->ev_start[k], d->ev_stop[k]), "elapsed");
+        const ScanCounters &sc = *d->h_scan[k];
+        out->step = d->launched[k];
+        out->device_ms = ms;
+        out->trains = sc.trains;
+        out->descriptors = sc.descriptors;
+        out->spans = sc.spans;
+        out->status = sc.status;
+        out->train_bytes = sc.train_bytes;
+        out->staged_tokens = sc.total_tokens;
+        out->writeback_tokens = d->pending_write_tokens[k];
+        d->in_flight[k] = false;
+    });
+}
+
+int kvr_dev_sync(kvr_dev *d) {
+    return guard([&] { ck(cudaStreamSynchronize(d->stream), "sync"); });
+}
+
+int kvr_dev_buffer_bytes(kvr_dev *d, int buffer, uint64_t *out) {
+    return guard([&] {
+        const DevCtx &c = d->base;
+        switch (buffer) {
+        case KVR_BUF_ARENA: *out = uint64_t(c.arena_pages) * c.page_bytes; break;
+        case KVR_BUF_RING: *out = uint64_t(c.n_slots) * c.L * c.R * c.row_elems * c.esz; break;
+        case KVR_BUF_TMAP: *out = uint64_t(c.n_slots) * c.max_tokens * 4; break;
+        case KVR_BUF_OUT:
+        case KVR_BUF_QUERY: *out = uint64_t(c.n_slots) * c.L * c.Hq * c.hd * 4; break;
+        case KVR_BUF_FAR: *out = uint64_t(c.n_slots) * c.L * c.max_chunks * c.row_elems * c.esz; break;
+        case KVR_BUF_TRAINS: *out = sizeof(kvr_train) * c.max_trains; break;
+        case KVR_BUF_DESCS: *out = sizeof(kvr_descriptor) * c.max_scan; break;
+        case KVR_BUF_SCAN: *out = sizeof(ScanCounters); break;
+        case KVR_BUF_SMAP: *out = uint64_t(c.n_slots) * c.smap_cap * 4; break;
+        default: throw std::runtime_error("unknown buffer");
+        }
+    });
+}
+
+int kvr_dev_read(kvr_dev *d, int buffer, uint64_t offset, uint64_t bytes, void *out) {
+    return guard([&] {
+        uint64_t size = 0;
+        if (kvr_dev_buffer_bytes(d, buffer, &size) != KVR_OK)
+            throw std::runtime_error("unknown buffer");
+        if (offset + bytes > size)
+            throw std::runtime_error("read past the end of the buffer");
+        const DevCtx &c = d->base;
+        const void *base = nullptr;
+        switch (buffer) {
+        case KVR_BUF_ARENA: base = c.arena; break;
+        case KVR_BUF_RING: base = c.ring; break;
+        case KVR_BUF_TMAP: base = c.tmap; break;
+        case KVR_BUF_OUT: base = c.out; break;
+        case KVR_BUF_QUERY: base = c.q; break;
+        case KVR_BUF_FAR: base = c.far; break;
+        case KVR_BUF_TRAINS: base = c.trains; break;
+        case KVR_BUF_DESCS: base = c.descs; break;
+        case KVR_BUF_SCAN: base = c.scan; break;
+        case KVR_BUF_SMAP: base = c.smap; break;
+        }
+        ck(cudaStreamSynchronize(d->stream), "read sync");
+        ck(cudaMemcpy(out, static_cast<const uint8_t *>(base) + offset, bytes, cudaMemcpyDeviceToHost),
+           "read D2H");
+    });
+}
+
+static int time_kernel(kvr_dev *d, uint32_t iters, double *ms, bool attn) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(d->stream), "sync");
+        // the last launched step's descriptor is still resident in its slot
+        const int k = d->launched[1] > d->launched[0] ? 1 : 0;
+        const DevCtx c = ctx_for(d, k);
+        if (attn && !d->attn)
+            throw std::runtime_error("attention disabled");
+        auto once = [&] {
+            if (attn)
+                launch_attn(d->attn, c, d->stream);
+            else
+                launch_gather(c, d->stream, d->sms);
+        };
+        once();
+        ck(cudaEventRecord(d->ev_attn[0], d->stream), "event");
+        for (uint32_t i = 0; i < iters; ++i)
+            once();
+        ck(cudaEventRecord(d->ev_attn[1], d->stream), "event");
+        ck(cudaEventSynchronize(d->ev_attn[1]), "sync");
+        float t = 0.f;
+        ck(cudaEventElapsedTime(&t, d->ev_attn[0], d->ev_attn[1]), "elapsed");
+        *ms = iters ? t / iters : 0.0;
+    });
+}
+
+int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms) { return time_kernel(d, iters, ms, true); }
+int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms) { return time_kernel(d, iters, ms, false); }
+
+const char *kvr_dev_attention_variant(kvr_dev *d) { return attn_variant(d->attn); }
+
+} // extern "C"

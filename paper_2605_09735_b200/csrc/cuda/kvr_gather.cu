@@ -1,0 +1,182 @@
+// kvrail-b200 K-gather: move every staged train into the fixed-shape window.
+//
+// Input is K-scan's span list in train order. A near-window span of a slot is
+// re-packed row by row into that slot's window ring (layer-major rows, token t
+// at row t mod R, only rows of the live window range are written); a far-view
+// span (a chunk summary slot) lands in the slot's far rows. Work unit = one
+// (token, layer) row of 2*d_kv elements; each CTA loops over units with a
+// TMA bulk-copy pipeline: an elected lane issues cp.async.bulk global->shared
+// into a ring of stage buffers (mbarrier completion), then cp.async.bulk
+// shared->global to the destination, recycling a buffer once its store has
+// finished reading it (bulk_group read wait). Pure HBM-bound byte movement.
+#include <algorithm>
+
+#include "kvr_internal.cuh"
+
+namespace kvr {
+
+namespace {
+
+constexpr int kStages = 8;  // stage buffers per CTA
+constexpr int kAhead = 4;   // loads in flight ahead of the stores
+constexpr uint32_t kMaxPiece = 16384; // rows larger than this move in pieces
+
+__device__ inline uint32_t smem_u32(const void *p) {
+    return uint32_t(__cvta_generic_to_shared(p));
+}
+
+__device__ inline void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ inline void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ inline void mbar_wait(uint64_t *bar, uint32_t phase) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "WAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(phase)
+                 : "memory");
+}
+__device__ inline void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ inline void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                 "r"(smem_u32(src)), "r"(bytes)
+                 : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+template <int N> __device__ inline void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+__device__ inline void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ inline void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+/// Resolve unit -> (src, dst, bytes); bytes == 0 when the row is masked out.
+struct Move {
+    const uint8_t *src;
+    uint8_t *dst;
+    uint32_t bytes;
+};
+
+__device__ inline Move resolve(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_spans,
+                               uint64_t unit, uint32_t pieces, uint32_t piece_bytes) {
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    const uint32_t piece = uint32_t(unit % pieces);
+    const uint64_t row_unit = unit / pieces;
+    const uint32_t l = uint32_t(row_unit % c.L);
+    const uint64_t tok_idx = row_unit / c.L;
+    uint32_t lo = 0, hi = n_spans; // last span with tok_prefix <= tok_idx
+    while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) / 2;
+        if (c.gspans[mid].tok_prefix <= tok_idx)
+            lo = mid;
+        else
+            hi = mid;
+    }
+    const GSpan sp = c.gspans[lo];
+    const uint64_t k = tok_idx - sp.tok_prefix;
+    Move m{nullptr, nullptr, 0};
+    if (sp.dev_slot >= c.n_slots)
+        return m;
+    const uint64_t off0 = uint64_t(piece) * piece_bytes;
+    const uint32_t bytes = uint32_t(row_bytes - off0 < piece_bytes ? row_bytes - off0 : piece_bytes);
+    m.src = c.arena + uint64_t(sp.block) * c.page_bytes + (sp.slot_begin + k) * c.token_bytes +
+            l * row_bytes + off0;
+    const uint64_t tok = sp.first_token + k;
+    if (sp.kind == 0) {
+        const uint64_t w = slots[sp.dev_slot].written;
+        const uint64_t lo_tok = w > c.W ? w - c.W : 0; // rows of [lo_tok, lo_tok + R) are live
+        if (tok < lo_tok || tok >= lo_tok + c.R)
+            return m;
+        m.dst = c.ring + (ring_row(c, sp.dev_slot, l, uint32_t(tok % c.R)) * c.esz) + off0;
+    } else {
+        if (tok < KVR_SUMMARY_BASE)
+            return m;
+        const uint64_t chunk = tok - KVR_SUMMARY_BASE;
+        if (chunk >= c.max_chunks)
+            return m;
+        m.dst = c.far + ((uint64_t(sp.dev_slot) * c.L + l) * c.max_chunks + chunk) * c.row_elems * c.esz + off0;
+    }
+    m.bytes = bytes;
+    return m;
+}
+
+// One warp per CTA; lane 0 drives a kStages-deep ring: loads run kAhead units
+// in front of the stores, and a buffer is refilled only after the store that
+// last read it has drained (bulk_group read wait with kStages-kAhead-1 groups
+// still allowed in flight).
+__global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
+    extern __shared__ __align__(128) uint8_t stage[];
+    __shared__ __align__(8) uint64_t full[kStages];
+    const kvr_step_header *h = hdr(c);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint32_t n_spans = c.scan->spans;
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    const uint32_t pieces = uint32_t((row_bytes + piece_bytes - 1) / piece_bytes);
+    const uint64_t units = c.scan->total_tokens * c.L * pieces;
+    if (units == 0 || (c.scan->status & 4u) || threadIdx.x != 0)
+        return;
+    for (int s = 0; s < kStages; ++s)
+        mbar_init(&full[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    Move mv[kStages];
+    uint32_t phase_bits = 0;
+    uint64_t next = blockIdx.x;
+    auto issue = [&](int s) {
+        while (next < units) {
+            const Move m = resolve(c, slots, n_spans, next, pieces, piece_bytes);
+            next += gridDim.x;
+            if (m.bytes) {
+                mv[s] = m;
+                mbar_expect_tx(&full[s], m.bytes);
+                bulk_g2s(stage + size_t(s) * piece_bytes, m.src, m.bytes, &full[s]);
+                return true;
+            }
+        }
+        return false;
+    };
+    uint64_t issued = 0, stored = 0;
+    while (issued < kAhead && issue(int(issued % kStages)))
+        ++issued;
+    while (stored < issued) {
+        const int s = int(stored % kStages);
+        mbar_wait(&full[s], (phase_bits >> s) & 1u);
+        phase_bits ^= 1u << s;
+        bulk_s2g(mv[s].dst, stage + size_t(s) * piece_bytes, mv[s].bytes);
+        ++stored;
+        // next load reuses the stage stored (kStages - kAhead) groups ago
+        bulk_wait_read<kStages - kAhead - 1>();
+        if (issue(int(issued % kStages)))
+            ++issued;
+    }
+    bulk_wait_all();
+}
+
+} // namespace
+
+uint32_t gather_piece_bytes(const DevCtx &c) {
+    const uint64_t row = uint64_t(c.row_elems) * c.esz;
+    return uint32_t(row <= kMaxPiece ? row : kMaxPiece);
+}
+
+void prepare_gather(const DevCtx &c) {
+    const int smem = int(kStages * gather_piece_bytes(c));
+    cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+}
+
+void launch_gather(const DevCtx &c, cudaStream_t s, int sms) {
+    const uint32_t piece = gather_piece_bytes(c);
+    const size_t smem = size_t(kStages) * piece;
+    const int per_sm = int(std::min<size_t>(32, (200u << 10) / smem));
+    k_gather<<<sms * std::max(per_sm, 1), 32, smem, s>>>(c, piece);
+}
+
+} // namespace kvr

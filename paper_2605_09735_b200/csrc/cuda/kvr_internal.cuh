@@ -1,0 +1,96 @@
+// kvrail-b200 device internals shared by the sm_100a kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "kvr_cuda.h"
+#include "kvrail_c.h"
+
+namespace kvr {
+
+constexpr uint32_t kNoMap = 0xffffffffu;
+constexpr int kWarp = 32;
+
+/// One staged span in train order, as consumed by K-gather.
+struct GSpan {
+    uint64_t first_token;  // logical token of slot_begin (near) or summary token (far)
+    uint64_t tok_prefix;   // exclusive prefix of slot_count over the gather list
+    uint32_t block, slot_begin, slot_count, dev_slot;
+    uint32_t kind, pad;
+};
+
+/// Scan/step counters kept in device memory.
+struct ScanCounters {
+    uint32_t trains, descriptors, spans, status;
+    uint64_t total_tokens;
+    uint64_t train_bytes;
+};
+
+/// Everything a kernel needs: geometry + device buffers. Passed by value.
+struct DevCtx {
+    uint64_t page_bytes, token_bytes, max_tokens, seed;
+    uint32_t tpp, arena_pages, L, Hkv, hd, Hq, group, d_kv, row_elems, esz;
+    uint32_t elem_kind, payload_mode, n_slots, W, R, far_cap, chunk_tokens, max_chunks, smap_cap;
+    uint32_t max_scan, max_trains;
+    uint8_t *arena;   // arena_pages * page_bytes
+    uint8_t *ring;    // [slot][L][R][row_elems] elements
+    uint32_t *tmap;   // [slot][max_tokens]
+    uint32_t *smap;   // [slot][smap_cap]
+    uint8_t *far;     // [slot][L][max_chunks][row_elems] elements
+    float *q;         // [slot][L][Hq][hd]
+    float *out;       // [slot][L][Hq][hd]
+    const uint8_t *desc; // device copy of the step descriptor
+    kvr_train *trains;
+    kvr_descriptor *descs;
+    GSpan *gspans;
+    ScanCounters *scan;
+};
+
+__host__ __device__ inline const kvr_step_header *hdr(const DevCtx &c) {
+    return reinterpret_cast<const kvr_step_header *>(c.desc);
+}
+template <typename T> __device__ inline const T *section(const DevCtx &c, uint64_t off) {
+    return reinterpret_cast<const T *>(c.desc + off);
+}
+
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+/// Reference payload lane value ((h % 2001) - 1000) / 1000 (scenario.cpp:200).
+__device__ inline float lane_value(uint64_t h) {
+    return float(int64_t(h % 2001ull) - 1000) / 1000.0f;
+}
+
+/// Arena byte offset of a global slot index (block * tpp + slot).
+__device__ inline uint64_t gslot_offset(const DevCtx &c, uint32_t gs) {
+    return uint64_t(gs / c.tpp) * c.page_bytes + uint64_t(gs % c.tpp) * c.token_bytes;
+}
+
+/// Ring element offset of (slot, layer, row).
+__device__ inline uint64_t ring_row(const DevCtx &c, uint32_t slot, uint32_t l, uint32_t row) {
+    return ((uint64_t(slot) * c.L + l) * c.R + row) * c.row_elems;
+}
+
+// ---- host launchers (one per kernel file) --------------------------------
+void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blob
+void launch_write(const DevCtx &c, cudaStream_t s, int sms);   // generated payloads + query
+void launch_far(const DevCtx &c, cudaStream_t s, int sms);     // far summaries
+void launch_map(const DevCtx &c, cudaStream_t s, int sms);     // page-table edits
+void launch_prime(const DevCtx &c, cudaStream_t s, int sms);   // window priming
+void launch_scan(const DevCtx &c, cudaStream_t s);             // stage + reduce
+void launch_gather(const DevCtx &c, cudaStream_t s, int sms);  // trains -> window
+struct AttnPlan;
+AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device); // builds the TMA descriptor
+void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s);
+void free_attn_plan(AttnPlan *p);
+const char *attn_variant(const AttnPlan *p);
+
+} // namespace kvr

@@ -1,0 +1,507 @@
+// kvrail-b200 DeviceStep: seals a step's host decisions into ONE committed
+// descriptor and publishes it to the B200 (kvr_cuda.h).
+//
+// The Pager reports byte events through the PayloadStore interface; this file
+// turns them into descriptor sections:
+//   on_alloc   -> zero ops, only for recycled (dirty) pages and only for the
+//                 slots this step does not overwrite anyway;
+//   copy_page  -> COW ops;  write -> host blob ops;  write_generated -> write
+//                 ops (token payloads, far summaries);
+//   on_commit  -> page-table edits for sessions bound to a device slot.
+// Within one descriptor the device runs zero -> cow -> blob -> write -> far ->
+// map -> prime -> scan -> gather -> attn. Sequences whose result depends on a
+// different order (a page written and then COW-copied, written twice, ...) are
+// split: the earlier part is flushed as an apply-only descriptor first.
+#include <algorithm>
+#include <cstring>
+#include <stdexcept>
+#include <unordered_map>
+#include <unordered_set>
+
+#include "kvrail/device_step.hpp"
+
+namespace kvrail {
+
+namespace {
+
+void ck(int rc) {
+    if (rc != KVR_OK)
+        throw std::runtime_error(std::string("CUDA/device failure: ") + kvr_dev_last_error());
+}
+
+constexpr uint64_t align16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
+
+} // namespace
+
+struct DeviceStep::Impl {
+    kvr_geometry g{};
+    kvr_dev *dev = nullptr;
+    std::shared_ptr<PayloadStore> store_;
+
+    // pending byte ops (current wave)
+    std::unordered_map<BlockId, std::vector<uint8_t>> zero_pages; // page -> slot written this wave
+    std::vector<BlockId> zero_order;
+    std::vector<kvr_cow_op> cows;
+    std::vector<kvr_edit_op> edits;
+    std::vector<kvr_write_op> writes, far_jobs;
+    std::vector<kvr_blob_op> blob_ops;
+    std::vector<uint8_t> blob;
+    std::unordered_map<BlockId, std::vector<uint8_t>> wave_slots; // slots written this wave
+    std::unordered_set<BlockId> wave_cow_dst;
+    // step inputs
+    std::vector<kvr_need_rec> needs;
+    std::vector<kvr_span_rec> spans;
+    std::vector<kvr_prime_op> primes;
+    std::vector<uint32_t> far_ids;
+    std::vector<kvr_slot_state> slots;
+    // state
+    std::vector<uint8_t> clean; // page known to be all zeros on the device
+    std::unordered_map<SessionId, uint32_t> bound;
+    DeviceStepStats done[2];
+    bool have_done[2] = {false, false};
+    uint64_t launched_step[2] = {~0ull, ~0ull};
+    uint64_t attn_bytes_pending[2] = {0, 0};
+
+    bool pending() const {
+        return !zero_order.empty() || !cows.empty() || !edits.empty() || !writes.empty() ||
+               !far_jobs.empty() || !blob_ops.empty() || !primes.empty();
+    }
+
+    // ---- descriptor packing ----
+    uint64_t pack(void *dst, uint64_t step, double now, const TransportConfig *tc, bool with_step) {
+        // zero ops: unwritten slot runs of recycled pages
+        std::vector<kvr_zero_op> zeros;
+        for (BlockId p : zero_order) {
+            auto it = zero_pages.find(p);
+            if (it == zero_pages.end())
+                continue;
+            const std::vector<uint8_t> &w = it->second;
+            for (uint32_t s = 0; s < g.tokens_per_page;) {
+                if (w[s]) {
+                    ++s;
+                    continue;
+                }
+                uint32_t e = s;
+                while (e < g.tokens_per_page && !w[e])
+                    ++e;
+                zeros.push_back({p, s, e - s, 0});
+                s = e;
+            }
+            // a page's slack beyond tpp * token_bytes is never addressed
+        }
+        kvr_step_header h{};
+        h.step = step;
+        h.now = now;
+        if (tc) {
+            h.tau = tc->merge_threshold;
+            h.max_hold = tc->max_hold;
+            h.merge = tc->merge ? 1 : 0;
+        }
+        uint64_t off = align16(sizeof(kvr_step_header));
+        auto place = [&](uint64_t bytes) {
+            const uint64_t at = off;
+            off = align16(off + bytes);
+            return at;
+        };
+        std::vector<kvr_write_op> all_writes = writes;
+        uint64_t prefix = 0;
+        for (kvr_write_op &w : all_writes) {
+            w.prefix = prefix;
+            prefix += w.count;
+        }
+        h.write_tokens = prefix;
+        for (kvr_write_op w : far_jobs) {
+            w.prefix = prefix;
+            all_writes.push_back(w);
+        }
+        const auto &nd = with_step ? needs : std::vector<kvr_need_rec>{};
+        const auto &sp = with_step ? spans : std::vector<kvr_span_rec>{};
+        const auto &fi = with_step ? far_ids : std::vector<uint32_t>{};
+        h.n_zero = uint32_t(zeros.size());
+        h.off_zero = place(zeros.size() * sizeof(kvr_zero_op));
+        h.n_cow = uint32_t(cows.size());
+        h.off_cow = place(cows.size() * sizeof(kvr_cow_op));
+        h.n_edit = uint32_t(edits.size());
+        h.off_edit = place(edits.size() * sizeof(kvr_edit_op));
+        h.n_write = uint32_t(all_writes.size());
+        h.off_write = place(all_writes.size() * sizeof(kvr_write_op));
+        h.n_blob = uint32_t(blob_ops.size());
+        h.off_blob_ops = place(blob_ops.size() * sizeof(kvr_blob_op));
+        h.off_blob = place(blob.size());
+        h.n_need = uint32_t(nd.size());
+        h.off_need = place(nd.size() * sizeof(kvr_need_rec));
+        h.n_span = uint32_t(sp.size());
+        h.off_span = place(sp.size() * sizeof(kvr_span_rec));
+        h.n_prime = uint32_t(primes.size());
+        h.off_prime = place(primes.size() * sizeof(kvr_prime_op));
+        h.n_far_ids = uint32_t(fi.size());
+        h.off_far_ids = place(fi.size() * sizeof(uint32_t));
+        h.off_slots = place(slots.size() * sizeof(kvr_slot_state));
+        h.total_bytes = off;
+        if (off > g.max_desc_bytes)
+            throw std::runtime_error("step descriptor exceeds max_desc_bytes");
+        auto *base = static_cast<uint8_t *>(dst);
+        auto put = [&](uint64_t at, const void *src, uint64_t bytes) {
+            if (bytes)
+                std::memcpy(base + at, src, bytes);
+        };
+        put(0, &h, sizeof(h));
+        put(h.off_zero, zeros.data(), zeros.size() * sizeof(kvr_zero_op));
+        put(h.off_cow, cows.data(), cows.size() * sizeof(kvr_cow_op));
+        put(h.off_edit, edits.data(), edits.size() * sizeof(kvr_edit_op));
+        put(h.off_write, all_writes.data(), all_writes.size() * sizeof(kvr_write_op));
+        put(h.off_blob_ops, blob_ops.data(), blob_ops.size() * sizeof(kvr_blob_op));
+        put(h.off_blob, blob.data(), blob.size());
+        put(h.off_need, nd.data(), nd.size() * sizeof(kvr_need_rec));
+        put(h.off_span, sp.data(), sp.size() * sizeof(kvr_span_rec));
+        put(h.off_prime, primes.data(), primes.size() * sizeof(kvr_prime_op));
+        put(h.off_far_ids, fi.data(), fi.size() * sizeof(uint32_t));
+        put(h.off_slots, slots.data(), slots.size() * sizeof(kvr_slot_state));
+        return off;
+    }
+
+    void clear_wave() {
+        zero_pages.clear();
+        zero_order.clear();
+        cows.clear();
+        edits.clear();
+        writes.clear();
+        far_jobs.clear();
+        blob_ops.clear();
+        blob.clear();
+        wave_slots.clear();
+        wave_cow_dst.clear();
+        primes.clear();
+    }
+
+    void flush() {
+        if (!pending())
+            return;
+        void *buf = nullptr;
+        ck(kvr_dev_desc_buffer(dev, 2, &buf));
+        const uint64_t bytes = pack(buf, 0, 0.0, nullptr, false);
+        ck(kvr_dev_apply_only(dev, 2, bytes));
+        clear_wave();
+    }
+
+    // ---- PayloadStore events ----
+    void note_slots(BlockId b, uint32_t slot, uint32_t count) {
+        auto &w = wave_slots[b];
+        if (w.empty())
+            w.assign(g.tokens_per_page, 0);
+        bool clash = false;
+        for (uint32_t i = 0; i < count; ++i)
+            clash |= w[slot + i] != 0;
+        if (clash) { // same slot written twice in one wave: order matters
+            flush();
+            auto &w2 = wave_slots[b];
+            w2.assign(g.tokens_per_page, 0);
+            for (uint32_t i = 0; i < count; ++i)
+                w2[slot + i] = 1;
+        } else {
+            for (uint32_t i = 0; i < count; ++i)
+                w[slot + i] = 1;
+        }
+        auto z = zero_pages.find(b);
+        if (z != zero_pages.end())
+            for (uint32_t i = 0; i < count; ++i)
+                z->second[slot + i] = 1;
+        clean[b] = 0;
+    }
+
+    void on_alloc(BlockId head, uint32_t count) {
+        for (uint32_t i = 0; i < count; ++i) {
+            const BlockId p = head + i;
+            if (clean[p])
+                continue;
+            if (wave_slots.count(p) || wave_cow_dst.count(p))
+                flush(); // zeroing must follow this wave's writes to the page
+            if (!zero_pages.count(p)) {
+                zero_pages[p].assign(g.tokens_per_page, 0);
+                zero_order.push_back(p);
+            }
+            clean[p] = 1;
+        }
+    }
+
+    void copy_page(BlockId src, BlockId dst) {
+        if (wave_slots.count(src) || wave_cow_dst.count(src))
+            flush(); // the copy must see this wave's writes to src
+        // the copy overwrites dst entirely; a pending zero of dst is moot
+        if (zero_pages.erase(dst))
+            zero_order.erase(std::remove(zero_order.begin(), zero_order.end(), dst), zero_order.end());
+        cows.push_back({src, dst});
+        wave_cow_dst.insert(dst);
+        clean[dst] = clean[src];
+    }
+
+    void write_host(BlockId b, uint32_t slot, uint32_t count, const std::byte *bytes) {
+        const uint64_t n = uint64_t(count) * g.token_bytes;
+        if (align16(blob.size() + n) + 65536 > g.max_desc_bytes / 2)
+            flush();
+        note_slots(b, slot, count);
+        blob_ops.push_back({blob.size(), b, slot, count, 0});
+        blob.insert(blob.end(), reinterpret_cast<const uint8_t *>(bytes),
+                    reinterpret_cast<const uint8_t *>(bytes) + n);
+        blob.resize(align16(blob.size()));
+    }
+
+    void write_gen(const GeneratedWrite &w) {
+        const auto it = bound.find(w.session);
+        const uint32_t slot = it == bound.end() ? KVR_NO_SLOT : it->second;
+        if (w.source == 1) {
+            if (slot == KVR_NO_SLOT)
+                throw std::runtime_error("far summary job for a session without a device slot");
+            note_slots(w.block, w.slot, w.count);
+            kvr_write_op op{};
+            op.token = w.token;
+            op.aux = w.aux;
+            op.block = w.block;
+            op.slot = w.slot;
+            op.count = 1;
+            op.session = w.session;
+            op.dev_slot = slot;
+            op.source = 1;
+            far_jobs.push_back(op);
+            return;
+        }
+        note_slots(w.block, w.slot, w.count);
+        if (!writes.empty()) { // coalesce consecutive tokens of one block
+            kvr_write_op &b = writes.back();
+            if (b.session == w.session && b.block == w.block && b.slot + b.count == w.slot &&
+                b.token + b.count == w.token && b.dev_slot == slot) {
+                b.count += w.count;
+                return;
+            }
+        }
+        kvr_write_op op{};
+        op.token = w.token;
+        op.block = w.block;
+        op.slot = w.slot;
+        op.count = w.count;
+        op.session = w.session;
+        op.dev_slot = slot;
+        op.source = 0;
+        writes.push_back(op);
+    }
+
+    void on_commit(SessionId sid, std::span<const ViewEdit> ed) {
+        const auto it = bound.find(sid);
+        if (it == bound.end())
+            return;
+        for (const ViewEdit &e : ed)
+            edits.push_back({e.tok_begin, e.tok_end, it->second, e.block, e.slot_begin, 0});
+    }
+
+    void read(BlockId b, uint32_t slot, uint32_t count, std::byte *out) {
+        flush();
+        ck(kvr_dev_read(dev, KVR_BUF_ARENA, uint64_t(b) * g.page_bytes + uint64_t(slot) * g.token_bytes,
+                        uint64_t(count) * g.token_bytes, out));
+    }
+};
+
+namespace {
+
+class DeviceStore final : public PayloadStore {
+public:
+    explicit DeviceStore(DeviceStep::Impl *m) : m_(m) {}
+    void on_alloc(BlockId head, uint32_t count) override { m_->on_alloc(head, count); }
+    void copy_page(BlockId src, BlockId dst) override { m_->copy_page(src, dst); }
+    void write(BlockId b, uint32_t slot, uint32_t count, const std::byte *bytes) override {
+        m_->write_host(b, slot, count, bytes);
+    }
+    void write_generated(const GeneratedWrite &w) override { m_->write_gen(w); }
+    void read(BlockId b, uint32_t slot, uint32_t count, std::byte *out) override {
+        m_->read(b, slot, count, out);
+    }
+    void on_commit(SessionId sid, bool, std::span<const ViewEdit> ed) override { m_->on_commit(sid, ed); }
+
+private:
+    DeviceStep::Impl *m_;
+};
+
+} // namespace
+
+DeviceStep::DeviceStep(const kvr_geometry &geometry) : impl_(std::make_unique<Impl>()) {
+    Impl &m = *impl_;
+    ck(kvr_dev_open(&geometry, &m.dev));
+    m.g = geometry;
+    if (!m.g.max_desc_bytes)
+        m.g.max_desc_bytes = 16ull << 20;
+    m.clean.assign(m.g.arena_pages, 1); // the arena starts zeroed
+    m.slots.assign(m.g.n_slots, kvr_slot_state{});
+    m.store_ = std::make_shared<DeviceStore>(impl_.get());
+}
+
+DeviceStep::~DeviceStep() {
+    if (impl_ && impl_->dev) {
+        kvr_dev_sync(impl_->dev);
+        kvr_dev_close(impl_->dev);
+    }
+}
+
+const kvr_geometry &DeviceStep::geometry() const { return impl_->g; }
+kvr_dev *DeviceStep::handle() const { return impl_->dev; }
+std::shared_ptr<PayloadStore> DeviceStep::store() { return impl_->store_; }
+
+void DeviceStep::bind(SessionId sid, uint32_t slot) {
+    if (slot >= impl_->g.n_slots)
+        throw std::runtime_error("device slot out of range");
+    impl_->bound[sid] = slot;
+}
+void DeviceStep::unbind(SessionId sid) { impl_->bound.erase(sid); }
+
+void DeviceStep::slot_state(uint32_t slot, SessionId sid, uint64_t written, bool live) {
+    kvr_slot_state &s = impl_->slots.at(slot);
+    s.session = sid;
+    s.written = written;
+    s.live = live ? 1 : 0;
+    s.far_begin = 0;
+    s.far_count = 0;
+}
+
+void DeviceStep::need(uint32_t slot, SessionId sid, TrainKind kind, std::span<const StagedSpan> spans,
+                      std::span<const uint64_t> first_tokens) {
+    Impl &m = *impl_;
+    kvr_need_rec n{};
+    n.slot = slot;
+    n.session = sid;
+    n.kind = uint32_t(kind);
+    n.span_begin = uint32_t(m.spans.size());
+    n.span_count = uint32_t(spans.size());
+    m.needs.push_back(n);
+    for (size_t i = 0; i < spans.size(); ++i)
+        m.spans.push_back({first_tokens[i], spans[i].block, spans[i].slot_begin, spans[i].slot_count, 0});
+}
+
+void DeviceStep::prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end) {
+    impl_->primes.push_back({tok_begin, tok_end, slot, 0});
+}
+
+void DeviceStep::far_selection(uint32_t slot, std::span<const uint64_t> chunk_ids) {
+    Impl &m = *impl_;
+    kvr_slot_state &s = m.slots.at(slot);
+    s.far_begin = uint32_t(m.far_ids.size());
+    s.far_count = 0;
+    for (uint64_t id : chunk_ids) {
+        if (s.far_count >= m.g.far_cap || id >= m.g.max_chunks)
+            break;
+        m.far_ids.push_back(uint32_t(id));
+        ++s.far_count;
+    }
+}
+
+void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
+    Impl &m = *impl_;
+    const uint32_t k = uint32_t(step & 1);
+    if (m.launched_step[k] != ~0ull && !m.have_done[k]) { // ring slot still busy
+        kvr_step_stats st{};
+        ck(kvr_dev_wait(m.dev, k, &st));
+        DeviceStepStats &d = m.done[k];
+        d.step = st.step;
+        d.device_ms = st.device_ms;
+        d.trains = st.trains;
+        d.descriptors = st.descriptors;
+        d.train_bytes = st.train_bytes;
+        d.writeback_tokens = st.writeback_tokens;
+        d.scan_status = st.status;
+        d.attn_bytes = m.attn_bytes_pending[k];
+        m.have_done[k] = true;
+    }
+    uint64_t attn = 0;
+    if (m.g.attention) {
+        const uint64_t row = 2ull * m.g.kv_heads * m.g.head_dim * m.g.elem_bytes;
+        for (const kvr_slot_state &s : m.slots)
+            if (s.live)
+                attn += (std::min<uint64_t>(s.written, m.g.near_window) + s.far_count) * m.g.layers * row;
+    }
+    void *buf = nullptr;
+    ck(kvr_dev_desc_buffer(m.dev, k, &buf));
+    const uint64_t bytes = m.pack(buf, step, now, &tc, true);
+    ck(kvr_dev_launch(m.dev, k, bytes));
+    m.launched_step[k] = step;
+    m.have_done[k] = false;
+    m.attn_bytes_pending[k] = attn;
+    m.clear_wave();
+    m.needs.clear();
+    m.spans.clear();
+    m.far_ids.clear();
+}
+
+DeviceStepStats DeviceStep::collect(uint64_t step) {
+    Impl &m = *impl_;
+    const uint32_t k = uint32_t(step & 1);
+    if (m.launched_step[k] != step)
+        throw std::runtime_error("collect: step " + std::to_string(step) + " is not in flight");
+    if (!m.have_done[k]) {
+        kvr_step_stats st{};
+        ck(kvr_dev_wait(m.dev, k, &st));
+        DeviceStepStats &d = m.done[k];
+        d.step = st.step;
+        d.device_ms = st.device_ms;
+        d.trains = st.trains;
+        d.descriptors = st.descriptors;
+        d.train_bytes = st.train_bytes;
+        d.writeback_tokens = st.writeback_tokens;
+        d.scan_status = st.status;
+        d.attn_bytes = m.attn_bytes_pending[k];
+        m.have_done[k] = true;
+    }
+    return m.done[k];
+}
+
+void DeviceStep::sync() { ck(kvr_dev_sync(impl_->dev)); }
+void DeviceStep::flush() { impl_->flush(); }
+
+void DeviceStep::read_arena(uint64_t offset, uint64_t bytes, void *out) {
+    impl_->flush();
+    ck(kvr_dev_read(impl_->dev, KVR_BUF_ARENA, offset, bytes, out));
+}
+
+void DeviceStep::read_ring_token(uint32_t slot, uint64_t token, void *out) {
+    const kvr_geometry &g = impl_->g;
+    const uint64_t row = 2ull * g.kv_heads * g.head_dim * g.elem_bytes;
+    for (uint32_t l = 0; l < g.layers; ++l) {
+        const uint64_t off = ((uint64_t(slot) * g.layers + l) * g.ring_rows + token % g.ring_rows) * row;
+        ck(kvr_dev_read(impl_->dev, KVR_BUF_RING, off, row, static_cast<uint8_t *>(out) + l * row));
+    }
+}
+
+void DeviceStep::read_page_table(uint32_t slot, uint64_t tok_begin, uint64_t count, uint32_t *out) {
+    const kvr_geometry &g = impl_->g;
+    ck(kvr_dev_read(impl_->dev, KVR_BUF_TMAP, (uint64_t(slot) * g.max_tokens + tok_begin) * 4, count * 4, out));
+}
+
+void DeviceStep::read_attention(uint32_t slot, float *out) {
+    const kvr_geometry &g = impl_->g;
+    const uint64_t n = uint64_t(g.layers) * g.q_heads * g.head_dim;
+    ck(kvr_dev_read(impl_->dev, KVR_BUF_OUT, uint64_t(slot) * n * 4, n * 4, out));
+}
+
+void DeviceStep::read_query(uint32_t slot, float *out) {
+    const kvr_geometry &g = impl_->g;
+    const uint64_t n = uint64_t(g.layers) * g.q_heads * g.head_dim;
+    ck(kvr_dev_read(impl_->dev, KVR_BUF_QUERY, uint64_t(slot) * n * 4, n * 4, out));
+}
+
+void DeviceStep::read_far_row(uint32_t slot, uint64_t chunk, void *out) {
+    const kvr_geometry &g = impl_->g;
+    const uint64_t row = 2ull * g.kv_heads * g.head_dim * g.elem_bytes;
+    for (uint32_t l = 0; l < g.layers; ++l) {
+        const uint64_t off = ((uint64_t(slot) * g.layers + l) * g.max_chunks + chunk) * row;
+        ck(kvr_dev_read(impl_->dev, KVR_BUF_FAR, off, row, static_cast<uint8_t *>(out) + l * row));
+    }
+}
+
+void DeviceStep::read_scan(std::vector<kvr_train> &trains, std::vector<kvr_descriptor> &descs) {
+    uint32_t ctr[4];
+    ck(kvr_dev_read(impl_->dev, KVR_BUF_SCAN, 0, sizeof(ctr), ctr));
+    trains.resize(ctr[0]);
+    descs.resize(ctr[1]);
+    if (ctr[0])
+        ck(kvr_dev_read(impl_->dev, KVR_BUF_TRAINS, 0, ctr[0] * sizeof(kvr_train), trains.data()));
+    if (ctr[1])
+        ck(kvr_dev_read(impl_->dev, KVR_BUF_DESCS, 0, ctr[1] * sizeof(kvr_descriptor), descs.data()));
+}
+
+} // namespace kvrail
