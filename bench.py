@@ -1,0 +1,321 @@
+#!/usr/bin/env python
+"""bench.py — KV-RM decode step on B200: decode tokens/s + merged KV-gather GB/s.
+
+Workload (BASELINE.json configs[1], "C2"): Llama-2-7B-shaped KV — 32 layers,
+32 KV heads x head_dim 128, fp16 (512 KiB per token), 16-token pages (8 MiB),
+tau = 8 pages, W* = 512, batch 64, prompts log-uniform 512-8192 tokens plus the
+reference generate-length law (p50/p90/p99 = 96/384/1024), admission as the
+reference Driver does it (scenario.cpp:279-360), synthetic seeded data.
+
+One step = one reference Driver::step (pager verbs, one frame commit per live
+session, stage needs) + one committed descriptor + one replay of the step graph
+(apply, writeback, far, map, prime, K-scan, K-gather, K-attn) on the GPU.
+
+  value  = emitted tokens / sum of per-step device time (CUDA events around the
+           descriptor H2D + graph + stats D2H on the launch stream), KV resident;
+  e2e    = emitted tokens / wall time of the same steps driven through the C-ABI
+           (host control plane, pinned H2D of each step's descriptor, D2H of the
+           step counters), synchronised at both ends.
+Multi-GPU (torchrun): requests shard by sequence (request_id % world); every rank
+runs its own pager + graph; the max over ranks of the timed region is used.
+
+--impl reference: the reference's own CPU path (oracle/_ref: run_scenario control
+plane + memcpy gather + build_view/attend), rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("decode tokens/s + merged KV-gather HBM GB/s (mixed-length batch, 1/2/4/8 B200)")
+MIB = 1 << 20
+
+
+def c2_config(steps: int, rank: int = 0, world: int = 1) -> dict:
+    page = 8 * MIB
+    return {
+        "label": "c2-llama2-7b-kv", "seed": 1, "steps": steps, "warmup_steps": 0,
+        "pager": {"page_bytes": page, "layers": 32, "kv_head_dim": 4096, "elem_bytes": 2},
+        "transport": {"tau_bytes": 8 * page, "delta_hold": 0.756, "merge": True},
+        "far_view": {"enabled": False, "w_star": 512},
+        "workload": {"requests": 10000, "concurrency": 64, "prompt_min": 512,
+                     "prompt_max": 8192, "arrivals_per_window": 40.0 * world, "seed": 1},
+        "shaping": {"arena_pages": 15000},
+        "b200": {"kv_heads": 32, "head_dim": 128, "q_heads": 32, "payload": "lanes",
+                 "dtype": "fp16", "shard_rank": rank, "shard_world": world},
+    }
+
+
+def peaks() -> dict:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"hbm_gbs": float(p["hbm_gbs"]), "src": "measured"}
+    except Exception:
+        return {"hbm_gbs": 6650.0, "src": "fallback"}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows: list[list[str]] = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.15)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(sm)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    return rank, local, world
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def reduce_max(vals: list[float], world: int) -> list[float]:
+    if world == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.tolist()
+
+
+def reduce_sum(vals: list[float], world: int) -> list[float]:
+    if world == 1:
+        return vals
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def run_b200(args, rank, local, world) -> dict | None:
+    import paper_2605_09735_b200 as pkg
+
+    fill_cap = 400
+    cfg = c2_config(fill_cap + args.warmup + args.steps, rank, world)
+    d = pkg.Driver(cfg, device=local)
+    width = cfg["workload"]["concurrency"]
+    # fill the fixed-width batch (admissions write whole prompts), then warm up
+    fill = 0
+    while fill < fill_cap:
+        r = d.step()
+        fill += 1
+        if r.live_sessions >= width:
+            break
+    for _ in range(args.warmup):
+        d.step()
+    d.sync()
+    first = d.progress()[0]
+    barrier(world)
+    with Clocks(local) as clocks:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            d.step()
+        d.sync()
+        t1 = time.perf_counter()
+    barrier(world)
+    recs = [d.record(s) for s in range(first, first + args.steps)]
+    dev_s = sum(r.device_ms for r in recs) / 1e3
+    wall_s = t1 - t0
+    tokens = sum(r.emitted_tokens for r in recs)
+    attn_bytes = sum(r.attn_bytes for r in recs)
+    attn_s = sum(r.attn_ms for r in recs) / 1e3
+    gather_bytes = sum(r.gather_bytes for r in recs)
+    gather_s = sum(r.gather_ms for r in recs) / 1e3
+    h2d = sum(r.h2d_bytes for r in recs) / args.steps
+    dev = d.device()
+    variant = dev.attention_variant()
+    dev_s_max, wall_s_max = reduce_max([dev_s, wall_s], world)
+    tokens_all, gather_bytes_all = reduce_sum([float(tokens), float(gather_bytes)], world)
+    out = {
+        "rank": rank, "cfg": cfg, "recs": recs, "dev_s": dev_s_max, "wall_s": wall_s_max,
+        "tokens": tokens_all, "attn_bytes": attn_bytes, "attn_s": attn_s,
+        "gather_bytes": gather_bytes, "gather_s": gather_s, "gather_bytes_all": gather_bytes_all,
+        "h2d": h2d, "variant": variant, "clocks": clocks.summary(), "fill_steps": fill,
+        "live_mean": statistics.mean(r.live_sessions for r in recs),
+        "trains_mean": statistics.mean(r.trains for r in recs),
+        "dma_mean": statistics.mean(r.dma_bytes for r in recs),
+        "mean_train_bytes": (sum(r.dma_bytes for r in recs) / max(1, sum(r.trains for r in recs))),
+        "p50_ms": statistics.median(r.device_ms for r in recs),
+        "p99_ms": sorted(r.device_ms for r in recs)[min(len(recs) - 1, int(0.99 * len(recs)))],
+    }
+    d.close()
+    return out
+
+
+def cpu_baseline_block(res: dict, threads: int | None = None) -> dict:
+    from oracle import cpu_baseline as cb
+    cfg = res["cfg"]
+    b = cfg["b200"]
+    threads = threads or os.cpu_count() or 1
+    leg = cb.decode_step(cfg, live=round(res["live_mean"]), layers=cfg["pager"]["layers"],
+                         q_heads=b["q_heads"], head_dim=b["head_dim"],
+                         window=cfg["far_view"]["w_star"], dma_bytes_per_step=res["dma_mean"],
+                         threads=threads, attention_calls=512 * threads)
+    return {"value": leg["tokens_per_s"], "unit": "tokens/s", "cores": leg["threads"],
+            "kind": "reference",
+            "sample": (f"{leg['attention_calls_timed']} of the {leg['attention_calls_per_step']} "
+                       f"reference build_view+attend calls of one C2 decode step (W*={cfg['far_view']['w_star']}, hd="
+                       f"{b['head_dim']}) on {leg['threads']} OpenMP threads + run_scenario "
+                       f"control plane (200 steps, 1 thread, pager geometry scaled to 1 KiB "
+                       f"tokens) + memcpy gather of the mean train bytes"),
+            "legs_s": {"control": leg["control_s"], "attention": leg["attention_s"],
+                       "gather": leg["gather_s"]}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    rank, local, world = dist_setup()
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(reference_arm(args, world)), flush=True)
+        return
+
+    res = run_b200(args, rank, local, world)
+    if rank != 0:
+        return
+    pk = peaks()
+    value = res["tokens"] / res["dev_s"]
+    e2e = res["tokens"] / res["wall_s"]
+    attn_gbs = res["attn_bytes"] / res["attn_s"] / 1e9 if res["attn_s"] else 0.0
+    gather_gbs = 2 * res["gather_bytes"] / res["gather_s"] / 1e9 if res["gather_s"] else 0.0
+    line = {
+        "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["dev_s"] / args.steps * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "fp16",
+        "data": "synthetic: seeded reference payload pattern (fill_token_payload lanes, RNE fp16)",
+        "config": {
+            "workload": "C2 Llama-2-7B-shaped KV (configs[1]): L=32, 32 KV heads x hd 128, fp16, "
+                        "batch 64 per GPU, prompts 512-8192 (log-uniform) + decode, W*=512",
+            "page_bytes": 8 * MIB, "tokens_per_page": 16, "tau_bytes": 64 * MIB,
+            "requests_shard": "request_id % n_gpus", "l2": "inputs larger than L2 "
+            "(~16 GiB of window KV read per step vs 126 MB L2)",
+            "attention_kernel": res["variant"], "fill_steps": res["fill_steps"],
+        },
+        "gather_hbm_gbs": gather_gbs,
+        "transport": {"trains_per_step": res["trains_mean"], "mean_train_bytes":
+                      res["mean_train_bytes"], "live_mean": res["live_mean"]},
+        "step_latency_ms": {"p50": res["p50_ms"], "p99": res["p99_ms"]},
+        "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],
+                "d2h_bytes_per_step": 32},
+        "gpu_launches": 11 * args.steps,
+        "roofline": {"bound": "hbm", "achieved": attn_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": attn_gbs / pk["hbm_gbs"], "traffic": None,
+                     "kernel": res["variant"], "peak_src": pk["src"],
+                     "bytes_per_launch": res["attn_bytes"] / args.steps,
+                     "ms_per_launch": res["attn_s"] / args.steps * 1e3},
+        "clocks": res["clocks"],
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline_block(res)
+        except Exception as e:  # the oracle is absent: report, do not fake
+            line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
+    print(json.dumps(line), flush=True)
+
+
+def reference_arm(args, world) -> dict:
+    """The reference's CPU implementation of the step (oracle/_ref), same workload."""
+    from oracle import cpu_baseline as cb
+    cfg = c2_config(400, 0, 1)
+    b = cfg["b200"]
+    live = cfg["workload"]["concurrency"]
+    per_step = []
+    ctl = cb.control_plane_seconds_per_step(cfg)
+    gbs = cb.memcpy_gbs()
+    dma = 2 * 8 * 9 * MIB  # two merged trains of one 9-page span, as the B200 run measures
+    threads = os.cpu_count() or 1
+    calls = live * cfg["pager"]["layers"] * b["q_heads"]
+    sample = min(calls, 512 * threads)
+    for i in range(args.warmup + args.steps):
+        t_attn = cb.attention_seconds(b["head_dim"], cfg["far_view"]["w_star"], sample,
+                                      threads) * calls / sample
+        if i >= args.warmup:
+            per_step.append(ctl + t_attn + 2.0 * dma / (gbs * 1e9))
+    total = sum(per_step)
+    value = live * len(per_step) / total
+    return {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": total / len(per_step) * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64 (reference attend)",
+            "data": "synthetic", "config": {"workload": "C2 (same as the b200 arm)"},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
+                             "kind": "reference",
+                             "sample": f"per timed step {sample} of the {calls} reference "
+                                       "build_view+attend calls of a C2 step (extrapolated), all "
+                                       "threads, + run_scenario control plane + memcpy"},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+
+
+if __name__ == "__main__":
+    main()

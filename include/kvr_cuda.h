@@ -112,7 +112,9 @@ typedef struct kvr_slot_state {
 /* step results (written by the device, read back one step later) */
 typedef struct kvr_step_stats {
     uint64_t step;
-    double device_ms;
+    double device_ms;       /* descriptor H2D + step kernels + stats D2H */
+    double gather_ms;       /* K-gather alone (event nodes inside the graph) */
+    double attn_ms;         /* K-attn alone */
     uint32_t trains, descriptors, spans, status;
     uint64_t train_bytes;
     uint64_t staged_tokens;

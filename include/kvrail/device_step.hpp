@@ -35,11 +35,14 @@ namespace kvrail {
 struct DeviceStepStats {
     uint64_t step = 0;
     double device_ms = 0.0;     // CUDA-event time of the step's device work
+    double gather_ms = 0.0;     // K-gather alone
+    double attn_ms = 0.0;       // K-attn alone
     uint32_t trains = 0;        // computed by K-scan
     uint32_t descriptors = 0;
     uint64_t train_bytes = 0;   // sum of train bytes (gather read side)
     uint64_t writeback_tokens = 0;
     uint64_t attn_bytes = 0;    // KV bytes the attention read
+    uint64_t h2d_bytes = 0;     // committed descriptor bytes published this step
     uint32_t scan_status = 0;   // 0 ok; else capacity overflow flags
 };
 
@@ -72,6 +75,8 @@ public:
     DeviceStepStats collect(uint64_t step);
     /// Wait for all launched work.
     void sync();
+    /// Whether `step` is the last step launched from its ring slot.
+    bool launched(uint64_t step) const;
     /// Flush byte ops queued outside a step (Pager API use without a Driver).
     void flush();
 

@@ -40,7 +40,13 @@ struct B200Config {
     uint64_t max_tokens = 0;       // per-slot token capacity of the device page table; 0 = auto
     uint32_t graph = 1;            // replay the step as a captured CUDA graph
     bool check = false;            // compare the device K-scan with host reduce() every step
+    uint32_t shard_rank = 0;       // requests shard by sequence across GPUs:
+    uint32_t shard_world = 1;      //   this rank keeps request_id % world == rank
 };
+
+/// Keep this rank's share of an event stream (request_id % world == rank).
+std::vector<TraceEvent> shard_events(const std::vector<TraceEvent> &events, uint32_t rank,
+                                     uint32_t world);
 
 struct ScenarioConfig {
     std::string label = "run";
@@ -116,6 +122,9 @@ public:
     uint64_t steps_done() const;
     const ScenarioConfig &config() const;
     const std::vector<StepRecord> &records() const;
+    /// Record of an executed step, completed with its device measurements
+    /// (waits for the device if that step is still in flight).
+    const StepRecord &record(uint64_t step);
     const std::vector<TraceEvent> &events() const;
     /// Parity trace text; empty unless b200.trace.
     const std::string &trace() const;

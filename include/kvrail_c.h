@@ -193,9 +193,12 @@ typedef struct kvr_step_record { /* StepRecord, sim_engine.hpp:47-63 + measured 
     uint64_t emitted_tokens;
     /* B200 additions (0 on a host-only driver) */
     double device_ms;          /* CUDA-event time of this step's graph replay */
+    double gather_ms;          /* K-gather kernel alone */
+    double attn_ms;            /* K-attn kernel alone */
     uint64_t writeback_tokens; /* token rows written to the arena this step */
     uint64_t gather_bytes;     /* bytes the gather moved (read side) */
     uint64_t attn_bytes;       /* KV bytes the window attention read */
+    uint64_t h2d_bytes;        /* committed step descriptor bytes copied host -> device */
 } kvr_step_record;
 
 /* ---- Pager (pager.hpp:121-183) ------------------------------------------ */
@@ -281,8 +284,13 @@ int kvr_attend_history(const float *images, uint64_t t, const double *chunk_scor
 typedef struct kvr_driver kvr_driver;
 int kvr_driver_create(const char *config_json, int device, kvr_driver **out);
 int kvr_driver_destroy(kvr_driver *d);
-/* One Driver::step (scenario.cpp:450-682). */
+/* One Driver::step (scenario.cpp:450-682). Device fields of the returned
+ * record are filled one step later; fetch them with kvr_driver_record. */
 int kvr_driver_step(kvr_driver *d, kvr_step_record *out);
+/* Record of an executed step including its device measurements. */
+int kvr_driver_record(kvr_driver *d, uint64_t step, kvr_step_record *out);
+/* Wait for all device work of the driver (no-op on a host-only driver). */
+int kvr_driver_sync(kvr_driver *d);
 /* Steps executed so far / configured total. */
 int kvr_driver_progress(kvr_driver *d, uint64_t *done, uint64_t *total);
 /* steps.csv (scenario.cpp:706-725) / report.json (scenario.cpp:727-766) of

@@ -1,0 +1,84 @@
+"""TEST INFRASTRUCTURE — the reference's CPU decode path, timed (bench.py only).
+
+Legs, all executed by the reference library compiled from its
+own sources (oracle/_ref, kind "reference"):
+  1. control plane: kvrail_ref::run_scenario on the same workload with the
+     pager geometry scaled to 1 KiB tokens (identical tokens-per-page, page
+     counts and tau in pages, so every pager / stage / reduce decision is the
+     same; only payload bytes shrink), single thread, wall time per step;
+  2. gather: host memcpy of the step's train bytes at the reference's
+     single-thread copy bandwidth (read + write);
+  3. attention: kvrail_ref::build_view + kvrail_ref::attend per (session, layer,
+     q-head) over the W*-token window, OpenMP over all host threads.
+tokens/s = live / (t1 + t2 + t3).
+"""
+from __future__ import annotations
+
+import copy
+import ctypes as C
+import os
+import time
+
+from . import bindings as ob
+
+
+def _lib():
+    lib = ob.ref()
+    lib.kvr_ref_cpu_attention_sample.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+                                                 C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    lib.kvr_ref_cpu_memcpy_gbs.argtypes = [C.c_uint64, C.c_int, C.POINTER(C.c_double)]
+    return lib
+
+
+def control_plane_seconds_per_step(config: dict, steps: int = 200) -> float:
+    cfg = copy.deepcopy(config)
+    cfg.pop("b200", None)
+    p = cfg.setdefault("pager", {})
+    tb = 2 * p["layers"] * p["kv_head_dim"] * p["elem_bytes"]
+    tpp = p["page_bytes"] // tb
+    scale = tb // 1024
+    p.update({"layers": 4, "kv_head_dim": 64, "elem_bytes": 2, "page_bytes": tpp * 1024})
+    t = cfg.setdefault("transport", {})
+    t["tau_bytes"] = int(t.get("tau_bytes", 131072) // scale)
+    cfg["steps"] = steps
+    cfg["warmup_steps"] = 0
+    _, _, _, wall = ob.ref_scenario(cfg, trace=False)
+    return wall / steps
+
+
+def attention_seconds(head_dim: int, window: int, calls: int, threads: int) -> float:
+    secs, chk = C.c_double(), C.c_double()
+    rc = _lib().kvr_ref_cpu_attention_sample(head_dim, window, calls, threads, C.byref(secs),
+                                             C.byref(chk))
+    if rc:
+        raise RuntimeError(ob.ref().kvr_ref_last_error().decode())
+    return secs.value
+
+
+def memcpy_gbs(nbytes: int = 256 << 20, reps: int = 4) -> float:
+    g = C.c_double()
+    rc = _lib().kvr_ref_cpu_memcpy_gbs(nbytes, reps, C.byref(g))
+    if rc:
+        raise RuntimeError(ob.ref().kvr_ref_last_error().decode())
+    return g.value
+
+
+def decode_step(config: dict, live: int, layers: int, q_heads: int, head_dim: int, window: int,
+                dma_bytes_per_step: float, threads: int | None = None,
+                attention_calls: int | None = None) -> dict:
+    """One reference decode step's CPU time, legs and tokens/s."""
+    threads = threads or os.cpu_count() or 1
+    calls_per_step = live * layers * q_heads
+    calls = attention_calls or calls_per_step
+    t_ctl = control_plane_seconds_per_step(config)
+    t_attn_sample = attention_seconds(head_dim, window, calls, threads)
+    t_attn = t_attn_sample * calls_per_step / calls
+    gbs = memcpy_gbs()
+    t_gather = 2.0 * dma_bytes_per_step / (gbs * 1e9)
+    total = t_ctl + t_attn + t_gather
+    return {
+        "tokens_per_s": live / total, "seconds_per_step": total, "control_s": t_ctl,
+        "attention_s": t_attn, "gather_s": t_gather, "memcpy_gbs": gbs, "threads": threads,
+        "attention_calls_timed": calls, "attention_calls_per_step": calls_per_step,
+        "attention_sample_s": t_attn_sample,
+    }

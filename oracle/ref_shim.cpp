@@ -498,4 +498,57 @@ int kvr_ref_scenario_events(const char *config_json, char **csv) {
 
 void kvr_ref_free(char *p) { std::free(p); }
 
+// ---- CPU baseline legs (bench.py cpu_baseline / --impl reference) ----------------
+// The reference's own attention path for one (session, layer, q-head): build the
+// fixed-width view of a `window`-token history through a TokenReader (the
+// near-window gather, far_view.cpp:64-111) and attend over it (far_view.cpp:113-
+// 155). `calls` such (session, head) evaluations run on `threads` OpenMP threads
+// (build_view/attend are serial inside); returns wall seconds.
+int kvr_ref_cpu_attention_sample(uint32_t head_dim, uint32_t window, uint32_t calls, int threads,
+                                 double *seconds, double *checksum) {
+    return guard([&] {
+        const uint32_t lanes = 2 * head_dim;
+        std::vector<float> hist(size_t(window) * lanes);
+        for (size_t i = 0; i < hist.size(); ++i)
+            hist[i] = float(int64_t((i * 2654435761ull) % 2001) - 1000) / 1000.0f;
+        std::vector<float> q(head_dim);
+        for (uint32_t d = 0; d < head_dim; ++d)
+            q[d] = float(int(d % 17) - 8) / 8.0f;
+        FarViewConfig cfg;
+        cfg.enabled = true;
+        cfg.near_window = window;
+        cfg.cap = 0;
+        cfg.chunk_tokens = 128;
+        double sum = 0.0;
+        const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for num_threads(threads) schedule(dynamic, 4) reduction(+ : sum)
+        for (int64_t c = 0; c < int64_t(calls); ++c) {
+            TokenReader read = [&](uint64_t tok, float *out) {
+                std::memcpy(out, hist.data() + tok * lanes, lanes * sizeof(float));
+            };
+            SummarizedView v = build_view(read, window, {}, lanes, cfg);
+            auto o = attend(v, q, 0, head_dim);
+            sum += o[c % head_dim];
+        }
+        const auto t1 = std::chrono::steady_clock::now();
+        *seconds = std::chrono::duration<double>(t1 - t0).count();
+        if (checksum)
+            *checksum = sum;
+    });
+}
+
+// Host copy bandwidth of the gather leg (read_slots-style memcpy, 1 thread, like
+// the reference Driver): returns (read + write) GB/s over `bytes`.
+int kvr_ref_cpu_memcpy_gbs(uint64_t bytes, int reps, double *gbs) {
+    return guard([&] {
+        std::vector<std::byte> a(bytes, std::byte{1}), b(bytes);
+        std::memcpy(b.data(), a.data(), bytes);
+        const auto t0 = std::chrono::steady_clock::now();
+        for (int r = 0; r < reps; ++r)
+            std::memcpy(r & 1 ? a.data() : b.data(), r & 1 ? b.data() : a.data(), bytes);
+        const auto t1 = std::chrono::steady_clock::now();
+        *gbs = 2.0 * double(bytes) * reps / std::chrono::duration<double>(t1 - t0).count() / 1e9;
+    });
+}
+
 } // extern "C"

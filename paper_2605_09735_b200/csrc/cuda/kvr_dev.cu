@@ -38,6 +38,7 @@ struct kvr_dev {
     void *h_desc[3] = {nullptr, nullptr, nullptr};
     ScanCounters *h_scan[2] = {nullptr, nullptr};
     cudaEvent_t ev_start[2] = {}, ev_stop[2] = {}, ev_attn[2] = {};
+    cudaEvent_t ev_phase[2][4] = {}; // per ring slot: gather begin/end, attention begin/end
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     AttnPlan *attn = nullptr;
     uint64_t launched[2] = {0, 0};
@@ -85,8 +86,16 @@ DevCtx ctx_for(const kvr_dev *d, int slot) {
     return c;
 }
 
-void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step) {
+// `k` >= 0: record the gather / attention phase events of ring slot k (as
+// event-record nodes when the stream is being captured into the step graph).
+void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, bool capturing = false) {
     cudaStream_t s = d->stream;
+    auto mark = [&](int i) {
+        if (k >= 0)
+            ck(capturing ? cudaEventRecordWithFlags(d->ev_phase[k][i], s, cudaEventRecordExternal)
+                         : cudaEventRecord(d->ev_phase[k][i], s),
+               "phase event");
+    };
     launch_apply(c, s, d->sms);
     launch_write(c, s, d->sms);
     launch_far(c, s, d->sms);
@@ -95,9 +104,13 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step) {
     if (!full_step)
         return;
     launch_scan(c, s);
+    mark(0);
     launch_gather(c, s, d->sms);
+    mark(1);
+    mark(2);
     if (d->g.attention && d->attn)
         launch_attn(d->attn, c, s);
+    mark(3);
 }
 
 } // namespace
@@ -143,6 +156,8 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
             ck(cudaEventCreate(&d->ev_start[i]), "event");
             ck(cudaEventCreate(&d->ev_stop[i]), "event");
             ck(cudaEventCreate(&d->ev_attn[i]), "event");
+            for (int j = 0; j < 4; ++j)
+                ck(cudaEventCreate(&d->ev_phase[i][j]), "event");
         }
         DevCtx &c = d->base;
         c.page_bytes = g.page_bytes;
@@ -239,6 +254,9 @@ int kvr_dev_close(kvr_dev *d) {
             cudaEventDestroy(d->ev_stop[i]);
         if (d->ev_attn[i])
             cudaEventDestroy(d->ev_attn[i]);
+        for (int j = 0; j < 4; ++j)
+            if (d->ev_phase[i][j])
+                cudaEventDestroy(d->ev_phase[i][j]);
         if (d->h_scan[i])
             cudaFreeHost(d->h_scan[i]);
     }
@@ -278,14 +296,14 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
             if (!d->graph[k]) {
                 cudaGraph_t graph;
                 ck(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal), "capture");
-                run_step_kernels(d, c, true);
+                run_step_kernels(d, c, true, int(k), true);
                 ck(cudaStreamEndCapture(d->stream, &graph), "capture end");
                 ck(cudaGraphInstantiate(&d->graph[k], graph, 0), "graph instantiate");
                 cudaGraphDestroy(graph);
             }
             ck(cudaGraphLaunch(d->graph[k], d->stream), "graph launch");
         } else {
-            run_step_kernels(d, c, true);
+            run_step_kernels(d, c, true, int(k), false);
             ck(cudaGetLastError(), "step launch");
         }
         ck(cudaMemcpyAsync(d->h_scan[k], c.scan, sizeof(ScanCounters), cudaMemcpyDeviceToHost, d->stream),
@@ -325,6 +343,11 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
         const ScanCounters &sc = *d->h_scan[k];
         out->step = d->launched[k];
         out->device_ms = ms;
+        float g = 0.f, a = 0.f;
+        ck(cudaEventElapsedTime(&g, d->ev_phase[k][0], d->ev_phase[k][1]), "elapsed");
+        ck(cudaEventElapsedTime(&a, d->ev_phase[k][2], d->ev_phase[k][3]), "elapsed");
+        out->gather_ms = g;
+        out->attn_ms = a;
         out->trains = sc.trains;
         out->descriptors = sc.descriptors;
         out->spans = sc.spans;

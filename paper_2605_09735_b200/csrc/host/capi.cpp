@@ -322,7 +322,8 @@ int kvr_driver_create(const char *config_json, int device, kvr_driver **out) {
             cfg.b200.device = device;
         cfg.validate();
         auto h = std::make_unique<kvr_driver>();
-        h->d = std::make_unique<ScenarioDriver>(cfg, resolve_events(cfg));
+        h->d = std::make_unique<ScenarioDriver>(
+            cfg, shard_events(resolve_events(cfg), cfg.b200.shard_rank, cfg.b200.shard_world));
         h->pager_view.p = h->d->pager();
         *out = h.release();
     });
@@ -332,13 +333,7 @@ int kvr_driver_destroy(kvr_driver *d) {
     return call([&] { delete d; });
 }
 
-int kvr_driver_step(kvr_driver *d, kvr_step_record *o) {
-    return call([&] {
-        if (d->d->done())
-            raise(Errc::bad_config, "all configured steps have run");
-        const StepRecord r = d->d->step();
-        if (!o)
-            return;
+static void fill_record(const StepRecord &r, kvr_step_record *o) {
         std::memset(o, 0, sizeof(*o));
         o->step = r.step;
         o->live_sessions = r.live_sessions;
@@ -356,9 +351,32 @@ int kvr_driver_step(kvr_driver *d, kvr_step_record *o) {
         o->commits = r.commits;
         o->emitted_tokens = r.emitted_tokens;
         o->device_ms = r.device_ms;
+        o->gather_ms = r.gather_ms;
+        o->attn_ms = r.attn_ms;
         o->writeback_tokens = r.writeback_tokens;
         o->gather_bytes = r.gather_bytes;
         o->attn_bytes = r.attn_bytes;
+        o->h2d_bytes = r.h2d_bytes;
+}
+
+int kvr_driver_step(kvr_driver *d, kvr_step_record *o) {
+    return call([&] {
+        if (d->d->done())
+            raise(Errc::bad_config, "all configured steps have run");
+        const StepRecord r = d->d->step();
+        if (o)
+            fill_record(r, o);
+    });
+}
+
+int kvr_driver_record(kvr_driver *d, uint64_t step, kvr_step_record *o) {
+    return call([&] { fill_record(d->d->record(step), o); });
+}
+
+int kvr_driver_sync(kvr_driver *d) {
+    return call([&] {
+        if (d->d->device())
+            d->d->device()->sync();
     });
 }
 

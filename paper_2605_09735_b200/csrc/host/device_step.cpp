@@ -61,6 +61,7 @@ struct DeviceStep::Impl {
     bool have_done[2] = {false, false};
     uint64_t launched_step[2] = {~0ull, ~0ull};
     uint64_t attn_bytes_pending[2] = {0, 0};
+    uint64_t desc_bytes_pending[2] = {0, 0};
 
     bool pending() const {
         return !zero_order.empty() || !cows.empty() || !edits.empty() || !writes.empty() ||
@@ -400,12 +401,15 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
         DeviceStepStats &d = m.done[k];
         d.step = st.step;
         d.device_ms = st.device_ms;
+        d.gather_ms = st.gather_ms;
+        d.attn_ms = st.attn_ms;
         d.trains = st.trains;
         d.descriptors = st.descriptors;
         d.train_bytes = st.train_bytes;
         d.writeback_tokens = st.writeback_tokens;
         d.scan_status = st.status;
         d.attn_bytes = m.attn_bytes_pending[k];
+        d.h2d_bytes = m.desc_bytes_pending[k];
         m.have_done[k] = true;
     }
     uint64_t attn = 0;
@@ -422,6 +426,7 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
     m.launched_step[k] = step;
     m.have_done[k] = false;
     m.attn_bytes_pending[k] = attn;
+    m.desc_bytes_pending[k] = bytes;
     m.clear_wave();
     m.needs.clear();
     m.spans.clear();
@@ -439,18 +444,22 @@ DeviceStepStats DeviceStep::collect(uint64_t step) {
         DeviceStepStats &d = m.done[k];
         d.step = st.step;
         d.device_ms = st.device_ms;
+        d.gather_ms = st.gather_ms;
+        d.attn_ms = st.attn_ms;
         d.trains = st.trains;
         d.descriptors = st.descriptors;
         d.train_bytes = st.train_bytes;
         d.writeback_tokens = st.writeback_tokens;
         d.scan_status = st.status;
         d.attn_bytes = m.attn_bytes_pending[k];
+        d.h2d_bytes = m.desc_bytes_pending[k];
         m.have_done[k] = true;
     }
     return m.done[k];
 }
 
 void DeviceStep::sync() { ck(kvr_dev_sync(impl_->dev)); }
+bool DeviceStep::launched(uint64_t step) const { return impl_->launched_step[step & 1] == step; }
 void DeviceStep::flush() { impl_->flush(); }
 
 void DeviceStep::read_arena(uint64_t offset, uint64_t bytes, void *out) {

@@ -152,6 +152,21 @@ std::vector<TraceEvent> resolve_events(const ScenarioConfig &cfg) {
     return ev;
 }
 
+std::vector<TraceEvent> shard_events(const std::vector<TraceEvent> &events, uint32_t rank,
+                                     uint32_t world) {
+    if (world <= 1)
+        return events;
+    if (rank >= world)
+        raise(Errc::bad_config, "shard rank out of range");
+    std::vector<TraceEvent> out;
+    for (const TraceEvent &e : events)
+        if (e.request_id % world == rank) {
+            out.push_back(e);
+            out.back().request_id = out.size() - 1;
+        }
+    return out;
+}
+
 // ---------------------------------------------------------------------------
 
 struct ScenarioDriver::Impl {
@@ -932,16 +947,22 @@ StepRecord ScenarioDriver::step() {
             const DeviceStepStats ds = m.dev->collect(r.step - 1);
             StepRecord &prev = m.records[r.step - 1];
             prev.device_ms = ds.device_ms;
+            prev.gather_ms = ds.gather_ms;
+            prev.attn_ms = ds.attn_ms;
             prev.writeback_tokens = ds.writeback_tokens;
             prev.gather_bytes = ds.train_bytes;
             prev.attn_bytes = ds.attn_bytes;
+            prev.h2d_bytes = ds.h2d_bytes;
         }
         if (m.t >= m.cfg.steps) {
             const DeviceStepStats ds = m.dev->collect(r.step);
             r.device_ms = ds.device_ms;
+            r.gather_ms = ds.gather_ms;
+            r.attn_ms = ds.attn_ms;
             r.writeback_tokens = ds.writeback_tokens;
             r.gather_bytes = ds.train_bytes;
             r.attn_bytes = ds.attn_bytes;
+            r.h2d_bytes = ds.h2d_bytes;
         }
     }
     m.records.push_back(r);
@@ -949,6 +970,24 @@ StepRecord ScenarioDriver::step() {
 }
 
 bool ScenarioDriver::done() const { return impl_->t >= impl_->cfg.steps; }
+
+const StepRecord &ScenarioDriver::record(uint64_t step) {
+    Impl &m = *impl_;
+    if (step >= m.records.size())
+        raise(Errc::bad_config, "step " + std::to_string(step) + " has not run");
+    StepRecord &r = m.records[step];
+    if (m.dev && r.device_ms == 0.0 && m.dev->launched(step)) {
+        const DeviceStepStats ds = m.dev->collect(step);
+        r.device_ms = ds.device_ms;
+        r.gather_ms = ds.gather_ms;
+        r.attn_ms = ds.attn_ms;
+        r.writeback_tokens = ds.writeback_tokens;
+        r.gather_bytes = ds.train_bytes;
+        r.attn_bytes = ds.attn_bytes;
+        r.h2d_bytes = ds.h2d_bytes;
+    }
+    return r;
+}
 uint64_t ScenarioDriver::steps_done() const { return impl_->t; }
 const ScenarioConfig &ScenarioDriver::config() const { return impl_->cfg; }
 const std::vector<StepRecord> &ScenarioDriver::records() const { return impl_->records; }
@@ -1223,6 +1262,8 @@ static ScenarioConfig config_from_json(const ojson &j) {
         take(p, "max_tokens", c.b200.max_tokens);
         take(p, "graph", c.b200.graph);
         take(p, "check", c.b200.check);
+        take(p, "shard_rank", c.b200.shard_rank);
+        take(p, "shard_world", c.b200.shard_world);
     }
     return c;
 }

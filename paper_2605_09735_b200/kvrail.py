@@ -146,8 +146,9 @@ class StepRecord(C.Structure):
                 ("step_latency", C.c_double), ("reserved_bytes", C.c_uint64),
                 ("active_bytes", C.c_uint64), ("commits", C.c_uint32), ("pad_", C.c_uint32),
                 ("emitted_tokens", C.c_uint64), ("device_ms", C.c_double),
+                ("gather_ms", C.c_double), ("attn_ms", C.c_double),
                 ("writeback_tokens", C.c_uint64), ("gather_bytes", C.c_uint64),
-                ("attn_bytes", C.c_uint64)]
+                ("attn_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64)]
 
 
 class Geometry(C.Structure):
@@ -260,6 +261,8 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_driver_create": [C.c_char_p, C.c_int, C.POINTER(vp)],
         "kvr_driver_destroy": [vp],
         "kvr_driver_step": [vp, C.POINTER(StepRecord)],
+        "kvr_driver_record": [vp, C.c_uint64, C.POINTER(StepRecord)],
+        "kvr_driver_sync": [vp],
         "kvr_driver_progress": [vp, U64P, U64P],
         "kvr_driver_steps_csv": [vp, C.c_char_p, C.c_uint64, U64P],
         "kvr_driver_report_json": [vp, C.c_char_p, C.c_uint64, U64P],
@@ -612,6 +615,15 @@ class Driver:
         r = StepRecord()
         check(native_lib().kvr_driver_step(self.h, C.byref(r)))
         return r
+
+    def record(self, step: int) -> StepRecord:
+        """Record of an executed step with its device measurements."""
+        r = StepRecord()
+        check(native_lib().kvr_driver_record(self.h, step, C.byref(r)))
+        return r
+
+    def sync(self):
+        check(native_lib().kvr_driver_sync(self.h))
 
     def progress(self) -> tuple[int, int]:
         a, b = C.c_uint64(), C.c_uint64()
