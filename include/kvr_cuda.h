@@ -59,6 +59,7 @@ typedef struct kvr_step_header {
     double max_hold;        /* TransportConfig::max_hold */
     uint32_t merge;
     uint32_t n_zero, n_cow, n_edit, n_write, n_blob, n_need, n_span, n_prime, n_far_ids;
+    uint32_t n_far_jobs;    /* source-1 ops: the last n_far_jobs of the n_write ops */
     uint64_t write_tokens;  /* sum of kvr_write_op.count over source-0 writes */
     uint64_t off_zero, off_cow, off_edit, off_write, off_blob_ops, off_blob, off_need, off_span,
         off_prime, off_far_ids, off_slots;

@@ -181,10 +181,11 @@ __device__ inline double load_lane(const DevCtx &c, const uint8_t *p, uint64_t l
 
 __global__ void k_far(DevCtx c) {
     const kvr_step_header *h = hdr(c);
-    const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write);
+    // far jobs are packed after the token writes
+    const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write) + (h->n_write - h->n_far_jobs);
     const uint64_t lanes = c.token_bytes / c.esz;
     const uint64_t lane_blocks = (lanes + blockDim.x - 1) / blockDim.x;
-    const uint64_t work = uint64_t(h->n_write) * lane_blocks;
+    const uint64_t work = uint64_t(h->n_far_jobs) * lane_blocks;
     for (uint64_t u = blockIdx.x; u < work; u += gridDim.x) {
         const kvr_write_op op = ops[u / lane_blocks];
         if (op.source != 1)

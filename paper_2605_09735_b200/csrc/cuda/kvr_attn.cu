@@ -26,7 +26,7 @@ namespace kvr {
 namespace {
 
 constexpr int kTile = 32; // tokens per tile (one per lane)
-constexpr int kMaxG = 4;  // kv heads per CTA (one consumer warp each)
+constexpr int kMaxG = 4;  // kv heads per CTA (a pair of consumer warps each)
 
 __device__ inline uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ inline void mbar_init(uint64_t *bar, uint32_t count) {
@@ -95,97 +95,139 @@ __device__ inline float warp_sum(float v) {
     return v;
 }
 
-template <typename T, int HD, int QG> struct Acc {
-    static constexpr int DPL = HD / 32; // output dims per lane
-    float m[QG], lsum[QG], acc[QG][DPL];
-    __device__ void init() {
-#pragma unroll
-        for (int q = 0; q < QG; ++q) {
-            m[q] = -INFINITY;
-            lsum[q] = 0.f;
-#pragma unroll
-            for (int k = 0; k < DPL; ++k)
-                acc[q][k] = 0.f;
+// DPL consecutive elements of a row as floats (lane <-> head dims).
+template <typename T, int N> __device__ inline void load_dims(const T *p, float (&o)[N]) {
+    if constexpr (sizeof(T) == 4) {
+        if constexpr (N == 4) {
+            const float4 v = *reinterpret_cast<const float4 *>(p);
+            o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+        } else if constexpr (N == 2) {
+            const float2 v = *reinterpret_cast<const float2 *>(p);
+            o[0] = v.x, o[1] = v.y;
+        } else {
+            o[0] = *p;
+        }
+    } else {
+        if constexpr (N == 4) {
+            const uint2 v = *reinterpret_cast<const uint2 *>(p);
+            const float2 a = Pair<T>::f2(v.x), b = Pair<T>::f2(v.y);
+            o[0] = a.x, o[1] = a.y, o[2] = b.x, o[3] = b.y;
+        } else if constexpr (N == 2) {
+            const float2 a = Pair<T>::f2(*reinterpret_cast<const uint32_t *>(p));
+            o[0] = a.x, o[1] = a.y;
+        } else {
+            o[0] = float(*p);
         }
     }
-    // One 32-row block: lane r scores row r (krow, nullptr when masked) and the
-    // warp then accumulates rows' V (vrow of row r fetched via shuffle).
-    __device__ void block(const T *krow, const T *vrow_lane, bool valid, const T *qs, float scale_log2) {
+}
+
+constexpr int kHalf = 16; // tokens per consumer warp per tile
+
+/// Online-softmax state of one consumer warp for QG q-heads sharing one kv head.
+/// QK^T: lane <-> head dims (q kept in registers), the 16 per-token partial dot
+/// products are reduce-scattered across the warp by a halving butterfly so lane
+/// l ends with the score of token l >> 1. PV: lane <-> head dims, the token
+/// probabilities are broadcast with shuffles.
+template <typename T, int HD, int QG> struct Attn {
+    static constexpr int DPL = HD / 32;
+    float q[QG][DPL];
+    float m[QG], lsum[QG], acc[QG][DPL];
+
+    __device__ void init(const float *qsrc) { // qsrc: [QG][HD] floats
         const int lane = threadIdx.x & 31;
+#pragma unroll
+        for (int g = 0; g < QG; ++g) {
+            m[g] = -INFINITY;
+            lsum[g] = 0.f;
+#pragma unroll
+            for (int k = 0; k < DPL; ++k) {
+                q[g][k] = qsrc[g * HD + DPL * lane + k];
+                acc[g][k] = 0.f;
+            }
+        }
+    }
+
+    // 16 rows: row(r) -> K row pointer (V row = + v_off elements); valid bit r of `mask`.
+    template <typename RowFn>
+    __device__ void block(RowFn row, uint32_t v_off, uint32_t mask, float scale_log2) {
+        const int lane = threadIdx.x & 31;
+        float part[QG][kHalf];
+#pragma unroll
+        for (int r = 0; r < kHalf; ++r) {
+            float k[DPL];
+            if (mask >> r & 1u) {
+                load_dims<T, DPL>(row(r) + DPL * lane, k);
+            } else {
+#pragma unroll
+                for (int i = 0; i < DPL; ++i)
+                    k[i] = 0.f;
+            }
+#pragma unroll
+            for (int g = 0; g < QG; ++g) {
+                float a = 0.f;
+#pragma unroll
+                for (int i = 0; i < DPL; ++i)
+                    a = fmaf(q[g][i], k[i], a);
+                part[g][r] = a;
+            }
+        }
+        // halving butterfly: 16 values -> 1 per lane (token lane >> 1)
         float s[QG];
 #pragma unroll
-        for (int q = 0; q < QG; ++q)
-            s[q] = 0.f;
-        if (valid) {
-            float s2[QG];
+        for (int g = 0; g < QG; ++g) {
 #pragma unroll
-            for (int q = 0; q < QG; ++q)
-                s2[q] = 0.f;
-#pragma unroll 8
-            for (int cc = 0; cc < HD / 2; ++cc) {
-                const int d = 2 * ((cc + lane) & (HD / 2 - 1)); // rotated: conflict-free banks
-                const float2 k = load_pair<T>(krow + d);
+            for (int w = kHalf / 2, bit = 16; w >= 1; w >>= 1, bit >>= 1) {
+                const bool hi = lane & bit;
 #pragma unroll
-                for (int q = 0; q < QG; ++q) {
-                    const float2 qq = load_pair<T>(qs + q * HD + d);
-                    s[q] = fmaf(k.x, qq.x, s[q]);
-                    s2[q] = fmaf(k.y, qq.y, s2[q]);
+                for (int j = 0; j < w; ++j) {
+                    const float send = hi ? part[g][j] : part[g][j + w];
+                    const float keep = hi ? part[g][j + w] : part[g][j];
+                    part[g][j] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
                 }
             }
-#pragma unroll
-            for (int q = 0; q < QG; ++q)
-                s[q] = (s[q] + s2[q]) * scale_log2;
+            s[g] = (part[g][0] + __shfl_xor_sync(0xffffffffu, part[g][0], 1)) * scale_log2;
         }
+        const bool valid = mask >> (lane >> 1) & 1u;
         float p[QG];
 #pragma unroll
-        for (int q = 0; q < QG; ++q) {
-            const float sv = valid ? s[q] : -INFINITY;
-            const float mt = warp_max(sv);
-            const float mn = fmaxf(m[q], mt);
-            const float alpha = mn == -INFINITY ? 1.f : exp2f(m[q] - mn);
-            p[q] = valid ? exp2f(sv - mn) : 0.f;
-            lsum[q] = lsum[q] * alpha + p[q];
-            m[q] = mn;
+        for (int g = 0; g < QG; ++g) {
+            const float sv = valid ? s[g] : -INFINITY;
+            const float mn = fmaxf(m[g], warp_max(sv));
+            const float alpha = mn == -INFINITY ? 1.f : exp2f(m[g] - mn);
+            p[g] = valid ? exp2f(sv - mn) : 0.f;
+            lsum[g] = lsum[g] * alpha + ((lane & 1) ? 0.f : p[g]);
+            m[g] = mn;
 #pragma unroll
-            for (int k = 0; k < DPL; ++k)
-                acc[q][k] *= alpha;
+            for (int i = 0; i < DPL; ++i)
+                acc[g][i] *= alpha;
         }
-        const uint64_t vaddr = reinterpret_cast<uint64_t>(vrow_lane);
-#pragma unroll 4
-        for (int r = 0; r < 32; ++r) {
-            const T *vr = reinterpret_cast<const T *>(__shfl_sync(0xffffffffu, vaddr, r));
-            if (!vr) // masked row (warp-uniform)
-                continue;
+#pragma unroll
+        for (int r = 0; r < kHalf; ++r) {
+            if (!(mask >> r & 1u))
+                continue; // warp-uniform
             float v[DPL];
+            load_dims<T, DPL>(row(r) + v_off + DPL * lane, v);
 #pragma unroll
-            for (int k = 0; k < DPL; k += 2) {
-                if constexpr (DPL == 1) {
-                    v[0] = float(vr[lane]);
-                } else {
-                    const float2 x = load_pair<T>(vr + DPL * lane + k);
-                    v[k] = x.x;
-                    v[k + 1] = x.y;
-                }
-            }
+            for (int g = 0; g < QG; ++g) {
+                const float pr = __shfl_sync(0xffffffffu, p[g], 2 * r);
 #pragma unroll
-            for (int q = 0; q < QG; ++q) {
-                const float pr = __shfl_sync(0xffffffffu, p[q], r);
-#pragma unroll
-                for (int k = 0; k < DPL; ++k)
-                    acc[q][k] = fmaf(pr, v[k], acc[q][k]);
+                for (int i = 0; i < DPL; ++i)
+                    acc[g][i] = fmaf(pr, v[i], acc[g][i]);
             }
         }
     }
 };
 
 template <typename T, int HD, int QG>
-__global__ void __launch_bounds__(32 * (kMaxG + 1), 1)
+__global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
     k_attn(DevCtx c, const __grid_constant__ CUtensorMap ring_map, uint32_t G, uint32_t stages) {
+    using A = Attn<T, HD, QG>;
+    constexpr int DPL = A::DPL;
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t tile_elems = kTile * G * HD;
-    T *tiles = reinterpret_cast<T *>(smem);                       // [stages][K|V][32][G][HD]
-    T *qsm = tiles + size_t(stages) * 2 * tile_elems;             // [kMaxG][QG][HD]
-    uint64_t *full = reinterpret_cast<uint64_t *>(qsm + kMaxG * QG * HD);
+    T *tiles = reinterpret_cast<T *>(smem);                                  // [stages][K|V][32][G][HD]
+    float *xchg = reinterpret_cast<float *>(tiles + size_t(stages) * 2 * tile_elems); // pair merge
+    uint64_t *full = reinterpret_cast<uint64_t *>(xchg + kMaxG * 32 * QG * (2 + DPL));
     uint64_t *empty = full + stages;
 
     const kvr_step_header *h = hdr(c);
@@ -198,7 +240,7 @@ __global__ void __launch_bounds__(32 * (kMaxG + 1), 1)
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], G);
+            mbar_init(&empty[s], 2 * G);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -211,7 +253,7 @@ __global__ void __launch_bounds__(32 * (kMaxG + 1), 1)
         n_tiles = w > t0 ? uint32_t((w - t0 + kTile - 1) / kTile) : 0;
     };
 
-    if (warp == kMaxG) { // ---------------- producer ----------------
+    if (warp == 2 * kMaxG) { // ---------------- producer: TMA tile loads ----------------
         if (lane != 0)
             return;
         asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
@@ -230,8 +272,8 @@ __global__ void __launch_bounds__(32 * (kMaxG + 1), 1)
                 T *kt = tiles + size_t(s) * 2 * tile_elems;
                 mbar_expect_tx(&full[s], bytes);
                 tma_load_4d(kt, &ring_map, 0, int(hg * G), row0, int(slot * c.L + l), &full[s]);
-                tma_load_4d(kt + tile_elems, &ring_map, 0, int(c.Hkv + hg * G), row0, int(slot * c.L + l),
-                            &full[s]);
+                tma_load_4d(kt + tile_elems, &ring_map, 0, int(c.Hkv + hg * G), row0,
+                            int(slot * c.L + l), &full[s]);
                 if (++s == stages) {
                     s = 0;
                     phase ^= 1;
@@ -240,56 +282,47 @@ __global__ void __launch_bounds__(32 * (kMaxG + 1), 1)
         }
         return;
     }
-    if (uint32_t(warp) >= G)
+    const uint32_t head_local = uint32_t(warp) >> 1, half = uint32_t(warp) & 1u;
+    if (head_local >= G)
         return;
 
-    // ---------------- consumers: warp `warp` owns kv head hg*G + warp ----------------
+    // ---------- consumers: warp pair (2h, 2h+1) owns kv head hg*G + h; each takes 16 rows ----------
     const float scale_log2 = 1.4426950408889634f / sqrtf(float(HD));
-    T *qs = qsm + warp * QG * HD;
+    float *mine = xchg + size_t(head_local) * 32 * QG * (2 + DPL);
     uint32_t s = 0, phase = 0;
     for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const uint32_t hg = it % groups, l = (it / groups) % c.L, slot = it / (groups * c.L);
         const kvr_slot_state st = slots[slot];
         if (!st.live)
             continue;
-        const uint32_t kvh = hg * G + warp;
+        const uint32_t kvh = hg * G + head_local;
         uint64_t lo, t0;
         uint32_t n_tiles;
         window(slot, lo, t0, n_tiles);
         const uint64_t w = st.written;
-        // queries of this kv head's group, rounded to T (exact: they were rounded already)
-        const float *qg = c.q + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD;
-        for (int i = lane; i < QG * HD / 2; i += 32) {
-            const float a = qg[2 * i], b = qg[2 * i + 1];
-            if constexpr (sizeof(T) == 4) {
-                reinterpret_cast<float2 *>(qs)[i] = make_float2(a, b);
-            } else {
-                reinterpret_cast<uint32_t *>(qs)[i] = Pair<T>::pack(a, b);
-            }
-        }
-        __syncwarp();
-        Acc<T, HD, QG> acc;
-        acc.init();
-        // far summaries (few rows; read straight from global)
+        A at;
+        at.init(c.q + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD);
+        // far summaries: rows straight from global memory
         const T *far_base = reinterpret_cast<const T *>(c.far) +
                             (uint64_t(slot) * c.L + l) * c.max_chunks * c.row_elems + uint64_t(kvh) * HD;
-        for (uint32_t f0 = 0; f0 < st.far_count; f0 += 32) {
-            const bool valid = f0 + lane < st.far_count;
-            const T *krow = nullptr, *vrow = nullptr;
-            if (valid) {
-                krow = far_base + uint64_t(far_ids[st.far_begin + f0 + lane]) * c.row_elems;
-                vrow = krow + c.d_kv;
-            }
-            acc.block(krow, vrow, valid, qs, scale_log2);
+        for (uint32_t f0 = half * kHalf; f0 < st.far_count; f0 += 2 * kHalf) {
+            const uint32_t n = min(uint32_t(kHalf), st.far_count - f0);
+            const uint32_t mask = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
+            const uint32_t *ids = far_ids + st.far_begin + f0;
+            at.block([&](int r) { return far_base + uint64_t(ids[r < int(n) ? r : 0]) * c.row_elems; },
+                     c.d_kv, mask, scale_log2);
         }
         // near window tiles from the TMA pipeline
         for (uint32_t k = 0; k < n_tiles; ++k) {
             mbar_wait(&full[s], phase);
             const T *kt = tiles + size_t(s) * 2 * tile_elems;
-            const uint64_t tok = t0 + uint64_t(k) * kTile + lane;
-            const bool valid = tok >= lo && tok < w;
-            const T *krow = kt + (size_t(lane) * G + warp) * HD;
-            acc.block(krow, valid ? krow + tile_elems : nullptr, valid, qs, scale_log2);
+            const uint64_t tok0 = t0 + uint64_t(k) * kTile + half * kHalf;
+            uint32_t mask = 0;
+#pragma unroll
+            for (int r = 0; r < kHalf; ++r)
+                mask |= uint32_t(tok0 + r >= lo && tok0 + r < w) << r;
+            const T *base = kt + (size_t(half) * kHalf * G + head_local) * HD;
+            at.block([&](int r) { return base + size_t(r) * G * HD; }, tile_elems, mask, scale_log2);
             __syncwarp();
             if (lane == 0)
                 mbar_arrive(&empty[s]);
@@ -298,19 +331,40 @@ __global__ void __launch_bounds__(32 * (kMaxG + 1), 1)
                 phase ^= 1;
             }
         }
-        // finalize
-        float *o = c.out + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD;
+        // merge the pair's states, then normalise
+        const uint32_t bar = 1 + head_local;
+        if (half) {
 #pragma unroll
-        for (int q = 0; q < QG; ++q) {
-            const float z = warp_sum(acc.lsum[q]);
-            const float inv = z > 0.f ? 1.f / z : 0.f;
+            for (int g = 0; g < QG; ++g) {
+                mine[(g * (2 + DPL) + 0) * 32 + lane] = at.m[g];
+                mine[(g * (2 + DPL) + 1) * 32 + lane] = at.lsum[g];
 #pragma unroll
-            for (int k = 0; k < Acc<T, HD, QG>::DPL; ++k)
-                o[q * HD + Acc<T, HD, QG>::DPL * lane + k] = acc.acc[q][k] * inv;
+                for (int i = 0; i < DPL; ++i)
+                    mine[(g * (2 + DPL) + 2 + i) * 32 + lane] = at.acc[g][i];
+            }
         }
-        __syncwarp();
+        asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+        if (!half) {
+            float *o = c.out + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD;
+#pragma unroll
+            for (int g = 0; g < QG; ++g) {
+                const float m1 = mine[(g * (2 + DPL) + 0) * 32 + lane];
+                const float l1 = mine[(g * (2 + DPL) + 1) * 32 + lane];
+                const float mn = fmaxf(at.m[g], m1);
+                const float a0 = mn == -INFINITY ? 0.f : exp2f(at.m[g] - mn);
+                const float a1 = mn == -INFINITY ? 0.f : exp2f(m1 - mn);
+                const float z = warp_sum(at.lsum[g] * a0 + l1 * a1);
+                const float inv = z > 0.f ? 1.f / z : 0.f;
+#pragma unroll
+                for (int i = 0; i < DPL; ++i)
+                    o[g * HD + DPL * lane + i] =
+                        (at.acc[g][i] * a0 + mine[(g * (2 + DPL) + 2 + i) * 32 + lane] * a1) * inv;
+            }
+        }
+        asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
     }
 }
+
 
 using AttnFn = void (*)(DevCtx, const CUtensorMap, uint32_t, uint32_t);
 
@@ -362,7 +416,8 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device) {
         }
     const size_t stage = 2 * kTile * p->G * row;
     p->stages = stage * 3 <= (200u << 10) ? 3 : 2;
-    p->smem = p->stages * stage + size_t(kMaxG) * c.group * c.hd * c.esz + 2 * p->stages * 8 + 16;
+    p->smem = p->stages * stage + size_t(kMaxG) * 32 * c.group * (2 + c.hd / 32) * 4 +
+              2 * p->stages * 8 + 16;
     p->grid = uint32_t(sms);
     cudaFuncSetAttribute(p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem));
 
@@ -396,7 +451,7 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device) {
 }
 
 void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s) {
-    p->fn<<<p->grid, 32 * (kMaxG + 1), p->smem, s>>>(c, p->map, p->G, p->stages);
+    p->fn<<<p->grid, 32 * (2 * kMaxG + 1), p->smem, s>>>(c, p->map, p->G, p->stages);
 }
 
 void free_attn_plan(AttnPlan *p) { delete p; }

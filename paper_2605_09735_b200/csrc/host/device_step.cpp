@@ -125,6 +125,7 @@ struct DeviceStep::Impl {
         h.n_edit = uint32_t(edits.size());
         h.off_edit = place(edits.size() * sizeof(kvr_edit_op));
         h.n_write = uint32_t(all_writes.size());
+        h.n_far_jobs = uint32_t(far_jobs.size());
         h.off_write = place(all_writes.size() * sizeof(kvr_write_op));
         h.n_blob = uint32_t(blob_ops.size());
         h.off_blob_ops = place(blob_ops.size() * sizeof(kvr_blob_op));
