@@ -87,6 +87,8 @@ public:
     void read_attention(uint32_t slot, float *out); // [L][Hq][hd]
     void read_query(uint32_t slot, float *out);     // [L][Hq][hd]
     void read_far_row(uint32_t slot, uint64_t chunk, void *out); // token image of a far row
+    /// Far chunks the last launched step showed to the attention of `slot`.
+    std::vector<uint64_t> far_selection_of(uint32_t slot) const;
     /// Last K-scan result: trains (desc_begin/count index `descs`).
     void read_scan(std::vector<kvr_train> &trains, std::vector<kvr_descriptor> &descs);
 

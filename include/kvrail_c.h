@@ -57,6 +57,9 @@ enum {
 
 /* Thread-local message of the last failing call ("<ErrcName>: msg"). */
 const char *kvr_last_error(void);
+/* sizeof of every POD struct of kvrail_c.h and kvr_cuda.h, in declaration
+ * order (FFI layout self-check); *n = number of structs. */
+int kvr_abi_struct_sizes(uint64_t *out, uint64_t cap, uint64_t *n);
 /* kvrail::errc_name (types.cpp:20-46) for a status code (code - 1). */
 const char *kvr_errc_name(int status);
 
@@ -330,6 +333,9 @@ int kvr_device_read_page_table(kvr_device *d, uint32_t slot, uint64_t tok_begin,
 int kvr_device_read_attention(kvr_device *d, uint32_t slot, float *out);
 int kvr_device_read_query(kvr_device *d, uint32_t slot, float *out);
 int kvr_device_read_far_row(kvr_device *d, uint32_t slot, uint64_t chunk, void *out);
+/* far chunks (select_chunks, far_view.cpp:49-62) the last step showed slot's attention */
+int kvr_device_far_selection(kvr_device *d, uint32_t slot, uint64_t *out, uint64_t cap,
+                             uint64_t *n_out);
 int kvr_device_read_scan(kvr_device *d, kvr_train *trains, uint64_t train_cap, uint64_t *n_trains,
                          kvr_descriptor *descs, uint64_t desc_cap, uint64_t *n_descs);
 

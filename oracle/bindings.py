@@ -144,6 +144,14 @@ def check_driver_window_and_attention(driver, far_images_of=None) -> float:
             got = dev.ring_token(slot, t)
             assert got == want, f"window ring mismatch slot {slot} token {t}"
             window += want
+        # far summaries the attention saw: device far rows == the arena summary slots
+        far = dev.far_selection(slot)
+        far_imgs = []
+        for chunk in far:
+            row = dev.far_row(slot, chunk)
+            assert row == token_bytes_via_view(pager, view, (1 << 40) + chunk, tb), \
+                f"far row {chunk} of slot {slot} differs from its summary slot"
+            far_imgs += as_floats(row, g.elem_kind)
         q_dev = dev.query(slot)
         out = dev.attention(slot)
         for layer in range(g.layers):
@@ -152,6 +160,16 @@ def check_driver_window_and_attention(driver, far_images_of=None) -> float:
                 q = fill_query(g.seed, session, step, layer, qh, g.head_dim, g.elem_kind)
                 assert q == q_dev[base:base + g.head_dim], "device query differs from the oracle"
                 want = attend_window(window, written - lo, g.layers, g.kv_heads, g.head_dim,
-                                     g.elem_kind, layer, qh // group, q)
+                                     g.elem_kind, layer, qh // group, q, far_imgs, len(far))
                 worst = max(worst, rel_error(out[base:base + g.head_dim], want))
     return worst
+
+
+def as_floats(raw: bytes, elem_kind: int) -> list[float]:
+    import numpy as np
+    if elem_kind == 0:
+        return np.frombuffer(raw, np.float32).tolist()
+    if elem_kind == 1:
+        return np.frombuffer(raw, np.float16).astype(np.float32).tolist()
+    u = np.frombuffer(raw, np.uint16).astype(np.uint32) << 16
+    return u.view(np.float32).tolist()

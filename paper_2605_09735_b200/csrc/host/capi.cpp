@@ -82,6 +82,25 @@ extern "C" {
 
 const char *kvr_last_error(void) { return g_msg.c_str(); }
 
+int kvr_abi_struct_sizes(uint64_t *out, uint64_t cap, uint64_t *n) {
+    const uint64_t sz[] = {
+        sizeof(kvr_pager_config), sizeof(kvr_token_range), sizeof(kvr_view_entry),
+        sizeof(kvr_view_info),    sizeof(kvr_reserved_block), sizeof(kvr_arena_stats),
+        sizeof(kvr_work_counters), sizeof(kvr_free_run),   sizeof(kvr_frame_delta),
+        sizeof(kvr_staged_span),  sizeof(kvr_stage_need),  sizeof(kvr_descriptor),
+        sizeof(kvr_transport_config), sizeof(kvr_train),   sizeof(kvr_step_record),
+        sizeof(kvr_geometry),     sizeof(kvr_step_header), sizeof(kvr_zero_op),
+        sizeof(kvr_cow_op),       sizeof(kvr_edit_op),     sizeof(kvr_write_op),
+        sizeof(kvr_blob_op),      sizeof(kvr_need_rec),    sizeof(kvr_span_rec),
+        sizeof(kvr_prime_op),     sizeof(kvr_slot_state),  sizeof(kvr_step_stats),
+    };
+    const uint64_t k = sizeof(sz) / sizeof(sz[0]);
+    for (uint64_t i = 0; out && i < k && i < cap; ++i)
+        out[i] = sz[i];
+    *n = k;
+    return KVR_OK;
+}
+
 const char *kvr_errc_name(int status) {
     if (status == KVR_OK)
         return "Ok";
@@ -477,6 +496,15 @@ int kvr_device_read_query(kvr_device *d, uint32_t slot, float *out) {
 }
 int kvr_device_read_far_row(kvr_device *d, uint32_t slot, uint64_t chunk, void *out) {
     return call([&] { DS->read_far_row(slot, chunk, out); });
+}
+int kvr_device_far_selection(kvr_device *d, uint32_t slot, uint64_t *out, uint64_t cap,
+                             uint64_t *n_out) {
+    return call([&] {
+        const auto v = DS->far_selection_of(slot);
+        for (uint64_t i = 0; out && i < v.size() && i < cap; ++i)
+            out[i] = v[i];
+        *n_out = v.size();
+    });
 }
 int kvr_device_read_scan(kvr_device *d, kvr_train *trains, uint64_t train_cap, uint64_t *n_trains,
                          kvr_descriptor *descs, uint64_t desc_cap, uint64_t *n_descs) {

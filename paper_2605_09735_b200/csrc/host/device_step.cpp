@@ -54,6 +54,7 @@ struct DeviceStep::Impl {
     std::vector<kvr_prime_op> primes;
     std::vector<uint32_t> far_ids;
     std::vector<kvr_slot_state> slots;
+    std::vector<std::vector<uint64_t>> far_shown; // per slot, as of the last launch
     // state
     std::vector<uint8_t> clean; // page known to be all zeros on the device
     std::unordered_map<SessionId, uint32_t> bound;
@@ -420,6 +421,10 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
             if (s.live)
                 attn += (std::min<uint64_t>(s.written, m.g.near_window) + s.far_count) * m.g.layers * row;
     }
+    m.far_shown.assign(m.slots.size(), {});
+    for (size_t s = 0; s < m.slots.size(); ++s)
+        for (uint32_t i = 0; i < m.slots[s].far_count; ++i)
+            m.far_shown[s].push_back(m.far_ids[m.slots[s].far_begin + i]);
     void *buf = nullptr;
     ck(kvr_dev_desc_buffer(m.dev, k, &buf));
     const uint64_t bytes = m.pack(buf, step, now, &tc, true);
@@ -501,6 +506,10 @@ void DeviceStep::read_far_row(uint32_t slot, uint64_t chunk, void *out) {
         const uint64_t off = ((uint64_t(slot) * g.layers + l) * g.max_chunks + chunk) * row;
         ck(kvr_dev_read(impl_->dev, KVR_BUF_FAR, off, row, static_cast<uint8_t *>(out) + l * row));
     }
+}
+
+std::vector<uint64_t> DeviceStep::far_selection_of(uint32_t slot) const {
+    return slot < impl_->far_shown.size() ? impl_->far_shown[slot] : std::vector<uint64_t>{};
 }
 
 void DeviceStep::read_scan(std::vector<kvr_train> &trains, std::vector<kvr_descriptor> &descs) {

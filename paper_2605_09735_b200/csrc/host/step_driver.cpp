@@ -158,12 +158,19 @@ std::vector<TraceEvent> shard_events(const std::vector<TraceEvent> &events, uint
         return events;
     if (rank >= world)
         raise(Errc::bad_config, "shard rank out of range");
+    // A shard is the trace replay of its sub-stream: ids renumbered, arrivals
+    // rebased to the shard's first request (resolve_events, scenario.cpp:86-90).
     std::vector<TraceEvent> out;
     for (const TraceEvent &e : events)
         if (e.request_id % world == rank) {
             out.push_back(e);
             out.back().request_id = out.size() - 1;
         }
+    if (!out.empty()) {
+        const uint64_t t0 = out.front().arrival_ms;
+        for (TraceEvent &e : out)
+            e.arrival_ms -= t0;
+    }
     return out;
 }
 

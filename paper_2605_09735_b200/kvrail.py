@@ -283,6 +283,7 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_device_read_attention": [vp, C.c_uint32, C.POINTER(C.c_float)],
         "kvr_device_read_query": [vp, C.c_uint32, C.POINTER(C.c_float)],
         "kvr_device_read_far_row": [vp, C.c_uint32, C.c_uint64, C.c_void_p],
+        "kvr_device_far_selection": [vp, C.c_uint32, U64P, C.c_uint64, U64P],
         "kvr_device_read_scan": [vp, C.POINTER(Train), C.c_uint64, U64P, C.POINTER(Descriptor),
                                  C.c_uint64, U64P],
         "kvr_dev_count": [C.POINTER(C.c_int)],
@@ -349,7 +350,7 @@ class Pager:
         return [(buf[i].block, buf[i].token_capacity) for i in range(n.value)]
 
     def reserve_range(self, s: int, begin: int, end: int):
-        cap = (end - begin) // max(1, self.cfg.tokens_per_page()) + 2
+        cap = max(0, end - begin) // max(1, self.cfg.tokens_per_page()) + 2
         buf = (ReservedBlock * cap)()
         n = C.c_uint64()
         self.api.pager_reserve_range(self.h, s, TokenRange(begin, end), buf, cap, C.byref(n))
@@ -544,6 +545,12 @@ class Device:
         buf = C.create_string_buffer(self.geometry.token_bytes)
         check(native_lib().kvr_device_read_far_row(self.h, slot, chunk, buf))
         return buf.raw
+
+    def far_selection(self, slot: int) -> list[int]:
+        buf = (C.c_uint64 * 4096)()
+        n = C.c_uint64()
+        check(native_lib().kvr_device_far_selection(self.h, slot, buf, 4096, C.byref(n)))
+        return list(buf)[:n.value]
 
     def page_table(self, slot: int, begin: int, count: int):
         buf = (C.c_uint32 * max(1, count))()

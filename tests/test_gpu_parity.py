@@ -1,0 +1,154 @@
+"""B200 parity: the device path against the reference, end to end.
+
+* Reference-byte payload ("bytes", scenario.cpp:193-206) generated on the GPU:
+  the per-step trace — which hashes the bytes of every staged train read back
+  from the DEVICE arena, and digests the whole pager — must equal the trace the
+  reference recorded (tests/golden), step for step.
+* b200.check: the device K-scan (stage + reduce on the GPU) must equal the host
+  reduce() on every step.
+* The window ring must hold exactly the arena bytes of every live slot's last
+  min(written, W*) tokens; far rows must equal their summary slots (K-far is
+  bit-exact with far_view.cpp:36-46); attention must be within 1e-3 of the
+  double-precision oracle (kvr_oracle.c, restating far_view.cpp:113-155).
+"""
+import copy
+import json
+import os
+
+import pytest
+
+from paper_2605_09735_b200 import kvrail as kv
+from oracle import bindings as ob
+
+pytestmark = pytest.mark.gpu
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def read(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return f.read()
+
+
+def run(cfg, **b200):
+    c = copy.deepcopy(cfg)
+    c.setdefault("b200", {}).update(dict(trace=True, check=True), **b200)
+    d = kv.Driver(c, device=0)
+    d.run()
+    return d
+
+
+def assert_scan_exact(d, steps):
+    checked, bad, first = d.device_check()
+    assert checked == steps and bad == 0, first
+
+
+def c1():
+    cfg = json.loads(read("c1_config.json"))
+    cfg["trace_path"] = os.path.join(GOLD, "c1_events.csv")
+    return cfg
+
+
+def test_c1_reference_bytes_on_device():
+    d = run(c1(), kv_heads=4, head_dim=64, payload="bytes", attention=False)
+    assert d.trace() == read("c1_trace.txt")
+    assert d.steps_csv() == read("c1_steps.csv")
+    assert_scan_exact(d, 64)
+
+
+@pytest.mark.parametrize("name", ["audit", "adv_burst"])
+def test_golden_scenarios_on_device(name):
+    cfg = json.loads(read(f"{name}_config.json"))
+    d = run(cfg, payload="bytes", attention=False)
+    assert d.trace() == read(f"{name}_trace.txt")
+    assert_scan_exact(d, cfg["steps"])
+
+
+def test_far_view_fp32_on_device():
+    """Far summaries computed by K-far equal the reference's (hashed in the
+    trace through the far trains), and attention over [far..., near...] holds."""
+    cfg = json.loads(read("far_config.json"))
+    d = run(cfg, kv_heads=1, head_dim=64)
+    assert d.trace() == read("far_trace.txt")
+    assert_scan_exact(d, cfg["steps"])
+    worst = ob.check_driver_window_and_attention(d)
+    assert worst <= 1e-3
+
+
+@pytest.mark.parametrize("dtype,kvh,hd,qh", [("fp16", 4, 64, 4), ("bf16", 4, 64, 16),
+                                             ("fp16", 2, 128, 2), ("bf16", 2, 128, 16),
+                                             ("fp16", 8, 32, 8)])
+def test_window_and_attention_lanes_payload(dtype, kvh, hd, qh):
+    cfg = c1()
+    cfg["steps"] = 40
+    cfg["pager"]["kv_head_dim"] = kvh * hd
+    cfg["pager"]["page_bytes"] = 16 * 2 * 2 * kvh * hd * 2
+    cfg["transport"]["tau_bytes"] = 8 * cfg["pager"]["page_bytes"]
+    cfg["far_view"]["w_star"] = 96
+    host = kv.Driver(dict(cfg, b200=dict(kv_heads=kvh, head_dim=hd, q_heads=qh, payload="lanes",
+                                          dtype=dtype, trace=True)))
+    host.run()
+    d = run(cfg, kv_heads=kvh, head_dim=hd, q_heads=qh, payload="lanes", dtype=dtype)
+    assert d.trace() == host.trace()
+    assert_scan_exact(d, 40)
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
+def test_far_view_bf16_extension():
+    """bf16 far view (a B200 extension: fp32 mean, RNE to bf16) runs at full width."""
+    cfg = json.loads(read("far_config.json"))
+    cfg["steps"] = 250
+    cfg["pager"].update({"elem_bytes": 2, "page_bytes": 8192})
+    d = run(cfg, kv_heads=2, head_dim=32, q_heads=4, payload="lanes", dtype="bf16")
+    assert_scan_exact(d, 250)
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
+def test_pager_on_device_random_streams():
+    """The Pager API with its payload in HBM: host payload writes, COW copies,
+    recycled-page zeroing and trims must read back exactly like the host pager."""
+    import random
+    from tests.test_pager import payload, small
+    g = kv.Geometry()
+    g.device, g.elem_kind, g.elem_bytes, g.payload_mode = 0, 1, 2, 1
+    g.page_bytes, g.token_bytes, g.arena_pages, g.tokens_per_page = 512, 32, 48, 16
+    g.layers, g.kv_heads, g.head_dim, g.q_heads = 1, 1, 8, 1
+    g.n_slots, g.near_window, g.ring_rows, g.far_cap = 3, 32, 64, 0
+    g.chunk_tokens, g.max_chunks, g.max_tokens, g.seed = 16, 1, 4096, 1
+    g.attention, g.use_graph = 0, 1
+    dev = kv.Device(g)
+    for seed in range(20):
+        rng = random.Random(seed)
+        a = kv.Pager(small(48), device=dev)
+        b = kv.Pager(small(48))
+        for s in range(3):
+            a.create_session(s)
+            b.create_session(s)
+        nxt = [0, 0, 0]
+        for _ in range(60):
+            s = rng.randrange(3)
+            k = rng.randrange(8)
+            if k < 2:
+                call = ("reserve", (s, rng.randrange(40)))
+            elif k < 3:
+                call = ("alias", (s, rng.randrange(3), rng.randrange(1, 40)))
+            elif k < 6:
+                lo = rng.randrange(a.session_cursor(s) + 1)
+                n = rng.randint(1, 20)
+                call = ("write_tokens", (s, lo, lo + n, payload(n, rng.randrange(256))))
+            elif k < 7:
+                call = ("trim_eos", (s,))
+            else:
+                call = ("frame_commit", (s, nxt[s]))
+            outs = []
+            for p in (a, b):
+                try:
+                    outs.append(getattr(p, call[0])(*call[1]))
+                except kv.KvrailError as e:
+                    outs.append(e.code)
+            assert outs[0] == outs[1]
+            if call[0] == "frame_commit" and not isinstance(outs[0], str):
+                nxt[s] += 1
+                for t in range(3):
+                    assert a.reconstruct_view(t) == b.reconstruct_view(t), (seed, t)
+        a.close()
+    dev.close()
