@@ -107,7 +107,13 @@ def test_pager_on_device_random_streams():
     """The Pager API with its payload in HBM: host payload writes, COW copies,
     recycled-page zeroing and trims must read back exactly like the host pager."""
     import random
-    from tests.test_pager import payload, small
+
+    def small(pages):
+        return kv.PagerConfig(512, pages, 1, 8, 2)
+
+    def payload(n, tag):
+        return bytes(((tag * 131 + i * 7) & 0xFF) for i in range(n * 32))
+
     g = kv.Geometry()
     g.device, g.elem_kind, g.elem_bytes, g.payload_mode = 0, 1, 2, 1
     g.page_bytes, g.token_bytes, g.arena_pages, g.tokens_per_page = 512, 32, 48, 16
