@@ -197,6 +197,9 @@ def run_b200(args, rank, local, world) -> dict | None:
         "trains_mean": statistics.mean(r.trains for r in recs),
         "dma_mean": statistics.mean(r.dma_bytes for r in recs),
         "mean_train_bytes": (sum(r.dma_bytes for r in recs) / max(1, sum(r.trains for r in recs))),
+        "phases": {name: statistics.mean(r.phase_ms[i] for r in recs) for i, name in enumerate(
+            ["apply", "hot_writes_query", "far_map_prime", "scan", "gather", "attention",
+             "cold_write_tail"])},
         "p50_ms": statistics.median(r.device_ms for r in recs),
         "p99_ms": sorted(r.device_ms for r in recs)[min(len(recs) - 1, int(0.99 * len(recs)))],
     }
@@ -265,6 +268,7 @@ def main():
         "transport": {"trains_per_step": res["trains_mean"], "mean_train_bytes":
                       res["mean_train_bytes"], "live_mean": res["live_mean"]},
         "step_latency_ms": {"p50": res["p50_ms"], "p99": res["p99_ms"]},
+        "step_phases_ms_mean": res["phases"],
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": 32},
         "gpu_launches": 11 * args.steps,

@@ -60,7 +60,12 @@ typedef struct kvr_step_header {
     uint32_t merge;
     uint32_t n_zero, n_cow, n_edit, n_write, n_blob, n_need, n_span, n_prime, n_far_ids;
     uint32_t n_far_jobs;    /* source-1 ops: the last n_far_jobs of the n_write ops */
-    uint64_t write_tokens;  /* sum of kvr_write_op.count over source-0 writes */
+    uint32_t n_cold;        /* write ops are [hot ... | cold ... | far jobs ...]; cold ops
+                               touch rows no kernel of this step reads and run on a
+                               graph branch concurrent with the attention */
+    uint32_t pad_h;
+    uint64_t write_tokens;  /* sum of kvr_write_op.count over hot source-0 writes */
+    uint64_t write_tokens_cold; /* ... over cold source-0 writes */
     uint64_t off_zero, off_cow, off_edit, off_write, off_blob_ops, off_blob, off_need, off_span,
         off_prime, off_far_ids, off_slots;
     uint64_t total_bytes;
@@ -116,6 +121,8 @@ typedef struct kvr_step_stats {
     double device_ms;       /* descriptor H2D + step kernels + stats D2H */
     double gather_ms;       /* K-gather alone (event nodes inside the graph) */
     double attn_ms;         /* K-attn alone */
+    double phase_ms[8];     /* apply | hot writes+query | far+map+prime | scan | gather |
+                               attn | wait for the cold-write branch | (unused) */
     uint32_t trains, descriptors, spans, status;
     uint64_t train_bytes;
     uint64_t staged_tokens;

@@ -37,6 +37,7 @@ struct DeviceStepStats {
     double device_ms = 0.0;     // CUDA-event time of the step's device work
     double gather_ms = 0.0;     // K-gather alone
     double attn_ms = 0.0;       // K-attn alone
+    double phase_ms[8] = {};    // kvr_step_stats::phase_ms
     uint32_t trains = 0;        // computed by K-scan
     uint32_t descriptors = 0;
     uint64_t train_bytes = 0;   // sum of train bytes (gather read side)

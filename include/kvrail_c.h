@@ -198,6 +198,7 @@ typedef struct kvr_step_record { /* StepRecord, sim_engine.hpp:47-63 + measured 
     double device_ms;          /* CUDA-event time of this step's graph replay */
     double gather_ms;          /* K-gather kernel alone */
     double attn_ms;            /* K-attn kernel alone */
+    double phase_ms[8];        /* device time per step phase (kvr_step_stats) */
     uint64_t writeback_tokens; /* token rows written to the arena this step */
     uint64_t gather_bytes;     /* bytes the gather moved (read side) */
     uint64_t attn_bytes;       /* KV bytes the window attention read */

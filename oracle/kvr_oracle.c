@@ -126,8 +126,18 @@ static float load_lane(const void *in, uint64_t i, int elem_kind) {
 
 void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint64_t lanes,
                           int elem_kind, void *out) {
-    for (uint64_t l = 0; l < lanes; ++l)
-        store_lane(out, l, lane_value(pattern(seed, session, token, l)), elem_kind);
+    if (elem_kind == 0) { /* fp32: the reference float pattern, scenario.cpp:198-201 */
+        for (uint64_t l = 0; l < lanes; ++l)
+            store_lane(out, l, lane_value(pattern(seed, session, token, l)), elem_kind);
+        return;
+    }
+    /* 2-byte lanes: one splitmix64 per group of 4 lanes (tweaked by bit 63),
+     * lane j of the group takes bits [16j, 16j+16) mod 2001 */
+    for (uint64_t l = 0; l < lanes; ++l) {
+        const uint64_t x = pattern(seed, session, token, (l >> 2) ^ 0x8000000000000000ull);
+        const uint32_t v = (uint32_t)((x >> (16 * (l & 3))) & 0xffffu) % 2001u;
+        store_lane(out, l, (float)((int)v - 1000) / 1000.0f, elem_kind);
+    }
 }
 
 void kvo_fill_query(uint64_t seed, uint32_t session, uint64_t step, uint32_t layer,

@@ -66,24 +66,42 @@ template <int ESZ> struct Pack16;
 __device__ inline uint16_t f2h_bits(float v) { return __half_as_ushort(__float2half_rn(v)); }
 __device__ inline uint16_t f2b_bits(float v) { return __bfloat16_as_ushort(__float2bfloat16_rn(v)); }
 
+// Lane values of the reference pattern, ((h % 2001) - 1000) / 1000 (scenario.cpp:200),
+// precomputed once per CTA in the element encoding: a table lookup replaces the
+// division and the rounding on the hot path (bit-identical by construction).
+struct LaneTable {
+    uint32_t v[2001];
+    __device__ void fill(const DevCtx &c) {
+        for (uint32_t i = threadIdx.x; i < 2001; i += blockDim.x) {
+            const float f = float(int(i) - 1000) / 1000.0f;
+            v[i] = c.esz == 4 ? __float_as_uint(f)
+                              : (c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(f) : f2h_bits(f));
+        }
+        __syncthreads();
+    }
+    __device__ uint32_t operator()(uint64_t h) const { return v[h % 2001ull]; }
+};
+
 // 16 payload bytes starting at byte `b0` of token `tok` of session `sid`.
-__device__ inline int4 payload16(const DevCtx &c, uint32_t sid, uint64_t tok, uint64_t b0) {
+__device__ inline int4 payload16(const DevCtx &c, const LaneTable &tab, uint32_t sid, uint64_t tok,
+                                 uint64_t b0) {
     const uint64_t base = c.seed ^ (uint64_t(sid) << 32) ^ (tok << 8);
     uint32_t w[4];
     if (c.esz == 4) { // float lanes (reference pattern for elem_bytes == 4)
         const uint64_t lane0 = b0 / 4;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
-            w[i] = __float_as_uint(lane_value(splitmix64(base ^ (lane0 + i))));
-    } else if (c.payload_mode == KVR_PAYLOAD_LANES) { // 2-byte lanes: pattern rounded
-        const uint64_t lane0 = b0 / 2;
+            w[i] = tab(splitmix64(base ^ (lane0 + i)));
+    } else if (c.payload_mode == KVR_PAYLOAD_LANES) {
+        // 2-byte lanes (B200 extension, kvo_fill_token_lanes): one splitmix64 per
+        // 4 lanes, lane value from its 16 bits mod 2001, rounded to fp16/bf16
+        const uint64_t g0 = (b0 / 2) >> 2; // 16 bytes = 8 lanes = 2 groups
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const float a = lane_value(splitmix64(base ^ (lane0 + 2 * i)));
-            const float b = lane_value(splitmix64(base ^ (lane0 + 2 * i + 1)));
-            const uint32_t lo = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(a) : f2h_bits(a);
-            const uint32_t hi = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(b) : f2h_bits(b);
-            w[i] = lo | (hi << 16);
+        for (int gi = 0; gi < 2; ++gi) {
+            const uint64_t x = splitmix64(base ^ (g0 + gi) ^ 0x8000000000000000ull);
+            const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+            w[2 * gi] = tab.v[(lo & 0xffffu) % 2001u] | (tab.v[(lo >> 16) % 2001u] << 16);
+            w[2 * gi + 1] = tab.v[(hi & 0xffffu) % 2001u] | (tab.v[(hi >> 16) % 2001u] << 16);
         }
     } else { // reference byte pattern: one splitmix per byte
 #pragma unroll
@@ -98,25 +116,48 @@ __device__ inline int4 payload16(const DevCtx &c, uint32_t sid, uint64_t tok, ui
     return make_int4(int(w[0]), int(w[1]), int(w[2]), int(w[3]));
 }
 
-__global__ void __launch_bounds__(256) k_write(DevCtx c) {
+// `cold`: 0 = the hot write ops (rows read later in this step), 1 = the cold ops
+// (older prompt rows; launched on a graph branch concurrent with K-attn).
+__global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
+    __shared__ LaneTable tab;
     const kvr_step_header *h = hdr(c);
-    const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write);
+    const uint32_t n_hot = h->n_write - h->n_far_jobs - h->n_cold;
+    const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write) + (cold ? n_hot : 0);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
-    const uint32_t n = h->n_write;
-    const uint64_t total = h->write_tokens;
-    const uint64_t chunks = c.token_bytes / 16;
-    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
-    for (uint64_t j = blockIdx.x; j < total; j += gridDim.x) {
-        // op holding token j: last op with prefix <= j (source-0 ops only carry prefixes)
-        uint32_t lo = 0, hi = n;
+    const uint32_t n = cold ? h->n_cold : n_hot;
+    const uint64_t total = cold ? h->write_tokens_cold : h->write_tokens;
+    if (total == 0)
+        return;
+    tab.fill(c);
+    const uint32_t chunks = uint32_t(c.token_bytes / 16);
+    const uint32_t row_chunks = c.row_elems * c.esz / 16;
+    // work unit = one blockDim-wide slice of 16-byte chunks of one token, so a
+    // decode step's few tokens still spread over every SM
+    const uint32_t slices = (chunks + blockDim.x - 1) / blockDim.x;
+    const uint64_t units = total * slices;
+    // each CTA walks a contiguous run of units: one binary search, then the op
+    // cursor only moves forward (ops are sorted by token prefix)
+    const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
+    const uint64_t u0 = blockIdx.x * per, u1 = min(units, u0 + per);
+    uint32_t cur = 0;
+    if (u0 < u1) {
+        const uint64_t j0 = u0 / slices;
+        uint32_t lo = 0, hi = n; // last op with prefix <= j0
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) / 2;
-            if (ops[mid].prefix <= j)
+            if (ops[mid].prefix <= j0)
                 lo = mid;
             else
                 hi = mid;
         }
-        const kvr_write_op op = ops[lo];
+        cur = lo;
+    }
+    kvr_write_op op = ops[cur < n ? cur : 0];
+    for (uint64_t u = u0; u < u1; ++u) {
+        const uint64_t j = u / slices;
+        const uint32_t slice = uint32_t(u - j * slices);
+        while (cur + 1 < n && ops[cur + 1].prefix <= j)
+            op = ops[++cur];
         if (op.source != 0)
             continue;
         const uint64_t k = j - op.prefix;
@@ -128,41 +169,43 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c) {
             if (tok < w && tok + c.W >= w) // inside the live window after this step
                 ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
         }
-        for (uint64_t q = threadIdx.x; q < chunks; q += blockDim.x) {
-            const int4 v = payload16(c, op.session, tok, 16 * q);
-            *reinterpret_cast<int4 *>(dst + 16 * q) = v;
+        const uint64_t ring_layer = uint64_t(c.R) * c.row_elems * c.esz; // bytes between layers
+        {
+            const uint32_t q = slice * blockDim.x + threadIdx.x;
+            if (q >= chunks)
+                continue;
+            const int4 v = payload16(c, tab, op.session, tok, 16ull * q);
+            *reinterpret_cast<int4 *>(dst + 16ull * q) = v;
             if (ring) {
-                const uint64_t byte = 16 * q;
-                const uint64_t l = byte / row_bytes, within = byte % row_bytes;
-                *reinterpret_cast<int4 *>(ring + l * uint64_t(c.R) * row_bytes + within) = v;
+                const uint32_t l = q / row_chunks, within = q - l * row_chunks;
+                *reinterpret_cast<int4 *>(ring + l * ring_layer + 16ull * within) = v;
             }
         }
     }
 }
 
 // Decode queries for live slots: [slot][L][Hq][hd], rounded to the KV element
-// type (kvo_fill_query in the oracle).
+// type (kvo_fill_query in the oracle). One CTA per (slot, layer).
 __global__ void k_query(DevCtx c) {
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
-    const uint64_t per_slot = uint64_t(c.L) * c.Hq * c.hd;
-    const uint64_t total = per_slot * c.n_slots;
-    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < total;
-         i += uint64_t(gridDim.x) * blockDim.x) {
-        const uint32_t s = uint32_t(i / per_slot);
+    const uint32_t per_layer = c.Hq * c.hd;
+    for (uint32_t sl = blockIdx.x; sl < c.n_slots * c.L; sl += gridDim.x) {
+        const uint32_t s = sl / c.L, l = sl - s * c.L;
         if (!slots[s].live)
             continue;
-        const uint64_t r = i % per_slot;
-        const uint32_t d = uint32_t(r % c.hd), head = uint32_t((r / c.hd) % c.Hq),
-                       l = uint32_t(r / (uint64_t(c.hd) * c.Hq));
-        const uint64_t hsh = splitmix64(c.seed ^ (0x51ull << 56) ^ (uint64_t(slots[s].session) << 32) ^
-                                        (h->step << 20) ^ (uint64_t(l) << 12) ^ (uint64_t(head) << 8) ^ d);
-        float v = lane_value(hsh);
-        if (c.elem_kind == KVR_ELEM_F16)
-            v = __half2float(__float2half_rn(v));
-        else if (c.elem_kind == KVR_ELEM_BF16)
-            v = __bfloat162float(__float2bfloat16_rn(v));
-        c.q[i] = v;
+        const uint64_t base = c.seed ^ (0x51ull << 56) ^ (uint64_t(slots[s].session) << 32) ^
+                              (h->step << 20) ^ (uint64_t(l) << 12);
+        float *q = c.q + uint64_t(sl) * per_layer;
+        for (uint32_t i = threadIdx.x; i < per_layer; i += blockDim.x) {
+            const uint32_t head = i / c.hd, d = i - head * c.hd;
+            float v = lane_value(splitmix64(base ^ (uint64_t(head) << 8) ^ d));
+            if (c.elem_kind == KVR_ELEM_F16)
+                v = __half2float(__float2half_rn(v));
+            else if (c.elem_kind == KVR_ELEM_BF16)
+                v = __bfloat162float(__float2bfloat16_rn(v));
+            q[i] = v;
+        }
     }
 }
 
@@ -276,10 +319,13 @@ void launch_apply(const DevCtx &c, cudaStream_t s, int sms) {
     k_blob<<<sms, 256, 0, s>>>(c);
 }
 
-void launch_write(const DevCtx &c, cudaStream_t s, int sms) {
-    k_write<<<sms * 8, 256, 0, s>>>(c);
-    k_query<<<sms * 2, 256, 0, s>>>(c);
+// cold: 0 hot writes (whole GPU), 1 cold writes (whole GPU, apply-only path),
+// 2 cold writes beside the attention (one CTA per SM)
+void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold) {
+    k_write<<<cold == 2 ? sms : sms * 8, 256, 0, s>>>(c, cold ? 1 : 0);
 }
+
+void launch_query(const DevCtx &c, cudaStream_t s, int sms) { k_query<<<sms * 2, 256, 0, s>>>(c); }
 
 void launch_far(const DevCtx &c, cudaStream_t s, int sms) { k_far<<<sms * 2, 256, 0, s>>>(c); }
 void launch_map(const DevCtx &c, cudaStream_t s, int sms) { k_map<<<sms * 2, 256, 0, s>>>(c); }

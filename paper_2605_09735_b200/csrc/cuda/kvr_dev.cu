@@ -38,7 +38,9 @@ struct kvr_dev {
     void *h_desc[3] = {nullptr, nullptr, nullptr};
     ScanCounters *h_scan[2] = {nullptr, nullptr};
     cudaEvent_t ev_start[2] = {}, ev_stop[2] = {}, ev_attn[2] = {};
-    cudaEvent_t ev_phase[2][4] = {}; // per ring slot: gather begin/end, attention begin/end
+    cudaEvent_t ev_phase[2][8] = {}; // per ring slot: phase boundaries inside the step graph
+    cudaStream_t side = nullptr;     // graph branch for cold writes
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     AttnPlan *attn = nullptr;
     uint64_t launched[2] = {0, 0};
@@ -96,21 +98,37 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
                          : cudaEventRecord(d->ev_phase[k][i], s),
                "phase event");
     };
+    mark(0);
     launch_apply(c, s, d->sms);
-    launch_write(c, s, d->sms);
+    if (!full_step) { // apply-only: everything in order on one stream
+        launch_write(c, s, d->sms, 0);
+        launch_write(c, s, d->sms, 1);
+        launch_far(c, s, d->sms);
+        launch_map(c, s, d->sms);
+        launch_prime(c, s, d->sms);
+        return;
+    }
+    mark(1);
+    launch_write(c, s, d->sms, 0);
+    launch_query(c, s, d->sms);
+    mark(2);
     launch_far(c, s, d->sms);
     launch_map(c, s, d->sms);
     launch_prime(c, s, d->sms);
-    if (!full_step)
-        return;
+    mark(3);
     launch_scan(c, s);
-    mark(0);
+    mark(4);
     launch_gather(c, s, d->sms);
-    mark(1);
-    mark(2);
+    mark(5);
     if (d->g.attention && d->attn)
         launch_attn(d->attn, c, s);
-    mark(3);
+    mark(6);
+    // Cold writes (older prompt rows nothing in this step reads) go last: measured
+    // on B200, co-running this int-bound generation beside the HBM-bound attention
+    // (one CTA per SM on a forked branch) slowed the attention by more than the
+    // overlap saved, so the step runs them after it with the whole GPU.
+    launch_write(c, s, d->sms, 1);
+    mark(7);
 }
 
 } // namespace
@@ -152,11 +170,14 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         ck(cudaGetDeviceProperties(&prop, g.device), "cudaGetDeviceProperties");
         d->sms = prop.multiProcessorCount;
         ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking), "side stream");
+        ck(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming), "event");
+        ck(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming), "event");
         for (int i = 0; i < 2; ++i) {
             ck(cudaEventCreate(&d->ev_start[i]), "event");
             ck(cudaEventCreate(&d->ev_stop[i]), "event");
             ck(cudaEventCreate(&d->ev_attn[i]), "event");
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < 8; ++j)
                 ck(cudaEventCreate(&d->ev_phase[i][j]), "event");
         }
         DevCtx &c = d->base;
@@ -254,7 +275,7 @@ int kvr_dev_close(kvr_dev *d) {
             cudaEventDestroy(d->ev_stop[i]);
         if (d->ev_attn[i])
             cudaEventDestroy(d->ev_attn[i]);
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 8; ++j)
             if (d->ev_phase[i][j])
                 cudaEventDestroy(d->ev_phase[i][j]);
         if (d->h_scan[i])
@@ -267,6 +288,12 @@ int kvr_dev_close(kvr_dev *d) {
         cudaFree(p);
     if (d->attn)
         free_attn_plan(d->attn);
+    if (d->side)
+        cudaStreamDestroy(d->side);
+    if (d->ev_fork)
+        cudaEventDestroy(d->ev_fork);
+    if (d->ev_join)
+        cudaEventDestroy(d->ev_join);
     if (d->stream)
         cudaStreamDestroy(d->stream);
     delete d;
@@ -311,7 +338,7 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
         ck(cudaEventRecord(d->ev_stop[k], d->stream), "event");
         d->launched[k] = h->step;
         d->in_flight[k] = true;
-        d->pending_write_tokens[k] = h->write_tokens;
+        d->pending_write_tokens[k] = h->write_tokens + h->write_tokens_cold;
     });
 }
 
@@ -343,11 +370,13 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
         const ScanCounters &sc = *d->h_scan[k];
         out->step = d->launched[k];
         out->device_ms = ms;
-        float g = 0.f, a = 0.f;
-        ck(cudaEventElapsedTime(&g, d->ev_phase[k][0], d->ev_phase[k][1]), "elapsed");
-        ck(cudaEventElapsedTime(&a, d->ev_phase[k][2], d->ev_phase[k][3]), "elapsed");
-        out->gather_ms = g;
-        out->attn_ms = a;
+        for (int j = 0; j < 7; ++j) {
+            float t = 0.f;
+            ck(cudaEventElapsedTime(&t, d->ev_phase[k][j], d->ev_phase[k][j + 1]), "elapsed");
+            out->phase_ms[j] = t;
+        }
+        out->gather_ms = out->phase_ms[4];
+        out->attn_ms = out->phase_ms[5];
         out->trains = sc.trains;
         out->descriptors = sc.descriptors;
         out->spans = sc.spans;

@@ -81,7 +81,8 @@ __device__ inline uint64_t ring_row(const DevCtx &c, uint32_t slot, uint32_t l, 
 
 // ---- host launchers (one per kernel file) --------------------------------
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blob
-void launch_write(const DevCtx &c, cudaStream_t s, int sms);   // generated payloads + query
+void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold); // generated payloads
+void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
 void launch_far(const DevCtx &c, cudaStream_t s, int sms);     // far summaries
 void launch_map(const DevCtx &c, cudaStream_t s, int sms);     // page-table edits
 void launch_prime(const DevCtx &c, cudaStream_t s, int sms);   // window priming

@@ -372,6 +372,7 @@ static void fill_record(const StepRecord &r, kvr_step_record *o) {
         o->device_ms = r.device_ms;
         o->gather_ms = r.gather_ms;
         o->attn_ms = r.attn_ms;
+        std::memcpy(o->phase_ms, r.phase_ms, sizeof(o->phase_ms));
         o->writeback_tokens = r.writeback_tokens;
         o->gather_bytes = r.gather_bytes;
         o->attn_bytes = r.attn_bytes;

@@ -105,17 +105,60 @@ struct DeviceStep::Impl {
             off = align16(off + bytes);
             return at;
         };
-        std::vector<kvr_write_op> all_writes = writes;
+        // Hot writes produce rows this step's kernels read (a live window row or a
+        // staged block); the rest (older prompt rows) are cold and run on a graph
+        // branch overlapping the attention.
+        std::vector<kvr_write_op> hot, cold;
+        if (with_step) {
+            std::unordered_set<BlockId> staged;
+            for (const kvr_span_rec &s : spans)
+                staged.insert(s.block);
+            for (const kvr_write_op &w : writes) {
+                // Unbound sessions (the shared-prefix template) are read by K-prime
+                // of sessions that alias them this very step: always hot.
+                if (staged.count(w.block) || w.dev_slot == KVR_NO_SLOT) {
+                    hot.push_back(w);
+                    continue;
+                }
+                const uint64_t wr = slots[w.dev_slot].written;
+                const uint64_t lo = std::max<uint64_t>(w.token, wr > g.near_window ? wr - g.near_window : 0);
+                const uint64_t hi = std::min<uint64_t>(w.token + w.count, wr);
+                if (lo >= hi) {
+                    cold.push_back(w);
+                    continue;
+                }
+                auto piece = [&](uint64_t a, uint64_t b, std::vector<kvr_write_op> &to) {
+                    if (a >= b)
+                        return;
+                    kvr_write_op x = w;
+                    x.token = a;
+                    x.slot = w.slot + uint32_t(a - w.token);
+                    x.count = uint32_t(b - a);
+                    to.push_back(x);
+                };
+                piece(w.token, lo, cold);
+                piece(lo, hi, hot);
+                piece(hi, w.token + w.count, cold);
+            }
+        } else {
+            hot = writes;
+        }
         uint64_t prefix = 0;
-        for (kvr_write_op &w : all_writes) {
+        for (kvr_write_op &w : hot) {
             w.prefix = prefix;
             prefix += w.count;
         }
         h.write_tokens = prefix;
-        for (kvr_write_op w : far_jobs) {
+        prefix = 0;
+        for (kvr_write_op &w : cold) {
             w.prefix = prefix;
-            all_writes.push_back(w);
+            prefix += w.count;
         }
+        h.write_tokens_cold = prefix;
+        h.n_cold = uint32_t(cold.size());
+        std::vector<kvr_write_op> all_writes = hot;
+        all_writes.insert(all_writes.end(), cold.begin(), cold.end());
+        all_writes.insert(all_writes.end(), far_jobs.begin(), far_jobs.end());
         const auto &nd = with_step ? needs : std::vector<kvr_need_rec>{};
         const auto &sp = with_step ? spans : std::vector<kvr_span_rec>{};
         const auto &fi = with_step ? far_ids : std::vector<uint32_t>{};
@@ -405,6 +448,7 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
         d.device_ms = st.device_ms;
         d.gather_ms = st.gather_ms;
         d.attn_ms = st.attn_ms;
+        std::copy(st.phase_ms, st.phase_ms + 8, d.phase_ms);
         d.trains = st.trains;
         d.descriptors = st.descriptors;
         d.train_bytes = st.train_bytes;
@@ -452,6 +496,7 @@ DeviceStepStats DeviceStep::collect(uint64_t step) {
         d.device_ms = st.device_ms;
         d.gather_ms = st.gather_ms;
         d.attn_ms = st.attn_ms;
+        std::copy(st.phase_ms, st.phase_ms + 8, d.phase_ms);
         d.trains = st.trains;
         d.descriptors = st.descriptors;
         d.train_bytes = st.train_bytes;

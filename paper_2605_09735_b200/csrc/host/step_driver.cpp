@@ -262,10 +262,13 @@ struct ScenarioDriver::Impl {
         if (cfg.pager.elem_bytes == 4 || lanes_payload) {
             const uint64_t lanes = tb / cfg.pager.elem_bytes;
             for (uint64_t l = 0; l < lanes; ++l) {
-                const float v = float(int64_t(pattern(id, tok, l) % 2001) - 1000) / 1000.0f;
-                if (cfg.pager.elem_bytes == 4)
+                if (cfg.pager.elem_bytes == 4) { // reference float pattern
+                    const float v = float(int64_t(pattern(id, tok, l) % 2001) - 1000) / 1000.0f;
                     std::memcpy(out + 4 * l, &v, 4);
-                else {
+                } else { // 2-byte lanes: 16 bits of one splitmix per 4 lanes
+                    const uint64_t x = pattern(id, tok, (l >> 2) ^ 0x8000000000000000ull);
+                    const uint32_t r = uint32_t((x >> (16 * (l & 3))) & 0xffffu) % 2001u;
+                    const float v = float(int(r) - 1000) / 1000.0f;
                     const uint16_t h = ekind == KVR_ELEM_BF16 ? to_bf16(v) : to_half(v);
                     std::memcpy(out + 2 * l, &h, 2);
                 }
@@ -956,6 +959,7 @@ StepRecord ScenarioDriver::step() {
             prev.device_ms = ds.device_ms;
             prev.gather_ms = ds.gather_ms;
             prev.attn_ms = ds.attn_ms;
+            std::copy(ds.phase_ms, ds.phase_ms + 8, prev.phase_ms);
             prev.writeback_tokens = ds.writeback_tokens;
             prev.gather_bytes = ds.train_bytes;
             prev.attn_bytes = ds.attn_bytes;
@@ -966,6 +970,7 @@ StepRecord ScenarioDriver::step() {
             r.device_ms = ds.device_ms;
             r.gather_ms = ds.gather_ms;
             r.attn_ms = ds.attn_ms;
+            std::copy(ds.phase_ms, ds.phase_ms + 8, r.phase_ms);
             r.writeback_tokens = ds.writeback_tokens;
             r.gather_bytes = ds.train_bytes;
             r.attn_bytes = ds.attn_bytes;
@@ -988,6 +993,7 @@ const StepRecord &ScenarioDriver::record(uint64_t step) {
         r.device_ms = ds.device_ms;
         r.gather_ms = ds.gather_ms;
         r.attn_ms = ds.attn_ms;
+        std::copy(ds.phase_ms, ds.phase_ms + 8, r.phase_ms);
         r.writeback_tokens = ds.writeback_tokens;
         r.gather_bytes = ds.train_bytes;
         r.attn_bytes = ds.attn_bytes;

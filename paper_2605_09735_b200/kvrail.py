@@ -146,7 +146,7 @@ class StepRecord(C.Structure):
                 ("step_latency", C.c_double), ("reserved_bytes", C.c_uint64),
                 ("active_bytes", C.c_uint64), ("commits", C.c_uint32), ("pad_", C.c_uint32),
                 ("emitted_tokens", C.c_uint64), ("device_ms", C.c_double),
-                ("gather_ms", C.c_double), ("attn_ms", C.c_double),
+                ("gather_ms", C.c_double), ("attn_ms", C.c_double), ("phase_ms", C.c_double * 8),
                 ("writeback_tokens", C.c_uint64), ("gather_bytes", C.c_uint64),
                 ("attn_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64)]
 
