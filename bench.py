@@ -168,10 +168,18 @@ def run_b200(args, rank, local, world) -> dict | None:
     d.sync()
     first = d.progress()[0]
     barrier(world)
+    counts = None
+    if world > 1:  # per-step completion / EOS counts: the only cross-GPU traffic
+        import torch
+        import torch.distributed as dist
+        counts = torch.zeros(3, dtype=torch.int64, device="cuda")
     with Clocks(local) as clocks:
         t0 = time.perf_counter()
         for _ in range(args.steps):
-            d.step()
+            r = d.step()
+            if counts is not None:
+                counts.copy_(torch.tensor([r.live_sessions, r.emitted_tokens, r.commits]))
+                dist.all_reduce(counts)
         d.sync()
         t1 = time.perf_counter()
     barrier(world)

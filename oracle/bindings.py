@@ -121,7 +121,8 @@ def token_bytes_via_view(pager, view, token: int, tb: int) -> bytes:
     raise KeyError(token)
 
 
-def check_driver_window_and_attention(driver, far_images_of=None) -> float:
+def check_driver_window_and_attention(driver, far_images_of=None, only_slots=None,
+                                      heads=None) -> float:
     """Window ring == arena for every live slot's near window; attention output
     of the last step within tolerance of the double-precision oracle. Returns the
     worst attention error (raises AssertionError on a byte mismatch)."""
@@ -134,6 +135,8 @@ def check_driver_window_and_attention(driver, far_images_of=None) -> float:
     step = done - 1
     worst = 0.0
     for slot, session, written in driver.live():
+        if only_slots is not None and slot not in only_slots:
+            continue
         if pager.session_eos(session):
             continue  # finished this step: its committed view is already empty
         view = pager.active_view(session)
@@ -156,6 +159,8 @@ def check_driver_window_and_attention(driver, far_images_of=None) -> float:
         out = dev.attention(slot)
         for layer in range(g.layers):
             for qh in range(g.q_heads):
+                if heads is not None and (layer, qh) not in heads:
+                    continue
                 base = (layer * g.q_heads + qh) * g.head_dim
                 q = fill_query(g.seed, session, step, layer, qh, g.head_dim, g.elem_kind)
                 assert q == q_dev[base:base + g.head_dim], "device query differs from the oracle"

@@ -148,14 +148,15 @@ template <typename T, int HD, int QG> struct Attn {
     }
 
     // 16 rows: row(r) -> K row pointer (V row = + v_off elements); valid bit r of `mask`.
-    template <typename RowFn>
+    // FULL: all 16 rows valid (the common case) — no per-row predicates at all.
+    template <bool FULL, typename RowFn>
     __device__ void block(RowFn row, uint32_t v_off, uint32_t mask, float scale_log2) {
         const int lane = threadIdx.x & 31;
         float part[QG][kHalf];
 #pragma unroll
         for (int r = 0; r < kHalf; ++r) {
             float k[DPL];
-            if (mask >> r & 1u) {
+            if (FULL || (mask >> r & 1u)) {
                 load_dims<T, DPL>(row(r) + DPL * lane, k);
             } else {
 #pragma unroll
@@ -187,7 +188,7 @@ template <typename T, int HD, int QG> struct Attn {
             }
             s[g] = (part[g][0] + __shfl_xor_sync(0xffffffffu, part[g][0], 1)) * scale_log2;
         }
-        const bool valid = mask >> (lane >> 1) & 1u;
+        const bool valid = FULL || (mask >> (lane >> 1) & 1u);
         float p[QG];
 #pragma unroll
         for (int g = 0; g < QG; ++g) {
@@ -203,8 +204,8 @@ template <typename T, int HD, int QG> struct Attn {
         }
 #pragma unroll
         for (int r = 0; r < kHalf; ++r) {
-            if (!(mask >> r & 1u))
-                continue; // warp-uniform
+            if (!FULL && !(mask >> r & 1u))
+                continue; // warp-uniform; masked rows may hold non-finite garbage
             float v[DPL];
             load_dims<T, DPL>(row(r) + v_off + DPL * lane, v);
 #pragma unroll
@@ -266,14 +267,23 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
             uint64_t lo, t0;
             uint32_t n_tiles;
             window(slot, lo, t0, n_tiles);
+            const uint64_t w = slots[slot].written;
             for (uint32_t k = 0; k < n_tiles; ++k) {
                 mbar_wait(&empty[s], phase ^ 1);
-                const int row0 = int((t0 + uint64_t(k) * kTile) % c.R);
+                const uint64_t tk = t0 + uint64_t(k) * kTile;
+                // 16-row halves with no live row (window edges) are not loaded
+                const bool h0 = tk < w && tk + kHalf > lo, h1 = tk + kHalf < w && tk + kTile > lo;
                 T *kt = tiles + size_t(s) * 2 * tile_elems;
-                mbar_expect_tx(&full[s], bytes);
-                tma_load_4d(kt, &ring_map, 0, int(hg * G), row0, int(slot * c.L + l), &full[s]);
-                tma_load_4d(kt + tile_elems, &ring_map, 0, int(c.Hkv + hg * G), row0,
-                            int(slot * c.L + l), &full[s]);
+                mbar_expect_tx(&full[s], (uint32_t(h0) + uint32_t(h1)) * (bytes / 2));
+                for (int hf = 0; hf < 2; ++hf) {
+                    if (!(hf ? h1 : h0))
+                        continue;
+                    const int row0 = int((tk + hf * kHalf) % c.R);
+                    T *dst = kt + size_t(hf) * kHalf * G * HD;
+                    tma_load_4d(dst, &ring_map, 0, int(hg * G), row0, int(slot * c.L + l), &full[s]);
+                    tma_load_4d(dst + tile_elems, &ring_map, 0, int(c.Hkv + hg * G), row0,
+                                int(slot * c.L + l), &full[s]);
+                }
                 if (++s == stages) {
                     s = 0;
                     phase ^= 1;
@@ -309,8 +319,13 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
             const uint32_t n = min(uint32_t(kHalf), st.far_count - f0);
             const uint32_t mask = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
             const uint32_t *ids = far_ids + st.far_begin + f0;
-            at.block([&](int r) { return far_base + uint64_t(ids[r < int(n) ? r : 0]) * c.row_elems; },
-                     c.d_kv, mask, scale_log2);
+            auto far_row = [&](int r) {
+                return far_base + uint64_t(ids[r < int(n) ? r : 0]) * c.row_elems;
+            };
+            if (mask == 0xffffu)
+                at.template block<true>(far_row, c.d_kv, mask, scale_log2);
+            else
+                at.template block<false>(far_row, c.d_kv, mask, scale_log2);
         }
         // near window tiles from the TMA pipeline
         for (uint32_t k = 0; k < n_tiles; ++k) {
@@ -322,7 +337,11 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
             for (int r = 0; r < kHalf; ++r)
                 mask |= uint32_t(tok0 + r >= lo && tok0 + r < w) << r;
             const T *base = kt + (size_t(half) * kHalf * G + head_local) * HD;
-            at.block([&](int r) { return base + size_t(r) * G * HD; }, tile_elems, mask, scale_log2);
+            auto tile_row = [&](int r) { return base + size_t(r) * G * HD; };
+            if (mask == 0xffffu)
+                at.template block<true>(tile_row, tile_elems, mask, scale_log2);
+            else if (mask) // a fully masked half was not even loaded
+                at.template block<false>(tile_row, tile_elems, mask, scale_log2);
             __syncwarp();
             if (lane == 0)
                 mbar_arrive(&empty[s]);
@@ -432,7 +451,7 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device) {
     }
     const cuuint64_t dims[4] = {c.hd, 2ull * c.Hkv, c.R, uint64_t(c.L) * c.n_slots};
     const cuuint64_t strides[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
-    const cuuint32_t box[4] = {c.hd, p->G, uint32_t(kTile), 1};
+    const cuuint32_t box[4] = {c.hd, p->G, uint32_t(kHalf), 1}; // 16-row halves
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUtensorMapDataType dt =
         c.esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
