@@ -80,6 +80,12 @@ public:
     bool launched(uint64_t step) const;
     /// Flush byte ops queued outside a step (Pager API use without a Driver).
     void flush();
+    /// Write at most `tokens` cold prompt rows per step (0 = all of them, the
+    /// default). Rows behind the window wait in a queue; a row is forced out
+    /// before a gather, far summary, page copy or host read touches it, and
+    /// dropped when its page is recycled.
+    void set_prefill_budget(uint64_t tokens);
+    uint64_t deferred_tokens() const;
 
     // ---- parity / inspection (synchronous) ----
     void read_arena(uint64_t offset, uint64_t bytes, void *out);

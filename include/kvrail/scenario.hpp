@@ -40,6 +40,7 @@ struct B200Config {
     uint64_t max_tokens = 0;       // per-slot token capacity of the device page table; 0 = auto
     uint32_t graph = 1;            // replay the step as a captured CUDA graph
     bool check = false;            // compare the device K-scan with host reduce() every step
+    uint64_t prefill_budget = 0;   // cold prompt rows written per step (deferred queue); 0 = all
     uint32_t shard_rank = 0;       // requests shard by sequence across GPUs:
     uint32_t shard_world = 1;      //   this rank keeps request_id % world == rank
 };

@@ -2,8 +2,8 @@
 
 Legs, all executed by the reference library compiled from its
 own sources (oracle/_ref, kind "reference"):
-  1. control plane: kvrail_ref::run_scenario on the same workload with the
-     pager geometry scaled to 1 KiB tokens (identical tokens-per-page, page
+  1. control plane: kvrail_ref::run_scenario on the same workload with
+     kv_head_dim and page_bytes shrunk by one power of two (identical tokens-per-page, page
      counts and tau in pages, so every pager / stage / reduce decision is the
      same; only payload bytes shrink), single thread, wall time per step;
   2. gather: host memcpy of the step's train bytes at the reference's
@@ -34,10 +34,16 @@ def control_plane_seconds_per_step(config: dict, steps: int = 200) -> float:
     cfg = copy.deepcopy(config)
     cfg.pop("b200", None)
     p = cfg.setdefault("pager", {})
-    tb = 2 * p["layers"] * p["kv_head_dim"] * p["elem_bytes"]
-    tpp = p["page_bytes"] // tb
-    scale = tb // 1024
-    p.update({"layers": 4, "kv_head_dim": 64, "elem_bytes": 2, "page_bytes": tpp * 1024})
+    # Shrink kv_head_dim and page_bytes by the same power of two: tokens per
+    # page, page counts and tau in pages (every pager / stage / reduce decision)
+    # stay identical, pages stay powers of two (also for 320 KiB tokens).
+    if cfg.get("far_view", {}).get("enabled") and p["elem_bytes"] == 2:
+        # the reference far view is fp32-only: same token bytes as fp32 lanes
+        p.update({"elem_bytes": 4, "kv_head_dim": p["kv_head_dim"] // 2})
+    scale = 1
+    while p["kv_head_dim"] // scale > 16 and p["kv_head_dim"] % (2 * scale) == 0:
+        scale *= 2
+    p.update({"kv_head_dim": p["kv_head_dim"] // scale, "page_bytes": p["page_bytes"] // scale})
     t = cfg.setdefault("transport", {})
     t["tau_bytes"] = int(t.get("tau_bytes", 131072) // scale)
     cfg["steps"] = steps

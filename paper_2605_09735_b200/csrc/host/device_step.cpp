@@ -14,6 +14,7 @@
 // split: the earlier part is flushed as an apply-only descriptor first.
 #include <algorithm>
 #include <cstring>
+#include <deque>
 #include <stdexcept>
 #include <unordered_map>
 #include <unordered_set>
@@ -55,6 +56,8 @@ struct DeviceStep::Impl {
     std::vector<uint32_t> far_ids;
     std::vector<kvr_slot_state> slots;
     std::vector<std::vector<uint64_t>> far_shown; // per slot, as of the last launch
+    std::deque<kvr_write_op> deferred;            // cold prefill rows not yet written
+    uint64_t prefill_budget = 0;                  // tokens per step; 0 = no deferral
     // state
     std::vector<uint8_t> clean; // page known to be all zeros on the device
     std::unordered_map<SessionId, uint32_t> bound;
@@ -109,14 +112,24 @@ struct DeviceStep::Impl {
         // staged block); the rest (older prompt rows) are cold and run on a graph
         // branch overlapping the attention.
         std::vector<kvr_write_op> hot, cold;
+        std::unordered_set<BlockId> staged;
+        for (const kvr_span_rec &s : spans)
+            staged.insert(s.block);
+        // Rows read before the cold phase: staged blocks (K-gather) and chunks a
+        // far job summarises (K-far), matched by session and token range.
+        auto read_early = [&](const kvr_write_op &w) {
+            if (staged.count(w.block))
+                return true;
+            for (const kvr_write_op &f : far_jobs)
+                if (f.session == w.session && w.token < f.aux + g.chunk_tokens && f.aux < w.token + w.count)
+                    return true;
+            return false;
+        };
         if (with_step) {
-            std::unordered_set<BlockId> staged;
-            for (const kvr_span_rec &s : spans)
-                staged.insert(s.block);
             for (const kvr_write_op &w : writes) {
                 // Unbound sessions (the shared-prefix template) are read by K-prime
                 // of sessions that alias them this very step: always hot.
-                if (staged.count(w.block) || w.dev_slot == KVR_NO_SLOT) {
+                if (w.dev_slot == KVR_NO_SLOT || read_early(w)) {
                     hot.push_back(w);
                     continue;
                 }
@@ -142,6 +155,43 @@ struct DeviceStep::Impl {
             }
         } else {
             hot = writes;
+        }
+        if (with_step && prefill_budget) {
+            // Prefill budget: cold rows join the deferred queue, which drains at
+            // most `prefill_budget` tokens per step; queued rows read this step
+            // are forced out with the hot writes.
+            for (auto it = deferred.begin(); it != deferred.end();) {
+                if (read_early(*it)) {
+                    hot.push_back(*it);
+                    it = deferred.erase(it);
+                } else {
+                    ++it;
+                }
+            }
+            // A queued row lies behind its session's window for good: it never
+            // touches the ring, whatever later owns its device slot.
+            for (kvr_write_op w : cold) {
+                w.dev_slot = KVR_NO_SLOT;
+                deferred.push_back(w);
+            }
+            cold.clear();
+            uint64_t left = prefill_budget;
+            while (left && !deferred.empty()) {
+                kvr_write_op &w = deferred.front();
+                if (w.count <= left) {
+                    left -= w.count;
+                    cold.push_back(w);
+                    deferred.pop_front();
+                } else { // split the op at the budget
+                    kvr_write_op x = w;
+                    x.count = uint32_t(left);
+                    cold.push_back(x);
+                    w.token += left;
+                    w.slot += uint32_t(left);
+                    w.count -= uint32_t(left);
+                    left = 0;
+                }
+            }
         }
         uint64_t prefix = 0;
         for (kvr_write_op &w : hot) {
@@ -256,6 +306,9 @@ struct DeviceStep::Impl {
     }
 
     void on_alloc(BlockId head, uint32_t count) {
+        if (!deferred.empty()) // a recycled page's old deferred rows are unobservable: drop
+            for (auto it = deferred.begin(); it != deferred.end();)
+                it = (it->block >= head && it->block < head + count) ? deferred.erase(it) : std::next(it);
         for (uint32_t i = 0; i < count; ++i) {
             const BlockId p = head + i;
             if (clean[p])
@@ -270,7 +323,24 @@ struct DeviceStep::Impl {
         }
     }
 
+    // Deferred prefill rows of `b` (all pages when b == kInvalidBlock) are written now.
+    void drain_deferred(BlockId b) {
+        bool any = false;
+        for (auto it = deferred.begin(); it != deferred.end();) {
+            if (b == kInvalidBlock || it->block == b) {
+                writes.push_back(*it);
+                it = deferred.erase(it);
+                any = true;
+            } else {
+                ++it;
+            }
+        }
+        if (any)
+            flush();
+    }
+
     void copy_page(BlockId src, BlockId dst) {
+        drain_deferred(src); // the copy must see src's deferred prefill rows
         if (wave_slots.count(src) || wave_cow_dst.count(src))
             flush(); // the copy must see this wave's writes to src
         // the copy overwrites dst entirely; a pending zero of dst is moot
@@ -340,6 +410,7 @@ struct DeviceStep::Impl {
     }
 
     void read(BlockId b, uint32_t slot, uint32_t count, std::byte *out) {
+        drain_deferred(b);
         flush();
         ck(kvr_dev_read(dev, KVR_BUF_ARENA, uint64_t(b) * g.page_bytes + uint64_t(slot) * g.token_bytes,
                         uint64_t(count) * g.token_bytes, out));
@@ -513,7 +584,21 @@ void DeviceStep::sync() { ck(kvr_dev_sync(impl_->dev)); }
 bool DeviceStep::launched(uint64_t step) const { return impl_->launched_step[step & 1] == step; }
 void DeviceStep::flush() { impl_->flush(); }
 
+void DeviceStep::set_prefill_budget(uint64_t tokens) {
+    if (!tokens)
+        impl_->drain_deferred(kInvalidBlock);
+    impl_->prefill_budget = tokens;
+}
+
+uint64_t DeviceStep::deferred_tokens() const {
+    uint64_t n = 0;
+    for (const kvr_write_op &w : impl_->deferred)
+        n += w.count;
+    return n;
+}
+
 void DeviceStep::read_arena(uint64_t offset, uint64_t bytes, void *out) {
+    impl_->drain_deferred(kInvalidBlock);
     impl_->flush();
     ck(kvr_dev_read(impl_->dev, KVR_BUF_ARENA, offset, bytes, out));
 }

@@ -350,6 +350,7 @@ struct ScenarioDriver::Impl {
         pc.arena_pages = arena_pages();
         if (cfg.b200.device >= 0) {
             dev = std::make_unique<DeviceStep>(geometry(pc.arena_pages));
+            dev->set_prefill_budget(cfg.b200.prefill_budget);
             pager = std::make_unique<Pager>(pc, dev->store());
         } else {
             pager = std::make_unique<Pager>(pc);
@@ -1275,6 +1276,7 @@ static ScenarioConfig config_from_json(const ojson &j) {
         take(p, "max_tokens", c.b200.max_tokens);
         take(p, "graph", c.b200.graph);
         take(p, "check", c.b200.check);
+        take(p, "prefill_budget", c.b200.prefill_budget);
         take(p, "shard_rank", c.b200.shard_rank);
         take(p, "shard_world", c.b200.shard_world);
     }

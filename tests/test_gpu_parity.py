@@ -63,6 +63,22 @@ def test_golden_scenarios_on_device(name):
     assert_scan_exact(d, cfg["steps"])
 
 
+@pytest.mark.parametrize("name,budget", [("c1", 8), ("adv_burst", 64), ("far", 4)])
+def test_prefill_budget_keeps_reference_bytes(name, budget):
+    """b200.prefill_budget defers cold prompt rows: every staged train, far
+    summary and host read must still see the reference bytes (same trace)."""
+    cfg = c1() if name == "c1" else json.loads(read(f"{name}_config.json"))
+    extra = dict(kv_heads=4, head_dim=64) if name == "c1" else {}
+    if name == "far":
+        extra = dict(kv_heads=1, head_dim=64)
+    else:
+        extra["attention"] = False
+    d = run(cfg, payload="bytes", prefill_budget=budget, **extra)
+    assert d.trace() == read(f"{name}_trace.txt")
+    if name == "far":
+        assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
 def test_far_view_fp32_on_device():
     """Far summaries computed by K-far equal the reference's (hashed in the
     trace through the far trains), and attention over [far..., near...] holds."""
