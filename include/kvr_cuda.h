@@ -44,7 +44,7 @@ typedef struct kvr_geometry {
     uint32_t max_chunks;    /* far rows kept per slot */
     uint64_t max_tokens;    /* per-slot capacity of the device page table */
     uint64_t seed;          /* synthetic payload seed (ScenarioConfig::seed) */
-    uint32_t attention;     /* run K-attn each step */
+    uint32_t attention;     /* K-attn each step: 0 off, 1 auto, 2 CUDA-core kernel, 3 tcgen05 kernel */
     uint32_t use_graph;     /* replay the step as a CUDA graph */
     uint64_t max_desc_bytes;/* capacity of one step descriptor */
     uint32_t max_scan_descs;/* K-scan capacity (descriptors / spans) */

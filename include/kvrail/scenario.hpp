@@ -36,6 +36,7 @@ struct B200Config {
     std::string dtype = "auto";    // fp16 | bf16 | fp32 | auto (elem_bytes 4 -> fp32, 2 -> fp16)
     bool trace = false;            // record the per-step parity trace
     bool attention = true;         // run the window attention kernel each step
+    std::string attention_kernel = "auto"; // auto | cuda_core | tcgen05 (GQA groups, head_dim 128)
     uint32_t ring_rows = 0;        // window ring rows per (slot, layer); 0 = auto
     uint64_t max_tokens = 0;       // per-slot token capacity of the device page table; 0 = auto
     uint32_t graph = 1;            // replay the step as a captured CUDA graph

@@ -409,14 +409,27 @@ template <typename T> AttnFn pick_hd(uint32_t hd, uint32_t g) {
 
 struct AttnPlan {
     AttnFn fn = nullptr;
+    const void *tc = nullptr; // tensor-core kernel (kvr_attn_tc.cu) when chosen
     CUtensorMap map{};
+    CUtensorMap far_map{}; // tensor-core kernel: far rows (gather4)
     uint32_t G = 1, stages = 2, grid = 1;
     size_t smem = 0;
     char name[96] = {0};
 };
 
-AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device) {
+AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
     auto *p = new AttnPlan();
+    if (mode == 3 || (mode == 1 && c.group >= 4 && attn_tc_supported(c))) {
+        p->tc = attn_tc_kernel(c);
+        if (!p->tc || !attn_tc_maps(c, &p->map, &p->far_map)) {
+            delete p;
+            return nullptr;
+        }
+        p->grid = uint32_t(sms);
+        std::snprintf(p->name, sizeof(p->name), "k_attn_tc<%s,hd%u,g%u> tcgen05 M128 N16 stages=3",
+                      c.elem_kind == KVR_ELEM_F16 ? "f16" : "bf16", c.hd, c.group);
+        return p;
+    }
     switch (c.elem_kind) {
     case KVR_ELEM_F16: p->fn = pick_hd<__half>(c.hd, c.group); break;
     case KVR_ELEM_BF16: p->fn = pick_hd<__nv_bfloat16>(c.hd, c.group); break;
@@ -470,6 +483,10 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device) {
 }
 
 void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s) {
+    if (p->tc) {
+        launch_attn_tc(p->tc, c, p->map, p->far_map, p->grid, s);
+        return;
+    }
     p->fn<<<p->grid, 32 * (2 * kMaxG + 1), p->smem, s>>>(c, p->map, p->G, p->stages);
 }
 

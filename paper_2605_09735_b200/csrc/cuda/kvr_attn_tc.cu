@@ -1,0 +1,583 @@
+// kvrail-b200 K-attn, tensor-core variant for GQA groups (g >= 2, head_dim 128,
+// fp16/bf16): the same fixed-shape window attention as kvr_attn.cu (attend() of
+// far_view.cpp:113-155 per (layer, q-head), q-head j -> kv-head j / g), with both
+// contractions on the 5th-generation tensor cores.
+//
+// Work item = (slot, layer, kv head); persistent grid, one CTA per SM.
+//   warp 0  producer: 128-row K|V tiles of the window ring by 4-D TMA (32-row
+//           boxes, 128-byte swizzle; boxes without a live row are skipped), far
+//           summary rows by cp.async into the same swizzled layout;
+//   warp 1  TMEM owner + MMA issuer (one thread):
+//             S^T[128 rows x 16]  = K_tile[128 x 128] . Qs^T      (K-major A)
+//             O^T[128 dims x 16] += V_tile^T[128 x 128] . Ps      (MN-major A)
+//           tcgen05.mma kind::f16, fp32 accumulators in TMEM (S and O double
+//           buffered, 64 columns), completion by tcgen05.commit -> mbarrier;
+//   warps 4-7 softmax/correction warpgroup: thread t owns TMEM lane t, i.e.
+//           token row t of S and head dim t of O. Online softmax in base 2 per
+//           q-head column (cross-warp tile max through shared memory), P written
+//           back as bf16/fp16 for the PV MMA, O folded into fp32 registers.
+// Precision: the MMA operands are 16-bit, so q and p are split hi + lo
+// (x = hi + lo, both in the element type) into columns [0, g) and [g, 2g) of
+// the N = 16 operand; S = S_hi + S_lo and O = O_hi + O_lo recover ~16 extra
+// mantissa bits, keeping the 1e-3 bound of the fp32 path.
+#include <cstdio>
+#include <type_traits>
+#include <cudaTypedefs.h>
+
+#include "kvr_internal.cuh"
+
+namespace kvr {
+
+namespace {
+
+constexpr int kRows = 128;                 // tokens per tile (S: M, PV: K)
+constexpr int kHd = 128;                   // head dim (S: K, PV: M)
+constexpr int kN = 16;                     // MMA N: g hi columns + g lo columns
+constexpr int kSub = 32;                   // rows per TMA box
+constexpr uint32_t kHalfBytes = kRows * 128; // one 64-dim half of a K or V tile (16 KiB)
+constexpr uint32_t kStageBytes = 4 * kHalfBytes; // K half0|half1, V half0|half1
+constexpr int kStages = 3;
+constexpr uint32_t kOpBytes = kN * kHd * 2; // one Q or P operand buffer (4 KiB)
+constexpr int kThreads = 384; // warp 0 TMA, warp 1 MMA, warps 4-7 / 8-11 softmax warpgroups
+
+__device__ inline uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
+__device__ inline void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ inline void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ inline void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ inline void mbar_wait(uint64_t *bar, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "W_%=:\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra W_%=;\n\t}" ::"r"(smem_u32(bar)),
+                 "r"(parity)
+                 : "memory");
+}
+__device__ inline void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
+                                   uint64_t *bar) {
+    asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5}], [%6];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ inline void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ inline void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ inline void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+/// Shared-memory matrix descriptor (sm_100 UMMA): start, leading/stride byte
+/// offsets (16-byte units), version 1, layout (0 none, 2 = 128-byte swizzle).
+__device__ inline uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+    return uint64_t((addr >> 4) & 0x3fff) | uint64_t((lbo >> 4) & 0x3fff) << 16 |
+           uint64_t((sbo >> 4) & 0x3fff) << 32 | 1ull << 46 | uint64_t(layout) << 61;
+}
+/// Instruction descriptor, kind::f16: fp32 accumulate, A/B 16-bit (0 f16, 1 bf16).
+__host__ __device__ constexpr uint32_t idesc(uint32_t fmt, uint32_t a_mn, uint32_t b_mn, uint32_t m,
+                                             uint32_t n) {
+    return (1u << 4) | (fmt << 7) | (fmt << 10) | (a_mn << 15) | (b_mn << 16) | ((n >> 3) << 17) |
+           ((m >> 4) << 24);
+}
+__device__ inline void mma_f16(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "setp.ne.b32 p, %4, 0;\n\t"
+                 "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+                 "l"(a), "l"(b), "r"(id), "r"(acc)
+                 : "memory");
+}
+__device__ inline void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(bar))
+                 : "memory");
+}
+__device__ inline void tmem_ld16(uint32_t taddr, float (&v)[16]) {
+    uint32_t r[16];
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+                 "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                   "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                   "=r"(r[14]), "=r"(r[15])
+                 : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+        v[i] = __uint_as_float(r[i]);
+}
+
+template <typename T> __device__ inline uint16_t to_bits(float x);
+template <> __device__ inline uint16_t to_bits<__half>(float x) { return __half_as_ushort(__float2half_rn(x)); }
+template <> __device__ inline uint16_t to_bits<__nv_bfloat16>(float x) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
+}
+template <typename T> __device__ inline float from_bits(uint16_t b);
+template <> __device__ inline float from_bits<__half>(uint16_t b) { return __half2float(__ushort_as_half(b)); }
+template <> __device__ inline float from_bits<__nv_bfloat16>(uint16_t b) {
+    return __bfloat162float(__ushort_as_bfloat16(b));
+}
+
+/// Byte offset of element (n, k) in a K-major, unswizzled N=16 operand
+/// (8x8 core matrices: 16-byte rows, K-adjacent cores 128 B apart).
+__device__ inline uint32_t op_off(uint32_t n, uint32_t k) {
+    return (n >> 3) * 2048u + (k >> 3) * 128u + (n & 7u) * 16u + (k & 7u) * 2u;
+}
+
+/// Tiles of one work item, identical for every role.
+struct Item {
+    uint32_t slot, layer, head, far_count, far_begin, n_far, n_near;
+    uint64_t lo, w, t0;
+};
+__device__ inline bool item_of(const DevCtx &c, const kvr_slot_state *slots, uint32_t it, Item &I) {
+    I.head = it % c.Hkv;
+    I.layer = (it / c.Hkv) % c.L;
+    I.slot = it / (c.Hkv * c.L);
+    const kvr_slot_state st = slots[I.slot];
+    if (!st.live)
+        return false;
+    I.w = st.written;
+    I.lo = I.w > c.W ? I.w - c.W : 0;
+    I.t0 = I.lo & ~uint64_t(kSub - 1);
+    I.n_near = I.w > I.t0 ? uint32_t((I.w - I.t0 + kRows - 1) / kRows) : 0;
+    I.far_count = st.far_count;
+    I.far_begin = st.far_begin;
+    I.n_far = (st.far_count + kRows - 1) / kRows;
+    return true;
+}
+
+__device__ inline bool mbar_test(uint64_t *bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile("{\n\t.reg .pred p;\n\t"
+                 "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                 "selp.u32 %0, 1, 0, p;\n\t}"
+                 : "=r"(ok)
+                 : "r"(smem_u32(bar)), "r"(parity)
+                 : "memory");
+    return ok != 0;
+}
+/// Four rows (arbitrary indices) x 64 columns of a 2-D tensor (sm_100 TMA gather4).
+__device__ inline void tma_gather4(uint32_t dst, const CUtensorMap *map, int col, int r0, int r1, int r2, int r3,
+                                   uint64_t *bar) {
+    asm volatile("cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+                 "r"(smem_u32(bar))
+                 : "memory");
+}
+
+/// Per-softmax-warpgroup barriers and operand buffers.
+struct WgBars {
+    uint64_t qfull, sfull[2], sempty[2], pfull[2], ofull[2], oempty[2];
+};
+constexpr uint32_t kWgBytes = 3 * kOpBytes; // Q + P[2]
+
+template <typename T, int G>
+__global__ void __launch_bounds__(kThreads, 1)
+    k_attn_tc(DevCtx c, const __grid_constant__ CUtensorMap ring_map, const __grid_constant__ CUtensorMap far_map) {
+    static_assert(2 * G <= kN, "hi/lo columns must fit N = 16");
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t *stages = smem;                                  // kStages x 64 KiB
+    uint8_t *wgbuf = stages + kStages * kStageBytes;         // 2 x (Q | P0 | P1)
+    float *red = reinterpret_cast<float *>(wgbuf + 2 * kWgBytes); // [wg][2][4][8] tile maxima
+    float *lred = red + 2 * 2 * 4 * 8;                       // [wg][4][8] row sums
+    uint64_t *full = reinterpret_cast<uint64_t *>(lred + 2 * 4 * 8);
+    uint64_t *empty = full + kStages;
+    WgBars *wb = reinterpret_cast<WgBars *>(empty + kStages);
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wb + 2);
+
+    const kvr_step_header *h = hdr(c);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint32_t *far_ids = section<uint32_t>(c, h->off_far_ids);
+    const uint32_t n_items = c.n_slots * c.L * c.Hkv;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    // zero stages and operand buffers: rows a tile does not load must hold
+    // finite values (p = 0 times V), unused hi/lo columns must be 0
+    for (uint32_t i = threadIdx.x; i < (kStages * kStageBytes + 2 * kWgBytes) / 16; i += kThreads)
+        reinterpret_cast<int4 *>(smem)[i] = make_int4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int w = 0; w < 2; ++w) {
+            mbar_init(&wb[w].qfull, 4);
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(&wb[w].sfull[b], 1);
+                mbar_init(&wb[w].sempty[b], 4);
+                mbar_init(&wb[w].pfull[b], 4);
+                mbar_init(&wb[w].ofull[b], 1);
+                mbar_init(&wb[w].oempty[b], 4);
+            }
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    fence_async_smem();
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) { // ---------------- producer (one thread) ----------------
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&far_map)) : "memory");
+            uint32_t s = 0, ph = 0;
+            for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+                Item I;
+                if (!item_of(c, slots, it, I))
+                    continue;
+                const int plane = int(I.slot * c.L + I.layer);
+                for (uint32_t k = 0; k < I.n_far + I.n_near; ++k) {
+                    mbar_wait(&empty[s], ph ^ 1);
+                    uint8_t *st = stages + s * kStageBytes;
+                    if (k < I.n_far) {
+                        // far summary rows: TMA gather4, 4 rows x 64 columns per op
+                        const uint32_t r0 = k * kRows, nr = min(uint32_t(kRows), I.far_count - r0);
+                        const uint32_t n4 = (nr + 3) / 4;
+                        mbar_expect_tx(&full[s], n4 * 4 * 512);
+                        const int base = plane * int(c.max_chunks);
+                        const uint32_t *ids = far_ids + I.far_begin + r0;
+                        for (uint32_t g4 = 0; g4 < n4; ++g4) {
+                            int r[4];
+#pragma unroll
+                            for (int x = 0; x < 4; ++x)
+                                r[x] = base + int(ids[min(4 * g4 + x, nr - 1)]);
+                            for (int kv = 0; kv < 2; ++kv)
+                                for (int hf = 0; hf < 2; ++hf)
+                                    tma_gather4(smem_u32(st + (2 * kv + hf) * kHalfBytes + g4 * 512), &far_map,
+                                                int((kv ? c.Hkv + I.head : I.head) * kHd + hf * 64), r[0], r[1],
+                                                r[2], r[3], &full[s]);
+                        }
+                    } else {
+                        const uint64_t tb = I.t0 + uint64_t(k - I.n_far) * kRows;
+                        uint32_t live_boxes = 0;
+                        for (int b = 0; b < kRows / kSub; ++b) {
+                            const uint64_t a = tb + b * kSub;
+                            live_boxes |= uint32_t(a < I.w && a + kSub > I.lo) << b;
+                        }
+                        mbar_expect_tx(&full[s], __popc(live_boxes) * 4 * kSub * 128);
+                        for (int b = 0; b < kRows / kSub; ++b) {
+                            if (!(live_boxes >> b & 1u))
+                                continue;
+                            const int row = int((tb + b * kSub) % c.R);
+                            for (int kv = 0; kv < 2; ++kv)
+                                for (int hf = 0; hf < 2; ++hf)
+                                    tma_load_4d(smem_u32(st + (2 * kv + hf) * kHalfBytes + b * kSub * 128),
+                                                &ring_map, hf * 64, int(kv ? c.Hkv + I.head : I.head), row, plane,
+                                                &full[s]);
+                        }
+                    }
+                    if (++s == kStages) {
+                        s = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) { // ---------------- MMA issuer (one thread) ----------------
+        if (lane == 0) {
+            constexpr uint32_t fmt = std::is_same_v<T, __nv_bfloat16> ? 1u : 0u;
+            constexpr uint32_t id_s = idesc(fmt, 0, 0, kRows, kN); // S^T = K . Q^T
+            constexpr uint32_t id_o = idesc(fmt, 1, 0, kHd, kN);   // O^T = V^T . P
+            struct Pend {
+                uint32_t stage, n, nk;
+            };
+            Pend fifo[2][4];
+            uint32_t head[2] = {0, 0}, size[2] = {0, 0};
+            uint32_t nw[2] = {0, 0}, mw[2] = {0, 0};
+            uint32_t s = 0, ph = 0, j = 0, k = 0;
+            uint32_t it = blockIdx.x;
+            Item I;
+            bool have = false;
+            auto next_item = [&]() {
+                have = false;
+                for (; it < n_items; it += gridDim.x)
+                    if (item_of(c, slots, it, I) && I.n_far + I.n_near > 0) {
+                        have = true;
+                        it += gridDim.x;
+                        break;
+                    }
+                k = 0;
+            };
+            next_item();
+            while (have || size[0] || size[1]) {
+                bool progress = false;
+                if (have) { // S for the next tile in stream order
+                    const uint32_t w = j & 1u, b = nw[w] & 1u;
+                    if ((k > 0 || mbar_test(&wb[w].qfull, mw[w] & 1u)) && mbar_test(&full[s], ph) &&
+                        mbar_test(&wb[w].sempty[b], ((nw[w] >> 1) & 1u) ^ 1u) && size[w] < 4) {
+                        tc_fence_after();
+                        const uint32_t kt = smem_u32(stages + s * kStageBytes);
+                        const uint32_t q = smem_u32(wgbuf + w * kWgBytes);
+                        for (uint32_t kk = 0; kk < kHd / 16; ++kk)
+                            mma_f16(tmem + 64 * w + 16 * b,
+                                    sdesc(kt + (kk >> 2) * kHalfBytes + (kk & 3u) * 32, 16, 1024, 2),
+                                    sdesc(q + kk * 256, 128, 2048, 0), id_s, kk > 0);
+                        mma_commit(&wb[w].sfull[b]);
+                        const uint32_t nk =
+                            k < I.n_far ? (min(uint32_t(kRows), I.far_count - k * kRows) + 15) / 16 : kRows / 16;
+                        fifo[w][(head[w] + size[w]) & 3u] = Pend{s, nw[w], nk};
+                        ++size[w];
+                        ++nw[w];
+                        if (++s == kStages) {
+                            s = 0;
+                            ph ^= 1;
+                        }
+                        if (++k == I.n_far + I.n_near) {
+                            ++mw[w];
+                            ++j;
+                            next_item();
+                        }
+                        progress = true;
+                    }
+                }
+                for (uint32_t w = 0; w < 2; ++w) { // PV for each warpgroup's oldest tile
+                    if (!size[w])
+                        continue;
+                    const Pend p = fifo[w][head[w]];
+                    const uint32_t b = p.n & 1u, par = (p.n >> 1) & 1u;
+                    if (!mbar_test(&wb[w].pfull[b], par) || !mbar_test(&wb[w].oempty[b], par ^ 1u))
+                        continue;
+                    tc_fence_after();
+                    const uint32_t v = smem_u32(stages + p.stage * kStageBytes + 2 * kHalfBytes);
+                    const uint32_t pa = smem_u32(wgbuf + w * kWgBytes + (1 + b) * kOpBytes);
+                    for (uint32_t kk = 0; kk < p.nk; ++kk)
+                        mma_f16(tmem + 64 * w + 32 + 16 * b, sdesc(v + kk * 2048, kHalfBytes, 1024, 2),
+                                sdesc(pa + kk * 256, 128, 2048, 0), id_o, kk > 0);
+                    mma_commit(&wb[w].ofull[b]);
+                    mma_commit(&empty[p.stage]);
+                    head[w] = (head[w] + 1) & 3u;
+                    --size[w];
+                    progress = true;
+                }
+                (void)progress;
+            }
+        }
+    } else if (warp >= 4) { // ---------------- softmax / correction warpgroups ----------------
+        const uint32_t w = uint32_t(warp - 4) >> 2;     // warpgroup 0: warps 4-7, 1: warps 8-11
+        const uint32_t t = threadIdx.x - 128 - 128 * w; // TMEM lane: token row of S, head dim of O
+        const uint32_t wq = uint32_t(warp) & 3u;
+        const uint32_t lane_base = ((32u * wq) << 16) + 64 * w;
+        const uint32_t bar_id = 1 + w;
+        WgBars &B = wb[w];
+        uint8_t *qb = wgbuf + w * kWgBytes;
+        float *rd = red + w * 2 * 4 * 8;
+        float *ld = lred + w * 4 * 8;
+        const float scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
+        uint32_t n = 0, j = 0, m_items = 0;
+        for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+            Item I;
+            if (!item_of(c, slots, it, I))
+                continue;
+            float *o = c.out + ((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G) * kHd;
+            if (I.n_far + I.n_near == 0) {
+                if (w == 0)
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        o[g * kHd + t] = 0.f;
+                continue;
+            }
+            if ((j++ & 1u) != w)
+                continue; // the other warpgroup's item
+            // Q (hi | lo) of this kv head's q-heads; thread t owns head dim t
+            {
+                const float *qs = c.q + ((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G) * kHd;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float x = qs[g * kHd + t];
+                    const uint16_t hi = to_bits<T>(x);
+                    const uint16_t lo = to_bits<T>(x - from_bits<T>(hi));
+                    *reinterpret_cast<uint16_t *>(qb + op_off(g, t)) = hi;
+                    *reinterpret_cast<uint16_t *>(qb + op_off(G + g, t)) = lo;
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&B.qfull);
+            }
+            ++m_items;
+            float m[G], l[G], acc[G], alpha_prev[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+                m[g] = -INFINITY, l[g] = 0.f, acc[g] = 0.f, alpha_prev[g] = 1.f;
+            auto correct = [&](uint32_t nn, const float (&alpha)[G]) {
+                const uint32_t b = nn & 1u;
+                mbar_wait(&B.ofull[b], (nn >> 1) & 1u);
+                tc_fence_after();
+                float ov[16];
+                tmem_ld16(tmem + lane_base + 32 + 16 * b, ov);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&B.oempty[b]);
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    acc[g] = acc[g] * alpha[g] + (ov[g] + ov[G + g]);
+            };
+            for (uint32_t k = 0; k < I.n_far + I.n_near; ++k, ++n) {
+                const uint32_t b = n & 1u;
+                bool valid;
+                if (k < I.n_far) {
+                    valid = k * kRows + t < I.far_count;
+                } else {
+                    const uint64_t tok = I.t0 + uint64_t(k - I.n_far) * kRows + t;
+                    valid = tok >= I.lo && tok < I.w;
+                }
+                mbar_wait(&B.sfull[b], (n >> 1) & 1u);
+                tc_fence_after();
+                float sv[16];
+                tmem_ld16(tmem + lane_base + 16 * b, sv);
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&B.sempty[b]);
+                float sc[G], mx[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    sc[g] = valid ? (sv[g] + sv[G + g]) * scale_log2 : -INFINITY;
+                    float v = sc[g];
+#pragma unroll
+                    for (int off = 16; off; off >>= 1)
+                        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+                    mx[g] = v;
+                }
+                if (lane == 0)
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        rd[(b * 4 + wq) * 8 + g] = mx[g];
+                asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+                float alpha[G];
+                uint8_t *pb = qb + (1 + b) * kOpBytes;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float tm = fmaxf(fmaxf(rd[(b * 4 + 0) * 8 + g], rd[(b * 4 + 1) * 8 + g]),
+                                           fmaxf(rd[(b * 4 + 2) * 8 + g], rd[(b * 4 + 3) * 8 + g]));
+                    const float mn = fmaxf(m[g], tm);
+                    alpha[g] = m[g] == -INFINITY ? 1.f : exp2f(m[g] - mn);
+                    const float p = valid ? exp2f(sc[g] - mn) : 0.f;
+                    l[g] = l[g] * alpha[g] + p;
+                    m[g] = mn;
+                    const uint16_t hi = to_bits<T>(p);
+                    const uint16_t lo = to_bits<T>(p - from_bits<T>(hi));
+                    *reinterpret_cast<uint16_t *>(pb + op_off(g, t)) = hi;
+                    *reinterpret_cast<uint16_t *>(pb + op_off(G + g, t)) = lo;
+                }
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&B.pfull[b]);
+                if (k > 0)
+                    correct(n - 1, alpha_prev);
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    alpha_prev[g] = alpha[g];
+            }
+            correct(n - 1, alpha_prev);
+            // row sums across the warpgroup, then normalise
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                float v = l[g];
+#pragma unroll
+                for (int off = 16; off; off >>= 1)
+                    v += __shfl_xor_sync(0xffffffffu, v, off);
+                if (lane == 0)
+                    ld[wq * 8 + g] = v;
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const float z = ld[g] + ld[8 + g] + ld[16 + g] + ld[24 + g];
+                o[g * kHd + t] = z > 0.f ? acc[g] / z : 0.f;
+            }
+            asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory"); // ld reused by the next item
+        }
+        (void)m_items;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+    }
+}
+
+using TcFn = void (*)(DevCtx, const CUtensorMap, const CUtensorMap);
+
+template <typename T> TcFn pick_tc(uint32_t g) {
+    switch (g) {
+    case 2: return k_attn_tc<T, 2>;
+    case 4: return k_attn_tc<T, 4>;
+    case 8: return k_attn_tc<T, 8>;
+    default: return nullptr;
+    }
+}
+
+using EncodeFn = PFN_cuTensorMapEncodeTiled_v12000;
+EncodeFn encoder() {
+    EncodeFn encode = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", reinterpret_cast<void **>(&encode), cudaEnableDefault, &q);
+    return encode;
+}
+
+} // namespace
+
+/// The tensor-core attention applies to head_dim 128, 16-bit elements and GQA
+/// groups of 2, 4 or 8 with at most 128 far rows per slot.
+bool attn_tc_supported(const DevCtx &c) {
+    return c.hd == kHd && c.esz == 2 && (c.group == 2 || c.group == 4 || c.group == 8) && c.far_cap <= kRows &&
+           c.R % kSub == 0;
+}
+
+size_t attn_tc_smem() {
+    return 1024 + kStages * kStageBytes + 2 * kWgBytes + (2 * 2 * 4 * 8 + 2 * 4 * 8) * 4 + 2 * kStages * 8 +
+           2 * sizeof(WgBars) + 16;
+}
+
+const void *attn_tc_kernel(const DevCtx &c) {
+    if (!attn_tc_supported(c))
+        return nullptr;
+    TcFn fn = c.elem_kind == KVR_ELEM_BF16 ? pick_tc<__nv_bfloat16>(c.group) : pick_tc<__half>(c.group);
+    if (fn)
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_tc_smem()));
+    return reinterpret_cast<const void *>(fn);
+}
+
+/// ring: 4-D view (head_dim, 2*Hkv heads, R rows, L*n_slots), 64 x 1 x 32 x 1
+/// boxes; far: 2-D view (row_elems, n_slots*L*max_chunks rows), 64 x 1 boxes
+/// for gather4. Both with the 128-byte swizzle the UMMA descriptors expect.
+bool attn_tc_maps(const DevCtx &c, CUtensorMap *ring, CUtensorMap *far) {
+    const EncodeFn encode = encoder();
+    if (!encode)
+        return false;
+    const uint64_t row = uint64_t(c.hd) * c.esz;
+    const cuuint64_t dims[4] = {c.hd, 2ull * c.Hkv, c.R, uint64_t(c.L) * c.n_slots};
+    const cuuint64_t strides[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
+    const cuuint32_t box[4] = {64, 1, uint32_t(kSub), 1};
+    const cuuint32_t estr[4] = {1, 1, 1, 1};
+    if (encode(ring, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, c.ring, dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        return false;
+    const cuuint64_t fdims[2] = {c.row_elems, uint64_t(c.n_slots) * c.L * c.max_chunks};
+    const cuuint64_t fstrides[1] = {uint64_t(c.row_elems) * c.esz};
+    const cuuint32_t fbox[2] = {64, 1};
+    return encode(far, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, c.far, fdims, fstrides, fbox, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+void launch_attn_tc(const void *fn, const DevCtx &c, const CUtensorMap &ring, const CUtensorMap &far, uint32_t grid,
+                    cudaStream_t s) {
+    reinterpret_cast<TcFn>(const_cast<void *>(fn))<<<grid, kThreads, attn_tc_smem(), s>>>(c, ring, far);
+}
+
+} // namespace kvr

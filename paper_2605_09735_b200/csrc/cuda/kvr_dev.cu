@@ -247,7 +247,7 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         prepare_scan(c.max_scan);
         prepare_gather(c);
         if (g.attention) {
-            d->attn = make_attn_plan(c, d->sms, g.device);
+            d->attn = make_attn_plan(c, d->sms, g.device, int(g.attention));
             if (!d->attn)
                 throw std::runtime_error("no attention kernel for this head_dim/group/dtype");
         }

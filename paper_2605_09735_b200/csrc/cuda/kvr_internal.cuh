@@ -89,7 +89,15 @@ void launch_prime(const DevCtx &c, cudaStream_t s, int sms);   // window priming
 void launch_scan(const DevCtx &c, cudaStream_t s);             // stage + reduce
 void launch_gather(const DevCtx &c, cudaStream_t s, int sms);  // trains -> window
 struct AttnPlan;
-AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device); // builds the TMA descriptor
+/// mode: 1 auto (tensor cores for GQA groups where supported), 2 CUDA-core
+/// kernel, 3 tensor-core kernel (null if unsupported). Builds the TMA descriptor.
+AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode);
+// tensor-core variant (kvr_attn_tc.cu)
+bool attn_tc_supported(const DevCtx &c);
+const void *attn_tc_kernel(const DevCtx &c);
+bool attn_tc_maps(const DevCtx &c, CUtensorMap *ring, CUtensorMap *far);
+void launch_attn_tc(const void *fn, const DevCtx &c, const CUtensorMap &ring, const CUtensorMap &far, uint32_t grid,
+                    cudaStream_t s);
 void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s);
 void free_attn_plan(AttnPlan *p);
 const char *attn_variant(const AttnPlan *p);

@@ -337,7 +337,12 @@ struct ScenarioDriver::Impl {
         g.max_tokens = max_tok;
         g.max_chunks = cfg.far_view.enabled ? uint32_t(max_tok / cfg.far_view.chunk_tokens + 2) : 1;
         g.seed = cfg.seed;
-        g.attention = b.attention ? 1 : 0;
+        g.attention = !b.attention                           ? 0
+                      : b.attention_kernel == "cuda_core" ? 2
+                      : b.attention_kernel == "tcgen05"   ? 3
+                                                          : 1;
+        if (b.attention_kernel != "auto" && b.attention_kernel != "cuda_core" && b.attention_kernel != "tcgen05")
+            raise(Errc::bad_config, "b200.attention_kernel must be auto, cuda_core or tcgen05");
         g.use_graph = b.graph;
         g.max_desc_bytes = 0;
         g.max_scan_descs = 0;
@@ -1272,6 +1277,7 @@ static ScenarioConfig config_from_json(const ojson &j) {
         take(p, "dtype", c.b200.dtype);
         take(p, "trace", c.b200.trace);
         take(p, "attention", c.b200.attention);
+        take(p, "attention_kernel", c.b200.attention_kernel);
         take(p, "ring_rows", c.b200.ring_rows);
         take(p, "max_tokens", c.b200.max_tokens);
         take(p, "graph", c.b200.graph);

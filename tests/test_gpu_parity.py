@@ -109,6 +109,39 @@ def test_window_and_attention_lanes_payload(dtype, kvh, hd, qh):
     assert ob.check_driver_window_and_attention(d) <= 1e-3
 
 
+@pytest.mark.parametrize("dtype,kvh,qh,w_star", [("bf16", 2, 8, 96), ("bf16", 2, 8, 512),
+                                                 ("fp16", 2, 8, 512), ("bf16", 2, 16, 512),
+                                                 ("bf16", 2, 4, 300), ("fp16", 1, 8, 200)])
+def test_tcgen05_gqa_attention(dtype, kvh, qh, w_star):
+    """The tensor-core GQA kernel (tcgen05 S = K.Q^T and O = V^T.P, TMEM
+    accumulators) against the double-precision oracle, window tiles of every
+    alignment (W* 96..512, ragged window edges)."""
+    hd = 128
+    cfg = c1()
+    cfg["steps"] = 40
+    cfg["pager"]["kv_head_dim"] = kvh * hd
+    cfg["pager"]["page_bytes"] = 16 * 2 * 2 * kvh * hd * 2
+    cfg["transport"]["tau_bytes"] = 8 * cfg["pager"]["page_bytes"]
+    cfg["far_view"]["w_star"] = w_star
+    d = run(cfg, kv_heads=kvh, head_dim=hd, q_heads=qh, payload="lanes", dtype=dtype,
+            attention_kernel="tcgen05")
+    assert "tc" in d.device().attention_variant()
+    assert_scan_exact(d, 40)
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
+def test_tcgen05_far_view_bf16():
+    """Far summary rows (cp.async into the swizzled tile) through the tensor-core kernel."""
+    cfg = json.loads(read("far_config.json"))
+    cfg["steps"] = 250
+    cfg["pager"].update({"elem_bytes": 2, "kv_head_dim": 256})
+    d = run(cfg, kv_heads=2, head_dim=128, q_heads=8, payload="lanes", dtype="bf16",
+            attention_kernel="tcgen05")
+    assert "tc" in d.device().attention_variant()
+    assert_scan_exact(d, 250)
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
 def test_far_view_bf16_extension():
     """bf16 far view (a B200 extension: fp32 mean, RNE to bf16) runs at full width."""
     cfg = json.loads(read("far_config.json"))
