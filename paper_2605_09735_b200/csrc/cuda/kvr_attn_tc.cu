@@ -51,6 +51,26 @@ __device__ inline void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 __device__ inline void mbar_arrive(uint64_t *bar) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+#ifdef KVR_HANG_CHECK
+__device__ inline void mbar_wait(uint64_t *bar, uint32_t parity) {
+    for (uint64_t i = 0;; ++i) {
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok)
+                     : "r"(smem_u32(bar)), "r"(parity)
+                     : "memory");
+        if (ok)
+            return;
+        if (i == (1ull << 22) && blockIdx.x == 40 && (threadIdx.x & 31) == __ffs(__activemask()) - 1)
+            printf("hang: block %d thread %d bar smem+%u parity %u\n", blockIdx.x, threadIdx.x, smem_u32(bar),
+                   parity);
+        if (i == (1ull << 25))
+            asm volatile("trap;");
+    }
+}
+#else
 __device__ inline void mbar_wait(uint64_t *bar, uint32_t parity) {
     asm volatile("{\n\t.reg .pred p;\n\t"
                  "W_%=:\n\t"
@@ -59,6 +79,7 @@ __device__ inline void mbar_wait(uint64_t *bar, uint32_t parity) {
                  "r"(parity)
                  : "memory");
 }
+#endif
 __device__ inline void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3,
                                    uint64_t *bar) {
     asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
@@ -108,21 +129,45 @@ __device__ inline void tmem_ld16(uint32_t taddr, float (&v)[16]) {
         v[i] = __uint_as_float(r[i]);
 }
 
-template <typename T> __device__ inline uint16_t to_bits(float x);
-template <> __device__ inline uint16_t to_bits<__half>(float x) { return __half_as_ushort(__float2half_rn(x)); }
-template <> __device__ inline uint16_t to_bits<__nv_bfloat16>(float x) {
-    return __bfloat16_as_ushort(__float2bfloat16_rn(x));
-}
-template <typename T> __device__ inline float from_bits(uint16_t b);
-template <> __device__ inline float from_bits<__half>(uint16_t b) { return __half2float(__ushort_as_half(b)); }
-template <> __device__ inline float from_bits<__nv_bfloat16>(uint16_t b) {
-    return __bfloat162float(__ushort_as_bfloat16(b));
-}
+template <typename T> struct Pack2;
+template <> struct Pack2<__nv_bfloat16> {
+    static __device__ uint32_t round(float a, float b, float2 &back) {
+        const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+        back = __bfloat1622float2(h);
+        return *reinterpret_cast<const uint32_t *>(&h);
+    }
+};
+template <> struct Pack2<__half> {
+    static __device__ uint32_t round(float a, float b, float2 &back) {
+        const __half2 h = __floats2half2_rn(a, b);
+        back = __half22float2(h);
+        return *reinterpret_cast<const uint32_t *>(&h);
+    }
+};
 
-/// Byte offset of element (n, k) in a K-major, unswizzled N=16 operand
-/// (8x8 core matrices: 16-byte rows, K-adjacent cores 128 B apart).
-__device__ inline uint32_t op_off(uint32_t n, uint32_t k) {
-    return (n >> 3) * 2048u + (k >> 3) * 128u + (n & 7u) * 16u + (k & 7u) * 2u;
+/// Row k of an N=16 MMA operand held MN-major, unswizzled (8x8 core matrices of
+/// 8 K-rows x 16 B; K-adjacent cores 128 B apart, N halves 2048 B apart): the
+/// thread owning k writes x split as hi (columns [0, G)) + lo (columns [G, 2G))
+/// with two 16-byte stores. Columns >= 2G stay zero.
+template <typename T, int G> __device__ inline void store_split(uint8_t *op, uint32_t k, const float (&x)[G]) {
+    uint32_t wd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if constexpr (G == 1) {
+        float2 back;
+        wd[0] = Pack2<T>::round(x[0], 0.f, back);
+        float2 b2;
+        wd[0] = (wd[0] & 0xffffu) | (Pack2<T>::round(x[0] - back.x, 0.f, b2) << 16);
+    } else {
+#pragma unroll
+        for (int g = 0; g < G; g += 2) {
+            float2 back, unused;
+            wd[g / 2] = Pack2<T>::round(x[g], x[g + 1], back);
+            wd[G / 2 + g / 2] = Pack2<T>::round(x[g] - back.x, x[g + 1] - back.y, unused);
+        }
+    }
+    uint8_t *row = op + (k >> 3) * 128u + (k & 7u) * 16u;
+    *reinterpret_cast<uint4 *>(row) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
+    if constexpr (2 * G > 8)
+        *reinterpret_cast<uint4 *>(row + 2048) = make_uint4(wd[4], wd[5], wd[6], wd[7]);
 }
 
 /// Tiles of one work item, identical for every role.
@@ -166,6 +211,71 @@ __device__ inline void tma_gather4(uint32_t dst, const CUtensorMap *map, int col
                  "r"(smem_u32(bar))
                  : "memory");
 }
+
+__device__ inline bool elect_one() {
+    uint32_t pred;
+    asm volatile("{\n\t.reg .pred P;\n\t"
+                 "elect.sync _|P, 0xffffffff;\n\t"
+                 "selp.u32 %0, 1, 0, P;\n\t}"
+                 : "=r"(pred));
+    return pred != 0;
+}
+
+/// The j-th active item (live, >= 1 tile) of a CTA belongs to warpgroup j % 2.
+struct Cursor {
+    uint32_t it, j;
+    __device__ void init() { it = blockIdx.x, j = 0; }
+    __device__ bool next(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items, uint32_t w, Item &I) {
+        for (; it < n_items; it += gridDim.x) {
+            if (!item_of(c, slots, it, I) || I.n_far + I.n_near == 0)
+                continue;
+            if ((j++ & 1u) == w) {
+                it += gridDim.x;
+                return true;
+            }
+        }
+        return false;
+    }
+};
+
+/// Tile stream of the producer and the MMA issuer. Items alternate between the
+/// two warpgroups; with kInterleave their tiles alternate too, otherwise an
+/// item's tiles are consecutive and the warpgroups overlap at item boundaries.
+#ifndef KVR_TC_INTERLEAVE
+#define KVR_TC_INTERLEAVE 0
+#endif
+constexpr bool kInterleave = KVR_TC_INTERLEAVE != 0;
+struct Stream { // (no arrays indexed by w: everything stays in registers)
+    Cursor c0, c1;
+    Item I0, I1;
+    bool h0, h1;
+    uint32_t k0, k1, turn;
+    __device__ void init(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items) {
+        c0.init();
+        c1.init();
+        h0 = c0.next(c, slots, n_items, 0, I0);
+        h1 = c1.next(c, slots, n_items, 1, I1);
+        k0 = k1 = turn = 0;
+    }
+    /// Warpgroup, tile index and item of the next tile; false at the end.
+    __device__ bool next(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items, uint32_t &w, uint32_t &kk,
+                         Item &I) {
+        if (!h0 && !h1)
+            return false;
+        w = (turn ? h1 : !h0) ? 1u : 0u;
+        turn = kInterleave ? w ^ 1u : w;
+        if (w) {
+            kk = k1, I = I1;
+            if (++k1 == I1.n_far + I1.n_near)
+                h1 = c1.next(c, slots, n_items, 1, I1), k1 = 0, turn = 0;
+        } else {
+            kk = k0, I = I0;
+            if (++k0 == I0.n_far + I0.n_near)
+                h0 = c0.next(c, slots, n_items, 0, I0), k0 = 0, turn = 1;
+        }
+        return true;
+    }
+};
 
 /// Per-softmax-warpgroup barriers and operand buffers.
 struct WgBars {
@@ -225,142 +335,144 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) { // ---------------- producer (one thread) ----------------
+    if (warp == 0) { // ---------------- producer (whole warp; lanes issue the TMA ops of a tile) ----------------
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&far_map)) : "memory");
-            uint32_t s = 0, ph = 0;
-            for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-                Item I;
-                if (!item_of(c, slots, it, I))
-                    continue;
-                const int plane = int(I.slot * c.L + I.layer);
-                for (uint32_t k = 0; k < I.n_far + I.n_near; ++k) {
-                    mbar_wait(&empty[s], ph ^ 1);
-                    uint8_t *st = stages + s * kStageBytes;
-                    if (k < I.n_far) {
-                        // far summary rows: TMA gather4, 4 rows x 64 columns per op
-                        const uint32_t r0 = k * kRows, nr = min(uint32_t(kRows), I.far_count - r0);
-                        const uint32_t n4 = (nr + 3) / 4;
-                        mbar_expect_tx(&full[s], n4 * 4 * 512);
-                        const int base = plane * int(c.max_chunks);
-                        const uint32_t *ids = far_ids + I.far_begin + r0;
-                        for (uint32_t g4 = 0; g4 < n4; ++g4) {
-                            int r[4];
+        }
+        Stream S;
+        S.init(c, slots, n_items);
+        uint32_t s = 0, ph = 0, w, k, row_base = 0;
+        Item I;
+        while (S.next(c, slots, n_items, w, k, I)) {
+            const int plane = int(I.slot * c.L + I.layer);
+            if (k == 0)
+                row_base = uint32_t(I.t0 % c.R); // ring row of the first near tile
+            mbar_wait(&empty[s], ph ^ 1);
+            const uint32_t st = smem_u32(stages + s * kStageBytes);
+            if (k < I.n_far) {
+                // far summary rows: TMA gather4, 4 rows x 64 columns per op; op o = 4 * group + (kv, half)
+                const uint32_t r0 = k * kRows, nr = min(uint32_t(kRows), I.far_count - r0);
+                const uint32_t n4 = (nr + 3) / 4;
+                if (lane == 0)
+                    mbar_expect_tx(&full[s], n4 * 4 * 512);
+                __syncwarp();
+                const int base = plane * int(c.max_chunks);
+                const uint32_t *ids = far_ids + I.far_begin + r0;
+                for (uint32_t o = lane; o < 4 * n4; o += 32) {
+                    const uint32_t g4 = o >> 2, kv = (o >> 1) & 1u, hf = o & 1u;
+                    int r[4];
 #pragma unroll
-                            for (int x = 0; x < 4; ++x)
-                                r[x] = base + int(ids[min(4 * g4 + x, nr - 1)]);
-                            for (int kv = 0; kv < 2; ++kv)
-                                for (int hf = 0; hf < 2; ++hf)
-                                    tma_gather4(smem_u32(st + (2 * kv + hf) * kHalfBytes + g4 * 512), &far_map,
-                                                int((kv ? c.Hkv + I.head : I.head) * kHd + hf * 64), r[0], r[1],
-                                                r[2], r[3], &full[s]);
-                        }
-                    } else {
-                        const uint64_t tb = I.t0 + uint64_t(k - I.n_far) * kRows;
-                        uint32_t live_boxes = 0;
-                        for (int b = 0; b < kRows / kSub; ++b) {
-                            const uint64_t a = tb + b * kSub;
-                            live_boxes |= uint32_t(a < I.w && a + kSub > I.lo) << b;
-                        }
-                        mbar_expect_tx(&full[s], __popc(live_boxes) * 4 * kSub * 128);
-                        for (int b = 0; b < kRows / kSub; ++b) {
-                            if (!(live_boxes >> b & 1u))
-                                continue;
-                            const int row = int((tb + b * kSub) % c.R);
-                            for (int kv = 0; kv < 2; ++kv)
-                                for (int hf = 0; hf < 2; ++hf)
-                                    tma_load_4d(smem_u32(st + (2 * kv + hf) * kHalfBytes + b * kSub * 128),
-                                                &ring_map, hf * 64, int(kv ? c.Hkv + I.head : I.head), row, plane,
-                                                &full[s]);
-                        }
+                    for (int x = 0; x < 4; ++x)
+                        r[x] = base + int(ids[min(4 * g4 + x, nr - 1)]);
+                    tma_gather4(st + (2 * kv + hf) * kHalfBytes + g4 * 512, &far_map,
+                                int((kv ? c.Hkv + I.head : I.head) * kHd + hf * 64), r[0], r[1], r[2], r[3],
+                                &full[s]);
+                }
+            } else {
+                const uint32_t kn = k - I.n_far;
+                const uint64_t tb = I.t0 + uint64_t(kn) * kRows;
+                uint32_t live_boxes = 0;
+#pragma unroll
+                for (int bx = 0; bx < kRows / kSub; ++bx) {
+                    const uint64_t a0 = tb + bx * kSub;
+                    live_boxes |= uint32_t(a0 < I.w && a0 + kSub > I.lo) << bx;
+                }
+                if (lane == 0)
+                    mbar_expect_tx(&full[s], __popc(live_boxes) * 4 * kSub * 128);
+                __syncwarp();
+                if (lane < 16) { // lane = box * 4 + (kv, half)
+                    const uint32_t bx = lane >> 2, kv = (lane >> 1) & 1u, hf = lane & 1u;
+                    if (live_boxes >> bx & 1u) {
+                        uint32_t row = row_base + kn * kRows + bx * kSub;
+                        while (row >= c.R)
+                            row -= c.R;
+                        tma_load_4d(st + (2 * kv + hf) * kHalfBytes + bx * kSub * 128, &ring_map, int(hf * 64),
+                                    int(kv ? c.Hkv + I.head : I.head), int(row), plane, &full[s]);
                     }
+                }
+            }
+            if (++s == kStages) {
+                s = 0;
+                ph ^= 1;
+            }
+        }
+    } else if (warp == 1) { // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
+        constexpr uint32_t fmt = std::is_same_v<T, __nv_bfloat16> ? 1u : 0u;
+        constexpr uint32_t id_s = idesc(fmt, 0, 1, kRows, kN); // S^T = K . Q^T (Q MN-major)
+        constexpr uint32_t id_o = idesc(fmt, 1, 1, kHd, kN);   // O^T = V^T . P (both MN-major)
+        // Event loop over mbarrier states (uniform across the warp): issue S for
+        // the next tile of the stream as soon as its K tile, S buffer and Q are
+        // ready, and each warpgroup's oldest pending PV as soon as its P is.
+        Stream S;
+        S.init(c, slots, n_items);
+        uint32_t s = 0, ph = 0, w = 0, k = 0;
+        uint32_t nw0 = 0, nw1 = 0, mw0 = 0, mw1 = 0, pv0 = 0, pv1 = 0;
+        uint32_t ring0 = 0, ring1 = 0; // pending tiles per warpgroup: byte (n & 3) = stage | K steps << 2
+        const uint32_t stage0 = smem_u32(stages), wg0 = smem_u32(wgbuf);
+        auto ready = [&](uint64_t *bar, uint32_t par) { return __shfl_sync(0xffffffffu, mbar_test(bar, par), 0); };
+        Item I;
+        bool have = S.next(c, slots, n_items, w, k, I);
+        while (have || pv0 < nw0 || pv1 < nw1) {
+            if (have) {
+                const uint32_t nwc = w ? nw1 : nw0, b = nwc & 1u;
+                if ((k > 0 || ready(&wb[w].qfull, (w ? mw1 : mw0) & 1u)) && ready(&full[s], ph) &&
+                    ready(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u)) {
+                    tc_fence_after();
+                    if (elect_one()) {
+                        const uint64_t a0 = sdesc(stage0 + s * kStageBytes, 16, 1024, 2);
+                        const uint64_t b0 = sdesc(wg0 + w * kWgBytes, 128, 2048, 0);
+#pragma unroll
+                        for (uint32_t kk = 0; kk < kHd / 16; ++kk) // K: 32 B steps in a 128-B row, then next half
+                            mma_f16(tmem + 64 * w + 16 * b, a0 + (((kk >> 2) * kHalfBytes + (kk & 3u) * 32) >> 4),
+                                    b0 + kk * (256 >> 4), id_s, kk > 0);
+                        mma_commit(&wb[w].sfull[b]);
+                    }
+                    __syncwarp();
+                    if (k == 0)
+                        (w ? mw1 : mw0) += 1;
+                    const uint32_t nk =
+                        k < I.n_far ? (min(uint32_t(kRows), I.far_count - k * kRows) + 15) / 16 : kRows / 16;
+                    const uint32_t sh = 8 * (nwc & 3u), e = (s | nk << 2) << sh;
+                    if (w)
+                        ring1 = (ring1 & ~(0xffu << sh)) | e;
+                    else
+                        ring0 = (ring0 & ~(0xffu << sh)) | e;
+                    (w ? nw1 : nw0) += 1;
                     if (++s == kStages) {
                         s = 0;
                         ph ^= 1;
                     }
+                    have = S.next(c, slots, n_items, w, k, I);
                 }
             }
-        }
-    } else if (warp == 1) { // ---------------- MMA issuer (one thread) ----------------
-        if (lane == 0) {
-            constexpr uint32_t fmt = std::is_same_v<T, __nv_bfloat16> ? 1u : 0u;
-            constexpr uint32_t id_s = idesc(fmt, 0, 0, kRows, kN); // S^T = K . Q^T
-            constexpr uint32_t id_o = idesc(fmt, 1, 0, kHd, kN);   // O^T = V^T . P
-            struct Pend {
-                uint32_t stage, n, nk;
-            };
-            Pend fifo[2][4];
-            uint32_t head[2] = {0, 0}, size[2] = {0, 0};
-            uint32_t nw[2] = {0, 0}, mw[2] = {0, 0};
-            uint32_t s = 0, ph = 0, j = 0, k = 0;
-            uint32_t it = blockIdx.x;
-            Item I;
-            bool have = false;
-            auto next_item = [&]() {
-                have = false;
-                for (; it < n_items; it += gridDim.x)
-                    if (item_of(c, slots, it, I) && I.n_far + I.n_near > 0) {
-                        have = true;
-                        it += gridDim.x;
-                        break;
-                    }
-                k = 0;
-            };
-            next_item();
-            while (have || size[0] || size[1]) {
-                bool progress = false;
-                if (have) { // S for the next tile in stream order
-                    const uint32_t w = j & 1u, b = nw[w] & 1u;
-                    if ((k > 0 || mbar_test(&wb[w].qfull, mw[w] & 1u)) && mbar_test(&full[s], ph) &&
-                        mbar_test(&wb[w].sempty[b], ((nw[w] >> 1) & 1u) ^ 1u) && size[w] < 4) {
-                        tc_fence_after();
-                        const uint32_t kt = smem_u32(stages + s * kStageBytes);
-                        const uint32_t q = smem_u32(wgbuf + w * kWgBytes);
-                        for (uint32_t kk = 0; kk < kHd / 16; ++kk)
-                            mma_f16(tmem + 64 * w + 16 * b,
-                                    sdesc(kt + (kk >> 2) * kHalfBytes + (kk & 3u) * 32, 16, 1024, 2),
-                                    sdesc(q + kk * 256, 128, 2048, 0), id_s, kk > 0);
-                        mma_commit(&wb[w].sfull[b]);
-                        const uint32_t nk =
-                            k < I.n_far ? (min(uint32_t(kRows), I.far_count - k * kRows) + 15) / 16 : kRows / 16;
-                        fifo[w][(head[w] + size[w]) & 3u] = Pend{s, nw[w], nk};
-                        ++size[w];
-                        ++nw[w];
-                        if (++s == kStages) {
-                            s = 0;
-                            ph ^= 1;
-                        }
-                        if (++k == I.n_far + I.n_near) {
-                            ++mw[w];
-                            ++j;
-                            next_item();
-                        }
-                        progress = true;
-                    }
+#pragma unroll
+            for (uint32_t x = 0; x < 2; ++x) {
+                const uint32_t pvn = x ? pv1 : pv0;
+                if (pvn >= (x ? nw1 : nw0))
+                    continue;
+                const uint32_t b = pvn & 1u, par = (pvn >> 1) & 1u;
+                if (!ready(&wb[x].pfull[b], par) || !ready(&wb[x].oempty[b], par ^ 1u))
+                    continue;
+                const uint32_t e = ((x ? ring1 : ring0) >> (8 * (pvn & 3u))) & 0xffu, st = e & 3u, nk = e >> 2;
+                tc_fence_after();
+                if (elect_one()) {
+                    const uint64_t a0 = sdesc(stage0 + st * kStageBytes + 2 * kHalfBytes, kHalfBytes, 1024, 2);
+                    const uint64_t b0 = sdesc(wg0 + x * kWgBytes + (1 + b) * kOpBytes, 128, 2048, 0);
+                    for (uint32_t kk = 0; kk < nk; ++kk) // +2048 B (V rows) / +256 B (P cores) per K step
+                        mma_f16(tmem + 64 * x + 32 + 16 * b, a0 + kk * (2048 >> 4), b0 + kk * (256 >> 4), id_o,
+                                kk > 0);
+                    mma_commit(&wb[x].ofull[b]);
+                    mma_commit(&empty[st]);
                 }
-                for (uint32_t w = 0; w < 2; ++w) { // PV for each warpgroup's oldest tile
-                    if (!size[w])
-                        continue;
-                    const Pend p = fifo[w][head[w]];
-                    const uint32_t b = p.n & 1u, par = (p.n >> 1) & 1u;
-                    if (!mbar_test(&wb[w].pfull[b], par) || !mbar_test(&wb[w].oempty[b], par ^ 1u))
-                        continue;
-                    tc_fence_after();
-                    const uint32_t v = smem_u32(stages + p.stage * kStageBytes + 2 * kHalfBytes);
-                    const uint32_t pa = smem_u32(wgbuf + w * kWgBytes + (1 + b) * kOpBytes);
-                    for (uint32_t kk = 0; kk < p.nk; ++kk)
-                        mma_f16(tmem + 64 * w + 32 + 16 * b, sdesc(v + kk * 2048, kHalfBytes, 1024, 2),
-                                sdesc(pa + kk * 256, 128, 2048, 0), id_o, kk > 0);
-                    mma_commit(&wb[w].ofull[b]);
-                    mma_commit(&empty[p.stage]);
-                    head[w] = (head[w] + 1) & 3u;
-                    --size[w];
-                    progress = true;
-                }
-                (void)progress;
+                __syncwarp();
+                (x ? pv1 : pv0) += 1;
             }
         }
+#ifdef KVR_HANG_CHECK
+        if (blockIdx.x == 40 && lane == 0)
+            printf("mma done: tiles %u %u items %u %u\n", nw0, nw1, mw0, mw1);
+#endif
     } else if (warp >= 4) { // ---------------- softmax / correction warpgroups ----------------
         const uint32_t w = uint32_t(warp - 4) >> 2;     // warpgroup 0: warps 4-7, 1: warps 8-11
         const uint32_t t = threadIdx.x - 128 - 128 * w; // TMEM lane: token row of S, head dim of O
@@ -372,32 +484,29 @@ __global__ void __launch_bounds__(kThreads, 1)
         float *rd = red + w * 2 * 4 * 8;
         float *ld = lred + w * 4 * 8;
         const float scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
-        uint32_t n = 0, j = 0, m_items = 0;
-        for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-            Item I;
-            if (!item_of(c, slots, it, I))
-                continue;
-            float *o = c.out + ((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G) * kHd;
-            if (I.n_far + I.n_near == 0) {
-                if (w == 0)
+        if (w == 0) // live slots with an empty window: zero output
+            for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
+                Item I;
+                if (item_of(c, slots, it, I) && I.n_far + I.n_near == 0)
 #pragma unroll
                     for (int g = 0; g < G; ++g)
-                        o[g * kHd + t] = 0.f;
-                continue;
+                        c.out[((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G + g) * kHd + t] =
+                            0.f;
             }
-            if ((j++ & 1u) != w)
-                continue; // the other warpgroup's item
+        uint32_t n = 0, m_items = 0;
+        Cursor cur;
+        cur.init();
+        Item I;
+        while (cur.next(c, slots, n_items, w, I)) {
+            float *o = c.out + ((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G) * kHd;
             // Q (hi | lo) of this kv head's q-heads; thread t owns head dim t
             {
                 const float *qs = c.q + ((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G) * kHd;
+                float x[G];
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const float x = qs[g * kHd + t];
-                    const uint16_t hi = to_bits<T>(x);
-                    const uint16_t lo = to_bits<T>(x - from_bits<T>(hi));
-                    *reinterpret_cast<uint16_t *>(qb + op_off(g, t)) = hi;
-                    *reinterpret_cast<uint16_t *>(qb + op_off(G + g, t)) = lo;
-                }
+                for (int g = 0; g < G; ++g)
+                    x[g] = qs[g * kHd + t];
+                store_split<T, G>(qb, t, x);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0)
@@ -454,7 +563,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     for (int g = 0; g < G; ++g)
                         rd[(b * 4 + wq) * 8 + g] = mx[g];
                 asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
-                float alpha[G];
+                float alpha[G], pv[G];
                 uint8_t *pb = qb + (1 + b) * kOpBytes;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
@@ -465,11 +574,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const float p = valid ? exp2f(sc[g] - mn) : 0.f;
                     l[g] = l[g] * alpha[g] + p;
                     m[g] = mn;
-                    const uint16_t hi = to_bits<T>(p);
-                    const uint16_t lo = to_bits<T>(p - from_bits<T>(hi));
-                    *reinterpret_cast<uint16_t *>(pb + op_off(g, t)) = hi;
-                    *reinterpret_cast<uint16_t *>(pb + op_off(G + g, t)) = lo;
+                    pv[g] = p;
                 }
+                store_split<T, G>(pb, t, pv);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0)
@@ -499,7 +606,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
             asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory"); // ld reused by the next item
         }
-        (void)m_items;
+#ifdef KVR_HANG_CHECK
+        if (blockIdx.x == 40 && (threadIdx.x & 127) == 0)
+            printf("wg %u done: tiles %u items %u\n", w, n, m_items);
+#endif
     }
     tc_fence_before();
     __syncthreads();

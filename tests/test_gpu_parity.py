@@ -130,6 +130,29 @@ def test_tcgen05_gqa_attention(dtype, kvh, qh, w_star):
     assert ob.check_driver_window_and_attention(d) <= 1e-3
 
 
+@pytest.mark.parametrize("far", [False, True])
+def test_tcgen05_many_items_per_cta(far):
+    """More (slot, layer, kv-head) items than 2 x SMs: both softmax warpgroups
+    run interleaved item streams and one runs out first (the single-warpgroup
+    tail of the schedule)."""
+    cfg = c1()
+    del cfg["trace_path"]
+    cfg["steps"] = 48
+    cfg["pager"].update({"layers": 8, "kv_head_dim": 256, "page_bytes": 16 * 2 * 8 * 256 * 2})
+    cfg["transport"]["tau_bytes"] = 8 * cfg["pager"]["page_bytes"]
+    cfg["workload"] = {"requests": 10000, "concurrency": 40, "prompt_min": 64, "prompt_max": 1024,
+                       "arrivals_per_window": 40.0, "seed": 1}
+    cfg["shaping"] = {"arena_pages": 6000, "staged_refresh_period": 4}
+    if far:
+        cfg["far_view"] = {"enabled": True, "w_star": 256, "cap": 16, "sv_chunk": 64}
+    d = run(cfg, kv_heads=2, head_dim=128, q_heads=8, payload="lanes", dtype="bf16",
+            attention_kernel="tcgen05")
+    assert "tc" in d.device().attention_variant()
+    assert_scan_exact(d, 48)
+    slots = [s for s, _, _ in d.live()][:6]
+    assert ob.check_driver_window_and_attention(d, only_slots=slots) <= 1e-3
+
+
 def test_tcgen05_far_view_bf16():
     """Far summary rows (cp.async into the swizzled tile) through the tensor-core kernel."""
     cfg = json.loads(read("far_config.json"))
