@@ -210,48 +210,98 @@ __global__ void k_query(DevCtx c) {
 }
 
 // ---------------------------------------------------------------------------
-// K-far: summary of chunk [aux, aux + chunk_tokens) of a slot, one thread per
-// lane, double accumulation in token order, float(acc * (1/count)) (bit-exact
-// with far_view.cpp:36-46 for fp32 lanes; fp16/bf16 lanes round to nearest even).
+// K-far: summary of chunk [aux, aux + chunk_tokens) of a slot: double
+// accumulation in token order, float(acc * (1/count)) (bit-exact with
+// far_view.cpp:36-46 for fp32 lanes; fp16/bf16 lanes round to nearest even).
+// Streams 16-byte columns (coalesced, 4 rows in flight per thread).
 
-__device__ inline double load_lane(const DevCtx &c, const uint8_t *p, uint64_t lane) {
-    if (c.esz == 4)
-        return double(reinterpret_cast<const float *>(p)[lane]);
-    const uint16_t b = reinterpret_cast<const uint16_t *>(p)[lane];
-    return c.elem_kind == KVR_ELEM_BF16 ? double(__bfloat162float(__ushort_as_bfloat16(b)))
-                                        : double(__half2float(__ushort_as_half(b)));
+template <int E> __device__ inline void add_chunk(const DevCtx &c, int4 v, double (&acc)[16 / E]) {
+    if constexpr (E == 4) {
+        acc[0] += double(__int_as_float(v.x)), acc[1] += double(__int_as_float(v.y));
+        acc[2] += double(__int_as_float(v.z)), acc[3] += double(__int_as_float(v.w));
+    } else {
+        const uint32_t w[4] = {uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w)};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            float2 f;
+            if (c.elem_kind == KVR_ELEM_BF16)
+                f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w[i]));
+            else
+                f = __half22float2(*reinterpret_cast<const __half2 *>(&w[i]));
+            acc[2 * i] += double(f.x), acc[2 * i + 1] += double(f.y);
+        }
+    }
 }
 
-__global__ void k_far(DevCtx c) {
+/// One CTA per (far job, 4 KiB column block): every thread streams one 16-byte
+/// column of the chunk's rows (row offsets staged in shared memory).
+template <int E> __device__ void far_columns(const DevCtx &c, const kvr_write_op &op, uint64_t col,
+                                             const uint64_t *rows, uint32_t n_rows) {
+    constexpr int N = 16 / E;
+    double acc[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i)
+        acc[i] = 0.0;
+    uint32_t k = 0;
+    for (; k + 4 <= n_rows; k += 4) { // four independent loads in flight
+        int4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            v[u] = rows[k + u] == ~0ull ? make_int4(0, 0, 0, 0)
+                                        : __ldcs(reinterpret_cast<const int4 *>(c.arena + rows[k + u] + col));
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+            add_chunk<E>(c, v[u], acc);
+    }
+    for (; k < n_rows; ++k)
+        if (rows[k] != ~0ull)
+            add_chunk<E>(c, __ldcs(reinterpret_cast<const int4 *>(c.arena + rows[k] + col)), acc);
+    uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot) * c.token_bytes + col;
+    const double inv = 1.0 / double(c.chunk_tokens);
+    if constexpr (E == 4) {
+        *reinterpret_cast<float4 *>(dst) = make_float4(float(acc[0] * inv), float(acc[1] * inv),
+                                                       float(acc[2] * inv), float(acc[3] * inv));
+    } else {
+        uint16_t o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float m = float(acc[i] * inv);
+            o[i] = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(m) : f2h_bits(m);
+        }
+        *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(o);
+    }
+}
+
+constexpr uint32_t kFarRows = 512; // chunk rows staged in shared memory
+
+__global__ void __launch_bounds__(256) k_far(DevCtx c) {
+    __shared__ uint64_t rows[kFarRows];
     const kvr_step_header *h = hdr(c);
     // far jobs are packed after the token writes
     const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write) + (h->n_write - h->n_far_jobs);
-    const uint64_t lanes = c.token_bytes / c.esz;
-    const uint64_t lane_blocks = (lanes + blockDim.x - 1) / blockDim.x;
-    const uint64_t work = uint64_t(h->n_far_jobs) * lane_blocks;
+    const uint64_t cols = c.token_bytes / 16; // 16-byte columns per row
+    const uint64_t col_blocks = (cols + blockDim.x - 1) / blockDim.x;
+    const uint64_t work = uint64_t(h->n_far_jobs) * col_blocks;
+    const uint32_t n_rows = min(c.chunk_tokens, kFarRows);
     for (uint64_t u = blockIdx.x; u < work; u += gridDim.x) {
-        const kvr_write_op op = ops[u / lane_blocks];
+        const kvr_write_op op = ops[u / col_blocks];
+        __syncthreads(); // rows[] of the previous unit consumed
         if (op.source != 1)
             continue;
-        const uint64_t lane = (u % lane_blocks) * blockDim.x + threadIdx.x;
-        if (lane >= lanes)
-            continue;
-        double acc = 0.0;
         const uint32_t *tm = c.tmap + uint64_t(op.dev_slot) * c.max_tokens;
-        for (uint32_t k = 0; k < c.chunk_tokens; ++k) {
+        for (uint32_t k = threadIdx.x; k < n_rows; k += blockDim.x) {
             const uint64_t tok = op.aux + k;
             const uint32_t gs = tok < c.max_tokens ? tm[tok] : kNoMap;
-            if (gs == kNoMap)
-                continue; // unmapped source: contributes zeros (host validated coverage)
-            acc += load_lane(c, c.arena + gslot_offset(c, gs), lane);
+            rows[k] = gs == kNoMap ? ~0ull : gslot_offset(c, gs); // unmapped: zeros (host validated coverage)
         }
-        const float mean = float(acc * (1.0 / double(c.chunk_tokens)));
-        uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot) * c.token_bytes;
+        __syncthreads();
+        const uint64_t col = (u % col_blocks) * blockDim.x + threadIdx.x;
+        if (col >= cols)
+            continue;
         if (c.esz == 4)
-            reinterpret_cast<float *>(dst)[lane] = mean;
+            far_columns<4>(c, op, col * 16, rows, n_rows);
         else
-            reinterpret_cast<uint16_t *>(dst)[lane] =
-                c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(mean) : f2h_bits(mean);
+            far_columns<2>(c, op, col * 16, rows, n_rows);
     }
 }
 

@@ -324,6 +324,10 @@ struct ScenarioDriver::Impl {
         g.ring_rows = b.ring_rows ? b.ring_rows : (need_rows + 31) / 32 * 32;
         g.far_cap = cfg.far_view.enabled ? cfg.far_view.cap : 0;
         g.chunk_tokens = cfg.far_view.chunk_tokens;
+        if (cfg.far_view.enabled && g.chunk_tokens > 512)
+            raise(Errc::bad_config, "b200 far view: sv_chunk must be <= 512 tokens");
+        if (g.token_bytes % 16)
+            raise(Errc::bad_config, "b200: token_bytes must be a multiple of 16");
         uint64_t max_tok = b.max_tokens;
         if (!max_tok) {
             uint32_t pmax = 1;
