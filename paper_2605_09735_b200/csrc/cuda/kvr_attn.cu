@@ -6,15 +6,16 @@
 // masked. Definition: attend() of far_view.cpp:113-155 per (layer, q-head)
 // with GQA q-head j -> kv-head j / group, fp32 accumulation (1e-3 rel. bound).
 //
-// Per CTA: one producer warp streams 32-token x G-head K and V tiles out of the
-// ring with 4-D TMA tensor loads (cp.async.bulk.tensor, mbarrier completion)
-// into a multi-stage shared-memory ring; G consumer warps (one per kv head)
-// compute. QK^T: lane <-> token, each lane walks the head dimension with a
-// lane-rotated column order (bank-conflict free on the unpadded TMA tile) and
-// reuses every K element for all `group` q-heads. PV: lane <-> output dims,
-// probabilities broadcast by shuffles. Online softmax in base 2. Decode
-// attention with g <= 8 is far below the tensor-core ridge (g flop/byte), so
-// this is a warp GEMV; a tcgen05 path for large GQA groups is DESIGN.md §6.
+// Per CTA (persistent): one producer warp streams K and V half-tiles (16 rows x G
+// heads) out of the ring with 4-D TMA tensor loads (cp.async.bulk.tensor,
+// mbarrier completion) into a 3-stage shared-memory ring, skipping halves with no
+// live row; 2*G consumer warps, a pair per kv head, take 16 rows each. QK^T: lane
+// <-> head dims with q in registers, the 16 per-row partial dot products are
+// reduce-scattered by a halving shuffle butterfly (lane l ends with row l >> 1).
+// PV: lane <-> head dims, probabilities broadcast by shuffles. Online softmax in
+// base 2; the pair merges its states through shared memory at item end. At g = 1
+// this is a warp GEMV at the HBM roofline; GQA groups g >= 4 with head_dim 128 use
+// the tcgen05 kernel in kvr_attn_tc.cu.
 #include <algorithm>
 #include <cstdio>
 #include <cudaTypedefs.h>
