@@ -143,50 +143,63 @@ def peaks() -> dict:
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock and throttle reasons sampled DURING the timed region
+    (B200_PROFILING.md clocks line): NVML polled every 2 ms on a thread, so even
+    a short timed region gets samples; nvidia-smi as the fallback."""
+    NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
+             "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
+             "sw_thermal_slowdown": "nvmlClocksEventReasonSwThermalSlowdown",
+             "sw_power_cap": "nvmlClocksEventReasonSwPowerCap",
+             "hw_power_brake_slowdown": "nvmlClocksEventReasonHwPowerBrakeSlowdown"}
 
     def __init__(self, device: int):
-        self.device = device
-        self.rows: list[list[str]] = []
-        self.proc = None
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES", "")
+        ids = [x for x in vis.split(",") if x.strip()]
+        self.device = int(ids[device]) if device < len(ids) and ids[device].isdigit() else device
+        self.sm, self.max_sm, self.reasons = [], [], set()
+        self.stop = threading.Event()
+        self.thread = None
+
+    def _poll(self):
+        import pynvml as nv
+        h = nv.nvmlDeviceGetHandleByIndex(self.device)
+        self.max_sm.append(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        masks = {k: getattr(nv, v) for k, v in self.NAMES.items() if hasattr(nv, v)}
+        while not self.stop.is_set():
+            self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
+            r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.reasons.update(k for k, m in masks.items() if r & m)
+            time.sleep(0.002)
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
+            time.sleep(0.01)  # first sample before the timed region starts
         except Exception:
-            self.proc = None
+            self.thread = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *a):
-        if self.proc:
-            time.sleep(0.15)
-            self.proc.terminate()
+        self.stop.set()
+        if self.thread:
+            self.thread.join(timeout=1)
+        if not self.sm:  # NVML unavailable: one nvidia-smi reading
+            q = "clocks.sm,clocks.max.sm"
             try:
-                self.proc.wait(timeout=2)
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=10).stdout.split(",")
+                self.sm, self.max_sm = [float(out[0])], [float(out[1])]
             except Exception:
-                self.proc.kill()
+                pass
 
     def summary(self) -> dict:
-        sm = [float(r[0]) for r in self.rows if r and r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if len(r) > 1 and r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4)
-                          if len(r) > 3 + i and r[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(sm)}
+        return {"sm_mhz": statistics.median(self.sm) if self.sm else None,
+                "sm_max_mhz": max(self.max_sm) if self.max_sm else None,
+                "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
 
 
 def dist_setup():
@@ -270,6 +283,13 @@ def run_b200(args, rank, local, world) -> dict | None:
         t1 = time.perf_counter()
     barrier(world)
     recs = [d.record(s) for s in range(first, first + args.steps)]
+    if args.dump_steps and rank == 0:  # per-step records for latency analysis
+        with open(args.dump_steps, "w") as f:
+            json.dump([{"step": r.step, "live": r.live_sessions, "emitted": r.emitted_tokens,
+                        "trains": r.trains, "dma": r.dma_bytes, "device_ms": r.device_ms,
+                        "wall_ms": lat_ms[i] if i < len(lat_ms) else None,
+                        "writeback_tokens": r.writeback_tokens, "h2d": r.h2d_bytes,
+                        "phases": list(r.phase_ms)[:7]} for i, r in enumerate(recs)], f)
     dev_s = sum(r.device_ms for r in recs) / 1e3
     wall_s = t1 - t0
     tokens = sum(r.emitted_tokens for r in recs)
@@ -280,13 +300,14 @@ def run_b200(args, rank, local, world) -> dict | None:
     h2d = sum(r.h2d_bytes for r in recs) / args.steps
     dev = d.device()
     variant = dev.attention_variant()
+    step_kernels = dev.step_kernels()
     dev_s_max, wall_s_max = reduce_max([dev_s, wall_s], world)
     tokens_all, gather_bytes_all = reduce_sum([float(tokens), float(gather_bytes)], world)
     out = {
         "rank": rank, "cfg": cfg, "recs": recs, "dev_s": dev_s_max, "wall_s": wall_s_max,
         "tokens": tokens_all, "attn_bytes": attn_bytes, "attn_s": attn_s,
         "gather_bytes": gather_bytes, "gather_s": gather_s, "gather_bytes_all": gather_bytes_all,
-        "h2d": h2d, "variant": variant, "clocks": clocks.summary(), "fill_steps": fill,
+        "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "clocks": clocks.summary(), "fill_steps": fill,
         "live_mean": statistics.mean(r.live_sessions for r in recs),
         "trains_mean": statistics.mean(r.trains for r in recs),
         "dma_mean": statistics.mean(r.dma_bytes for r in recs),
@@ -335,13 +356,14 @@ def cpu_baseline_block(res: dict, threads: int | None = None) -> dict:
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS),
                     help="c2 = the headline workload (BASELINE.json configs[1]); c3/c4/c5 = "
                          "the other B200 configs of SURVEY.md §8d")
+    ap.add_argument("--dump-steps", default="", help="write per-step records (JSON) here")
     ap.add_argument("--prefill-budget", type=int, default=0,
                     help="b200.prefill_budget: cold prompt rows written per step (0 = all)")
     args = ap.parse_args()
@@ -388,7 +410,7 @@ def main():
         "step_phases_ms_mean": res["phases"],
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": 32},
-        "gpu_launches": 11 * args.steps,
+        "gpu_launches": res["step_kernels"] * args.steps,
         "roofline": {"bound": "hbm", "achieved": attn_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": attn_gbs / pk["hbm_gbs"], "traffic": None,
                      "kernel": res["variant"], "peak_src": pk["src"],

@@ -166,6 +166,8 @@ int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms_per_launch);
 int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms_per_launch);
 /* name of the attention kernel variant chosen for this geometry */
 const char *kvr_dev_attention_variant(kvr_dev *d);
+/* kernel nodes in the captured step graph (0 before the first graph launch) */
+int kvr_dev_step_kernels(kvr_dev *d, uint32_t *out);
 
 #ifdef __cplusplus
 }

@@ -43,6 +43,7 @@ struct kvr_dev {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     AttnPlan *attn = nullptr;
+    uint32_t graph_kernels = 0; // kernel nodes in the captured step graph
     uint64_t launched[2] = {0, 0};
     bool in_flight[2] = {false, false};
     uint64_t pending_write_tokens[2] = {0, 0};
@@ -325,6 +326,17 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
                 ck(cudaStreamBeginCapture(d->stream, cudaStreamCaptureModeThreadLocal), "capture");
                 run_step_kernels(d, c, true, int(k), true);
                 ck(cudaStreamEndCapture(d->stream, &graph), "capture end");
+                size_t n_nodes = 0;
+                ck(cudaGraphGetNodes(graph, nullptr, &n_nodes), "graph nodes");
+                std::vector<cudaGraphNode_t> nodes(n_nodes);
+                ck(cudaGraphGetNodes(graph, nodes.data(), &n_nodes), "graph nodes");
+                uint32_t kernels = 0;
+                for (cudaGraphNode_t nd : nodes) {
+                    cudaGraphNodeType ty;
+                    ck(cudaGraphNodeGetType(nd, &ty), "graph node type");
+                    kernels += ty == cudaGraphNodeTypeKernel;
+                }
+                d->graph_kernels = kernels;
                 ck(cudaGraphInstantiate(&d->graph[k], graph, 0), "graph instantiate");
                 cudaGraphDestroy(graph);
             }
@@ -468,5 +480,9 @@ int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms) { return time
 int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms) { return time_kernel(d, iters, ms, false); }
 
 const char *kvr_dev_attention_variant(kvr_dev *d) { return attn_variant(d->attn); }
+
+int kvr_dev_step_kernels(kvr_dev *d, uint32_t *out) {
+    return guard([&] { *out = d->graph_kernels; });
+}
 
 } // extern "C"

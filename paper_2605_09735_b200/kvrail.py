@@ -297,6 +297,7 @@ def _bind_extras(lib: C.CDLL) -> None:
         fn.restype = C.c_int
     lib.kvr_dev_attention_variant.argtypes = [vp]
     lib.kvr_dev_attention_variant.restype = C.c_char_p
+    lib.kvr_dev_step_kernels.argtypes = [vp, C.POINTER(C.c_uint32)]
     lib.kvr_dev_last_error.restype = C.c_char_p
 
 
@@ -594,6 +595,12 @@ class Device:
 
     def attention_variant(self) -> str:
         return native_lib().kvr_dev_attention_variant(self.raw()).decode()
+
+    def step_kernels(self) -> int:
+        """Kernel nodes in the captured step graph (launches per step)."""
+        n = C.c_uint32()
+        check(native_lib().kvr_dev_step_kernels(self.raw(), C.byref(n)))
+        return n.value
 
 
 # ---- scenario driver ------------------------------------------------------------
