@@ -153,33 +153,41 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
         cur = lo;
     }
     kvr_write_op op = ops[cur < n ? cur : 0];
+    // (token, slice) advance incrementally; per-token addresses are recomputed
+    // only when the token changes (no 64-bit division in the loop)
+    uint64_t j = u0 / slices;
+    uint32_t slice = uint32_t(u0 - j * slices);
+    uint64_t j_cached = ~0ull, tok = 0;
+    uint8_t *dst = nullptr, *ring = nullptr;
+    const uint64_t ring_layer = uint64_t(c.R) * c.row_elems * c.esz; // bytes between layers
+    const uint32_t q_base = threadIdx.x;
     for (uint64_t u = u0; u < u1; ++u) {
-        const uint64_t j = u / slices;
-        const uint32_t slice = uint32_t(u - j * slices);
-        while (cur + 1 < n && ops[cur + 1].prefix <= j)
-            op = ops[++cur];
-        if (op.source != 0)
-            continue;
-        const uint64_t k = j - op.prefix;
-        const uint64_t tok = op.token + k;
-        uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + (op.slot + k) * c.token_bytes;
-        uint8_t *ring = nullptr;
-        if (op.dev_slot != KVR_NO_SLOT) {
-            const uint64_t w = slots[op.dev_slot].written;
-            if (tok < w && tok + c.W >= w) // inside the live window after this step
-                ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
+        if (j != j_cached) {
+            j_cached = j;
+            while (cur + 1 < n && ops[cur + 1].prefix <= j)
+                op = ops[++cur];
+            const uint64_t k = j - op.prefix;
+            tok = op.token + k;
+            dst = c.arena + uint64_t(op.block) * c.page_bytes + (op.slot + k) * c.token_bytes;
+            ring = nullptr;
+            if (op.dev_slot != KVR_NO_SLOT) {
+                const uint64_t w = slots[op.dev_slot].written;
+                if (tok < w && tok + c.W >= w) // inside the live window after this step
+                    ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
+            }
         }
-        const uint64_t ring_layer = uint64_t(c.R) * c.row_elems * c.esz; // bytes between layers
-        {
-            const uint32_t q = slice * blockDim.x + threadIdx.x;
-            if (q >= chunks)
-                continue;
+        const uint32_t q = slice * blockDim.x + q_base;
+        if (op.source == 0 && q < chunks) {
             const int4 v = payload16(c, tab, op.session, tok, 16ull * q);
             *reinterpret_cast<int4 *>(dst + 16ull * q) = v;
             if (ring) {
                 const uint32_t l = q / row_chunks, within = q - l * row_chunks;
                 *reinterpret_cast<int4 *>(ring + l * ring_layer + 16ull * within) = v;
             }
+        }
+        if (++slice == slices) {
+            slice = 0;
+            ++j;
         }
     }
 }
@@ -197,8 +205,9 @@ __global__ void k_query(DevCtx c) {
         const uint64_t base = c.seed ^ (0x51ull << 56) ^ (uint64_t(slots[s].session) << 32) ^
                               (h->step << 20) ^ (uint64_t(l) << 12);
         float *q = c.q + uint64_t(sl) * per_layer;
+        const uint32_t hd_shift = __ffs(c.hd) - 1; // head_dim is a power of two (32/64/128)
         for (uint32_t i = threadIdx.x; i < per_layer; i += blockDim.x) {
-            const uint32_t head = i / c.hd, d = i - head * c.hd;
+            const uint32_t head = i >> hd_shift, d = i & (c.hd - 1);
             float v = lane_value(splitmix64(base ^ (uint64_t(head) << 8) ^ d));
             if (c.elem_kind == KVR_ELEM_F16)
                 v = __half2float(__float2half_rn(v));
@@ -375,7 +384,7 @@ void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold) {
     k_write<<<cold == 2 ? sms : sms * 8, 256, 0, s>>>(c, cold ? 1 : 0);
 }
 
-void launch_query(const DevCtx &c, cudaStream_t s, int sms) { k_query<<<sms * 2, 256, 0, s>>>(c); }
+void launch_query(const DevCtx &c, cudaStream_t s, int sms) { k_query<<<sms * 8, 256, 0, s>>>(c); }
 
 void launch_far(const DevCtx &c, cudaStream_t s, int sms) { k_far<<<sms * 2, 256, 0, s>>>(c); }
 void launch_map(const DevCtx &c, cudaStream_t s, int sms) { k_map<<<sms * 2, 256, 0, s>>>(c); }
