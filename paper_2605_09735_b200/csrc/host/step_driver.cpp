@@ -459,8 +459,15 @@ struct ScenarioDriver::Impl {
             r.span_first = r.reserved_end - nspan * tpp;
             if (dev)
                 dev->bind(r.id, slot);
-            for (uint64_t tok = start; tok < r.prompt; ++tok)
-                write_token(r.id, tok);
+            // The reference writes the prompt token by token (scenario.cpp:336-340);
+            // one range write makes the same coverage checks and COWs in the same
+            // block order (and the pager counts no writes), so the device path
+            // issues it at once.
+            if (dev && start < r.prompt)
+                pager->write_tokens_generated(r.id, {start, r.prompt});
+            else
+                for (uint64_t tok = start; tok < r.prompt; ++tok)
+                    write_token(r.id, tok);
             r.written = r.prompt;
             r.write_begin = start;
             r.admitted_now = true;
@@ -508,9 +515,13 @@ struct ScenarioDriver::Impl {
         if (!fv.enabled || r.local_step == 0)
             return;
         const uint64_t near_begin = r.written > fv.near_window ? r.written - fv.near_window : 0;
+        if (near_begin < r.summarized_until + fv.chunk_tokens)
+            return;
+        // The committed view cannot change inside this loop (reserve_range and the
+        // summary writes touch the shadow only), so it is read once.
+        const ViewDescriptor view = pager->active_view(r.id);
         while (near_begin >= r.summarized_until + fv.chunk_tokens) {
             const uint64_t lo = r.summarized_until, hi = lo + fv.chunk_tokens;
-            const ViewDescriptor view = pager->active_view(r.id);
             const uint32_t lanes = uint32_t(cfg.pager.token_bytes() / 4);
             double score = 0.0;
             std::vector<float> chunk;
