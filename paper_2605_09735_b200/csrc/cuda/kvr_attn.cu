@@ -412,7 +412,7 @@ struct AttnPlan {
     AttnFn fn = nullptr;
     const void *tc = nullptr; // tensor-core kernel (kvr_attn_tc.cu) when chosen
     CUtensorMap map{};
-    CUtensorMap far_map{}; // tensor-core kernel: far rows (gather4)
+    TcMaps tc_maps{};      // tensor-core kernel descriptors
     uint32_t G = 1, stages = 2, grid = 1;
     size_t smem = 0;
     char name[96] = {0};
@@ -422,7 +422,7 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
     auto *p = new AttnPlan();
     if (mode == 3 || (mode == 1 && c.group >= 4 && attn_tc_supported(c))) {
         p->tc = attn_tc_kernel(c);
-        if (!p->tc || !attn_tc_maps(c, &p->map, &p->far_map)) {
+        if (!p->tc || !attn_tc_maps(c, &p->tc_maps)) {
             delete p;
             return nullptr;
         }
@@ -485,7 +485,7 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
 
 void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s) {
     if (p->tc) {
-        launch_attn_tc(p->tc, c, p->map, p->far_map, p->grid, s);
+        launch_attn_tc(p->tc, c, p->tc_maps, p->grid, s);
         return;
     }
     p->fn<<<p->grid, 32 * (2 * kMaxG + 1), p->smem, s>>>(c, p->map, p->G, p->stages);

@@ -87,6 +87,13 @@ __device__ inline void tma_load_4d(uint32_t dst, const CUtensorMap *map, int c0,
                  "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(smem_u32(bar))
                  : "memory");
 }
+__device__ inline void tma_load_5d(uint32_t dst, const CUtensorMap *map, int c0, int c1, int c2, int c3, int c4,
+                                   uint64_t *bar) {
+    asm volatile("cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+                 " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+                 "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ inline void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ inline void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ inline void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
@@ -170,10 +177,24 @@ template <typename T, int G> __device__ inline void store_split(uint8_t *op, uin
         *reinterpret_cast<uint4 *>(row + 2048) = make_uint4(wd[4], wd[5], wd[6], wd[7]);
 }
 
-/// Tiles of one work item, identical for every role.
+/// Tiles of one work item, identical for every role. The near window [lo, w)
+/// is cut into 32-row boxes from L0 = lo rounded down to 32; full 4-box tiles
+/// come first, the remaining 1-3 newest boxes form a tail tile, and far summary
+/// rows are folded into that tail tile when they fit in front of its boxes
+/// (C5: 64 far rows + 1 box = one tile instead of two).
 struct Item {
-    uint32_t slot, layer, head, far_count, far_begin, n_far, n_near;
-    uint64_t lo, w, t0;
+    uint32_t slot, layer, head, far_count, far_begin;
+    uint32_t n_far;      // far-only tiles (far rows not folded)
+    uint32_t tail_boxes; // boxes of the tail tile (0 = no tail tile)
+    uint32_t fold_pos;   // first smem row of the tail boxes (far rows folded in front)
+    uint32_t n_tiles;
+    uint64_t lo, w, L0;
+};
+struct Tile {
+    uint32_t far_rows, far_off; // far list rows [far_off, +far_rows) -> smem rows [0, far_rows)
+    uint32_t box_first, n_boxes; // near boxes at smem rows [32 box_first, 32 (box_first + n_boxes))
+    uint32_t nk;                 // PV K steps (16 rows each) covering every used row
+    uint64_t tok_r0;             // token of smem row 0 for the near rows (mod 2^64)
 };
 __device__ inline bool item_of(const DevCtx &c, const kvr_slot_state *slots, uint32_t it, Item &I) {
     I.head = it % c.Hkv;
@@ -184,12 +205,47 @@ __device__ inline bool item_of(const DevCtx &c, const kvr_slot_state *slots, uin
         return false;
     I.w = st.written;
     I.lo = I.w > c.W ? I.w - c.W : 0;
-    I.t0 = I.lo & ~uint64_t(kSub - 1);
-    I.n_near = I.w > I.t0 ? uint32_t((I.w - I.t0 + kRows - 1) / kRows) : 0;
+    I.L0 = I.lo & ~uint64_t(kSub - 1);
+    const uint64_t E = (I.w + kSub - 1) & ~uint64_t(kSub - 1);
+    const uint32_t nbox = I.w > I.lo ? uint32_t((E - I.L0) / kSub) : 0;
+    I.tail_boxes = nbox & 3u;
     I.far_count = st.far_count;
     I.far_begin = st.far_begin;
-    I.n_far = (st.far_count + kRows - 1) / kRows;
+    const uint32_t P = (I.far_count + kSub - 1) & ~uint32_t(kSub - 1);
+    const bool fold = I.far_count > 0 && I.tail_boxes > 0 && P + kSub * I.tail_boxes <= uint32_t(kRows);
+    I.fold_pos = fold ? P : 0;
+    I.n_far = I.far_count > 0 && !fold ? (I.far_count + kRows - 1) / kRows : 0;
+    I.n_tiles = I.n_far + (I.tail_boxes > 0) + (nbox >> 2);
     return true;
+}
+__device__ inline Tile tile_of(const Item &I, uint32_t k) {
+    Tile tl;
+    if (k < I.n_far) {
+        tl.far_off = k * kRows;
+        tl.far_rows = min(uint32_t(kRows), I.far_count - tl.far_off);
+        tl.box_first = tl.n_boxes = 0;
+        tl.nk = (tl.far_rows + 15) / 16;
+        tl.tok_r0 = 0;
+        return tl;
+    }
+    k -= I.n_far;
+    const uint32_t n_full = I.n_tiles - I.n_far - (I.tail_boxes ? 1u : 0u);
+    if (k < n_full) { // full tiles from L0
+        tl.far_rows = tl.far_off = 0;
+        tl.box_first = 0;
+        tl.n_boxes = kRows / kSub;
+        tl.nk = kRows / 16;
+        tl.tok_r0 = I.L0 + uint64_t(kRows) * k;
+        return tl;
+    }
+    // tail tile: the last 1-3 boxes, with the far rows folded in front of them
+    tl.far_off = 0;
+    tl.far_rows = I.fold_pos ? I.far_count : 0;
+    tl.box_first = I.fold_pos / kSub;
+    tl.n_boxes = I.tail_boxes;
+    tl.nk = (I.fold_pos + kSub * I.tail_boxes) / 16;
+    tl.tok_r0 = I.L0 + uint64_t(kRows) * n_full - I.fold_pos;
+    return tl;
 }
 
 __device__ inline bool mbar_test(uint64_t *bar, uint32_t parity) {
@@ -227,7 +283,7 @@ struct Cursor {
     __device__ void init() { it = blockIdx.x, j = 0; }
     __device__ bool next(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items, uint32_t w, Item &I) {
         for (; it < n_items; it += gridDim.x) {
-            if (!item_of(c, slots, it, I) || I.n_far + I.n_near == 0)
+            if (!item_of(c, slots, it, I) || I.n_tiles == 0)
                 continue;
             if ((j++ & 1u) == w) {
                 it += gridDim.x;
@@ -266,11 +322,11 @@ struct Stream { // (no arrays indexed by w: everything stays in registers)
         turn = kInterleave ? w ^ 1u : w;
         if (w) {
             kk = k1, I = I1;
-            if (++k1 == I1.n_far + I1.n_near)
+            if (++k1 == I1.n_tiles)
                 h1 = c1.next(c, slots, n_items, 1, I1), k1 = 0, turn = 0;
         } else {
             kk = k0, I = I0;
-            if (++k0 == I0.n_far + I0.n_near)
+            if (++k0 == I0.n_tiles)
                 h0 = c0.next(c, slots, n_items, 0, I0), k0 = 0, turn = 1;
         }
         return true;
@@ -285,7 +341,7 @@ constexpr uint32_t kWgBytes = 3 * kOpBytes; // Q + P[2]
 
 template <typename T, int G>
 __global__ void __launch_bounds__(kThreads, 1)
-    k_attn_tc(DevCtx c, const __grid_constant__ CUtensorMap ring_map, const __grid_constant__ CUtensorMap far_map) {
+    k_attn_tc(DevCtx c, const __grid_constant__ TcMaps maps) {
     static_assert(2 * G <= kN, "hi/lo columns must fit N = 16");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -337,8 +393,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     if (warp == 0) { // ---------------- producer (whole warp; lanes issue the TMA ops of a tile) ----------------
         if (lane == 0) {
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
-            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&far_map)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.ring)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.tile)) : "memory");
+            asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.far)) : "memory");
         }
         Stream S;
         S.init(c, slots, n_items);
@@ -347,49 +404,52 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (S.next(c, slots, n_items, w, k, I)) {
             const int plane = int(I.slot * c.L + I.layer);
             if (k == 0)
-                row_base = uint32_t(I.t0 % c.R); // ring row of the first near tile
+                row_base = uint32_t(I.L0 % c.R); // ring row of the item's first box
+            const Tile tl = tile_of(I, k);
             mbar_wait(&empty[s], ph ^ 1);
             const uint32_t st = smem_u32(stages + s * kStageBytes);
-            if (k < I.n_far) {
-                // far summary rows: TMA gather4, 4 rows x 64 columns per op; op o = 4 * group + (kv, half)
-                const uint32_t r0 = k * kRows, nr = min(uint32_t(kRows), I.far_count - r0);
-                const uint32_t n4 = (nr + 3) / 4;
-                if (lane == 0)
-                    mbar_expect_tx(&full[s], n4 * 4 * 512);
-                __syncwarp();
+            // near boxes holding a live row: boxes start at or after L0 > lo - 32, so
+            // a box is live iff it starts below w
+            const uint64_t first_tok = tl.tok_r0 + uint64_t(kSub) * tl.box_first;
+            const uint32_t n_live =
+                first_tok < I.w ? min(tl.n_boxes, uint32_t((I.w - first_tok + kSub - 1) / kSub)) : 0u;
+            const uint32_t live_boxes = ((1u << n_live) - 1u) << tl.box_first;
+            const uint32_t n4 = (tl.far_rows + 3) / 4;
+            if (lane == 0)
+                mbar_expect_tx(&full[s], n4 * 4 * 512 + __popc(live_boxes) * 4 * kSub * 128);
+            __syncwarp();
+            if (tl.far_rows) { // far summary rows: TMA gather4, 4 rows x 64 columns; op o = 4 * group + (kv, half)
                 const int base = plane * int(c.max_chunks);
-                const uint32_t *ids = far_ids + I.far_begin + r0;
+                const uint32_t *ids = far_ids + I.far_begin + tl.far_off;
                 for (uint32_t o = lane; o < 4 * n4; o += 32) {
                     const uint32_t g4 = o >> 2, kv = (o >> 1) & 1u, hf = o & 1u;
                     int r[4];
 #pragma unroll
                     for (int x = 0; x < 4; ++x)
-                        r[x] = base + int(ids[min(4 * g4 + x, nr - 1)]);
-                    tma_gather4(st + (2 * kv + hf) * kHalfBytes + g4 * 512, &far_map,
+                        r[x] = base + int(ids[min(4 * g4 + x, tl.far_rows - 1)]);
+                    tma_gather4(st + (2 * kv + hf) * kHalfBytes + g4 * 512, &maps.far,
                                 int((kv ? c.Hkv + I.head : I.head) * kHd + hf * 64), r[0], r[1], r[2], r[3],
                                 &full[s]);
                 }
-            } else {
-                const uint32_t kn = k - I.n_far;
-                const uint64_t tb = I.t0 + uint64_t(kn) * kRows;
-                uint32_t live_boxes = 0;
-#pragma unroll
-                for (int bx = 0; bx < kRows / kSub; ++bx) {
-                    const uint64_t a0 = tb + bx * kSub;
-                    live_boxes |= uint32_t(a0 < I.w && a0 + kSub > I.lo) << bx;
-                }
+            }
+            uint32_t row0 = 0; // ring row of the first box (offsets within an item stay below R)
+            if (tl.n_boxes) {
+                row0 = row_base + uint32_t(first_tok - I.L0);
+                if (row0 >= c.R)
+                    row0 -= c.R;
+            }
+            if (live_boxes == 0xfu && row0 + kRows <= c.R) {
+                // whole tile in one op: 5-D view (64 dims, flat ring rows, half, head, K|V)
                 if (lane == 0)
-                    mbar_expect_tx(&full[s], __popc(live_boxes) * 4 * kSub * 128);
-                __syncwarp();
-                if (lane < 16) { // lane = box * 4 + (kv, half)
-                    const uint32_t bx = lane >> 2, kv = (lane >> 1) & 1u, hf = lane & 1u;
-                    if (live_boxes >> bx & 1u) {
-                        uint32_t row = row_base + kn * kRows + bx * kSub;
-                        while (row >= c.R)
-                            row -= c.R;
-                        tma_load_4d(st + (2 * kv + hf) * kHalfBytes + bx * kSub * 128, &ring_map, int(hf * 64),
-                                    int(kv ? c.Hkv + I.head : I.head), int(row), plane, &full[s]);
-                    }
+                    tma_load_5d(st, &maps.tile, 0, int(plane * c.R + row0), 0, int(I.head), 0, &full[s]);
+            } else if (lane < 16) { // lane = box * 4 + (kv, half), 32-row boxes never straddle the ring end
+                const uint32_t bx = lane >> 2, kv = (lane >> 1) & 1u, hf = lane & 1u;
+                if (live_boxes >> bx & 1u) {
+                    uint32_t row = row0 + (bx - tl.box_first) * kSub;
+                    if (row >= c.R)
+                        row -= c.R;
+                    tma_load_4d(st + (2 * kv + hf) * kHalfBytes + bx * kSub * 128, &maps.ring, int(hf * 64),
+                                int(kv ? c.Hkv + I.head : I.head), int(row), plane, &full[s]);
                 }
             }
             if (++s == kStages) {
@@ -431,8 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     __syncwarp();
                     if (k == 0)
                         (w ? mw1 : mw0) += 1;
-                    const uint32_t nk =
-                        k < I.n_far ? (min(uint32_t(kRows), I.far_count - k * kRows) + 15) / 16 : kRows / 16;
+                    const uint32_t nk = tile_of(I, k).nk;
                     const uint32_t sh = 8 * (nwc & 3u), e = (s | nk << 2) << sh;
                     if (w)
                         ring1 = (ring1 & ~(0xffu << sh)) | e;
@@ -487,7 +546,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (w == 0) // live slots with an empty window: zero output
             for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
                 Item I;
-                if (item_of(c, slots, it, I) && I.n_far + I.n_near == 0)
+                if (item_of(c, slots, it, I) && I.n_tiles == 0)
 #pragma unroll
                     for (int g = 0; g < G; ++g)
                         c.out[((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G + g) * kHd + t] =
@@ -531,15 +590,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 for (int g = 0; g < G; ++g)
                     acc[g] = acc[g] * alpha[g] + (ov[g] + ov[G + g]);
             };
-            for (uint32_t k = 0; k < I.n_far + I.n_near; ++k, ++n) {
+            for (uint32_t k = 0; k < I.n_tiles; ++k, ++n) {
                 const uint32_t b = n & 1u;
-                bool valid;
-                if (k < I.n_far) {
-                    valid = k * kRows + t < I.far_count;
-                } else {
-                    const uint64_t tok = I.t0 + uint64_t(k - I.n_far) * kRows + t;
-                    valid = tok >= I.lo && tok < I.w;
-                }
+                const Tile tl = tile_of(I, k);
+                const uint64_t tok = tl.tok_r0 + t;
+                const bool valid = t < tl.far_rows || (t >= kSub * tl.box_first &&
+                                                      t < kSub * (tl.box_first + tl.n_boxes) && tok >= I.lo && tok < I.w);
                 mbar_wait(&B.sfull[b], (n >> 1) & 1u);
                 tc_fence_after();
                 float sv[16];
@@ -619,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-using TcFn = void (*)(DevCtx, const CUtensorMap, const CUtensorMap);
+using TcFn = void (*)(DevCtx, const TcMaps);
 
 template <typename T> TcFn pick_tc(uint32_t g) {
     switch (g) {
@@ -664,30 +720,37 @@ const void *attn_tc_kernel(const DevCtx &c) {
 /// ring: 4-D view (head_dim, 2*Hkv heads, R rows, L*n_slots), 64 x 1 x 32 x 1
 /// boxes; far: 2-D view (row_elems, n_slots*L*max_chunks rows), 64 x 1 boxes
 /// for gather4. Both with the 128-byte swizzle the UMMA descriptors expect.
-bool attn_tc_maps(const DevCtx &c, CUtensorMap *ring, CUtensorMap *far) {
+bool attn_tc_maps(const DevCtx &c, TcMaps *maps) {
     const EncodeFn encode = encoder();
     if (!encode)
         return false;
     const uint64_t row = uint64_t(c.hd) * c.esz;
-    const cuuint64_t dims[4] = {c.hd, 2ull * c.Hkv, c.R, uint64_t(c.L) * c.n_slots};
-    const cuuint64_t strides[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
-    const cuuint32_t box[4] = {64, 1, uint32_t(kSub), 1};
-    const cuuint32_t estr[4] = {1, 1, 1, 1};
-    if (encode(ring, CU_TENSOR_MAP_DATA_TYPE_UINT16, 4, c.ring, dims, strides, box, estr,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-        return false;
-    const cuuint64_t fdims[2] = {c.row_elems, uint64_t(c.n_slots) * c.L * c.max_chunks};
-    const cuuint64_t fstrides[1] = {uint64_t(c.row_elems) * c.esz};
-    const cuuint32_t fbox[2] = {64, 1};
-    return encode(far, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, c.far, fdims, fstrides, fbox, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    const cuuint32_t estr[5] = {1, 1, 1, 1, 1};
+    auto enc = [&](CUtensorMap *m, uint32_t rank, void *base, const cuuint64_t *dims, const cuuint64_t *strides,
+                   const cuuint32_t *box) {
+        return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, rank, base, dims, strides, box, estr,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    };
+    // 32-row boxes: (head_dim, 2*Hkv heads, R rows, L*n_slots)
+    const cuuint64_t d4[4] = {c.hd, 2ull * c.Hkv, c.R, uint64_t(c.L) * c.n_slots};
+    const cuuint64_t s4[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
+    const cuuint32_t b4[4] = {64, 1, uint32_t(kSub), 1};
+    // whole tiles: (64 dims, flat rows = plane * R + row, half, head, K|V); the box
+    // lands as [K|V][half][128 rows][64 dims], exactly the stage layout
+    const cuuint64_t d5[5] = {64, uint64_t(c.L) * c.n_slots * c.R, 2, c.Hkv, 2};
+    const cuuint64_t s5[4] = {2ull * c.Hkv * row, 128, row, uint64_t(c.Hkv) * row};
+    const cuuint32_t b5[5] = {64, uint32_t(kRows), 2, 1, 2};
+    // far rows: (row_elems, n_slots*L*max_chunks rows), 64 x 1 boxes for gather4
+    const cuuint64_t df[2] = {c.row_elems, uint64_t(c.n_slots) * c.L * c.max_chunks};
+    const cuuint64_t sf[1] = {uint64_t(c.row_elems) * c.esz};
+    const cuuint32_t bf[2] = {64, 1};
+    return enc(&maps->ring, 4, c.ring, d4, s4, b4) && enc(&maps->tile, 5, c.ring, d5, s5, b5) &&
+           enc(&maps->far, 2, c.far, df, sf, bf);
 }
 
-void launch_attn_tc(const void *fn, const DevCtx &c, const CUtensorMap &ring, const CUtensorMap &far, uint32_t grid,
-                    cudaStream_t s) {
-    reinterpret_cast<TcFn>(const_cast<void *>(fn))<<<grid, kThreads, attn_tc_smem(), s>>>(c, ring, far);
+void launch_attn_tc(const void *fn, const DevCtx &c, const TcMaps &maps, uint32_t grid, cudaStream_t s) {
+    reinterpret_cast<TcFn>(const_cast<void *>(fn))<<<grid, kThreads, attn_tc_smem(), s>>>(c, maps);
 }
 
 } // namespace kvr

@@ -95,9 +95,13 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode);
 // tensor-core variant (kvr_attn_tc.cu)
 bool attn_tc_supported(const DevCtx &c);
 const void *attn_tc_kernel(const DevCtx &c);
-bool attn_tc_maps(const DevCtx &c, CUtensorMap *ring, CUtensorMap *far);
-void launch_attn_tc(const void *fn, const DevCtx &c, const CUtensorMap &ring, const CUtensorMap &far, uint32_t grid,
-                    cudaStream_t s);
+/// TMA descriptors of the tensor-core kernel: ring in 32-row boxes, ring in whole
+/// 128-row K|V tiles (one op per tile), far rows for gather4.
+struct TcMaps {
+    CUtensorMap ring, tile, far;
+};
+bool attn_tc_maps(const DevCtx &c, TcMaps *maps);
+void launch_attn_tc(const void *fn, const DevCtx &c, const TcMaps &maps, uint32_t grid, cudaStream_t s);
 void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s);
 void free_attn_plan(AttnPlan *p);
 const char *attn_variant(const AttnPlan *p);
