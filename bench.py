@@ -120,8 +120,26 @@ def c5_config(steps: int, rank: int = 0, world: int = 1) -> dict:
     }
 
 
-CONFIGS = {"c2": c2_config, "c3": c3_config, "c4": c4_config, "c5": c5_config}
+def c1_config(steps: int, rank: int = 0, world: int = 1) -> dict:
+    """C1 (configs[0], the reference's CPU-runnable case) as a B200 workload:
+    2 layers, 4 KV heads x 64, bf16 lanes, 16 concurrent requests."""
+    page = 32768
+    return {
+        "label": "c1-tiny", "seed": 1, "steps": steps, "warmup_steps": 0,
+        "pager": {"page_bytes": page, "layers": 2, "kv_head_dim": 256, "elem_bytes": 2},
+        "transport": {"tau_bytes": 8 * page, "delta_hold": 0.756, "merge": True},
+        "far_view": {"enabled": False, "w_star": 512},
+        "workload": workload(world, concurrency=16, prompt_min=64, prompt_max=512),
+        "shaping": {"arena_pages": 4096, "staged_refresh_period": 4},
+        "b200": {"kv_heads": 4, "head_dim": 64, "q_heads": 16, "payload": "lanes",
+                 "dtype": "bf16", "shard_rank": rank, "shard_world": world},
+    }
+
+
+CONFIGS = {"c1": c1_config, "c2": c2_config, "c3": c3_config, "c4": c4_config, "c5": c5_config}
 WORKLOADS = {
+    "c1": "C1 tiny (configs[0] shape): L=2, 4 KV heads x hd 64, 16 q heads, bf16, batch 16, "
+          "prompts 64-512",
     "c2": "C2 Llama-2-7B-shaped KV (configs[1]): L=32, 32 KV heads x hd 128, fp16, "
           "batch 64 per GPU, prompts 512-8192 (log-uniform) + decode, W*=512",
     "c3": "C3 Llama-3-8B-shaped GQA: L=32, 8 KV heads x hd 128, 32 q heads (g=4), bf16, "
@@ -202,15 +220,27 @@ class Clocks:
                 "reasons": sorted(self.reasons), "samples": len(self.sm), "source": "nvml"}
 
 
-def dist_setup():
+COLL_DEVICE = "cuda"  # where the per-step count tensors live ("cpu" with --backend gloo)
+
+
+def dist_setup(backend: str = "nccl"):
+    """One process per GPU (torchrun env). KVR_BENCH_DEVICE pins every rank to one
+    device — only for exercising the multi-rank path on a 1-GPU box with gloo."""
+    global COLL_DEVICE
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if "KVR_BENCH_DEVICE" in os.environ:
+        local = int(os.environ["KVR_BENCH_DEVICE"])
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            COLL_DEVICE = "cpu"
+            dist.init_process_group(backend)
     return rank, local, world
 
 
@@ -225,7 +255,7 @@ def reduce_max(vals: list[float], world: int) -> list[float]:
         return vals
     import torch
     import torch.distributed as dist
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    t = torch.tensor(vals, dtype=torch.float64, device=COLL_DEVICE)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()
 
@@ -235,7 +265,7 @@ def reduce_sum(vals: list[float], world: int) -> list[float]:
         return vals
     import torch
     import torch.distributed as dist
-    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    t = torch.tensor(vals, dtype=torch.float64, device=COLL_DEVICE)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return t.tolist()
 
@@ -266,7 +296,7 @@ def run_b200(args, rank, local, world) -> dict | None:
     if world > 1:  # per-step completion / EOS counts: the only cross-GPU traffic
         import torch
         import torch.distributed as dist
-        counts = torch.zeros(3, dtype=torch.int64, device="cuda")
+        counts = torch.zeros(3, dtype=torch.int64, device=COLL_DEVICE)
     lat_ms = []
     with Clocks(local) as clocks:
         t0 = time.perf_counter()
@@ -364,11 +394,13 @@ def main():
                     help="c2 = the headline workload (BASELINE.json configs[1]); c3/c4/c5 = "
                          "the other B200 configs of SURVEY.md §8d")
     ap.add_argument("--dump-steps", default="", help="write per-step records (JSON) here")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for the per-step counts (N > 1)")
     ap.add_argument("--prefill-budget", type=int, default=0,
                     help="b200.prefill_budget: cold prompt rows written per step (0 = all)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    rank, local, world = dist_setup()
+    rank, local, world = dist_setup(args.backend)
 
     if args.impl == "reference":
         if rank == 0:
