@@ -118,6 +118,7 @@ __device__ inline int4 payload16(const DevCtx &c, const LaneTable &tab, uint32_t
 
 // `cold`: 0 = the hot write ops (rows read later in this step), 1 = the cold ops
 // (older prompt rows; launched on a graph branch concurrent with K-attn).
+template <uint32_t kPer> // chunks per thread per unit (independent generator chains)
 __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
     __shared__ LaneTable tab;
     const kvr_step_header *h = hdr(c);
@@ -133,7 +134,7 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
     const uint32_t row_chunks = c.row_elems * c.esz / 16;
     // work unit = one blockDim-wide slice of 16-byte chunks of one token, so a
     // decode step's few tokens still spread over every SM
-    const uint32_t slices = (chunks + blockDim.x - 1) / blockDim.x;
+    const uint32_t slices = (chunks + kPer * blockDim.x - 1) / (kPer * blockDim.x);
     const uint64_t units = total * slices;
     // each CTA walks a contiguous run of units: one binary search, then the op
     // cursor only moves forward (ops are sorted by token prefix)
@@ -176,13 +177,23 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
                     ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
             }
         }
-        const uint32_t q = slice * blockDim.x + q_base;
-        if (op.source == 0 && q < chunks) {
-            const int4 v = payload16(c, tab, op.session, tok, 16ull * q);
-            *reinterpret_cast<int4 *>(dst + 16ull * q) = v;
-            if (ring) {
-                const uint32_t l = q / row_chunks, within = q - l * row_chunks;
-                *reinterpret_cast<int4 *>(ring + l * ring_layer + 16ull * within) = v;
+        if (op.source == 0) {
+            int4 v[kPer];
+#pragma unroll
+            for (uint32_t x = 0; x < kPer; ++x) {
+                const uint32_t q = (slice * kPer + x) * blockDim.x + q_base;
+                v[x] = q < chunks ? payload16(c, tab, op.session, tok, 16ull * q) : int4{};
+            }
+#pragma unroll
+            for (uint32_t x = 0; x < kPer; ++x) {
+                const uint32_t q = (slice * kPer + x) * blockDim.x + q_base;
+                if (q >= chunks)
+                    continue;
+                *reinterpret_cast<int4 *>(dst + 16ull * q) = v[x];
+                if (ring) {
+                    const uint32_t l = q / row_chunks, within = q - l * row_chunks;
+                    *reinterpret_cast<int4 *>(ring + l * ring_layer + 16ull * within) = v[x];
+                }
             }
         }
         if (++slice == slices) {
@@ -381,7 +392,12 @@ void launch_apply(const DevCtx &c, cudaStream_t s, int sms) {
 // cold: 0 hot writes (whole GPU), 1 cold writes (whole GPU, apply-only path),
 // 2 cold writes beside the attention (one CTA per SM)
 void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold) {
-    k_write<<<cold == 2 ? sms : sms * 8, 256, 0, s>>>(c, cold ? 1 : 0);
+    // hot writes (few decode tokens + window rows): one chunk per thread for
+    // spread; cold prompt rows: two chunks per thread for generator ILP
+    if (cold)
+        k_write<2><<<cold == 2 ? sms : sms * 8, 256, 0, s>>>(c, 1);
+    else
+        k_write<1><<<sms * 8, 256, 0, s>>>(c, 0);
 }
 
 void launch_query(const DevCtx &c, cudaStream_t s, int sms) { k_query<<<sms * 8, 256, 0, s>>>(c); }
