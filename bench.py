@@ -278,6 +278,8 @@ def run_b200(args, rank, local, world) -> dict | None:
     cfg = CONFIGS[args.config](fill_cap + args.warmup + args.steps, rank, world)
     if args.prefill_budget:
         cfg["b200"]["prefill_budget"] = args.prefill_budget
+    if args.attention_kernel != "auto":
+        cfg["b200"]["attention_kernel"] = args.attention_kernel
     d = pkg.Driver(cfg, device=local)
     width = cfg["workload"]["concurrency"]
     # fill the fixed-width batch (admissions write whole prompts), then warm up
@@ -394,6 +396,8 @@ def main():
                     help="c2 = the headline workload (BASELINE.json configs[1]); c3/c4/c5 = "
                          "the other B200 configs of SURVEY.md §8d")
     ap.add_argument("--dump-steps", default="", help="write per-step records (JSON) here")
+    ap.add_argument("--attention-kernel", default="auto", choices=["auto", "cuda_core", "tcgen05"],
+                    help="b200.attention_kernel (auto: tensor cores for GQA groups >= 4)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for the per-step counts (N > 1)")
     ap.add_argument("--prefill-budget", type=int, default=0,

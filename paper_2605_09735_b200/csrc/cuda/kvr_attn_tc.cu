@@ -679,6 +679,7 @@ using TcFn = void (*)(DevCtx, const TcMaps);
 
 template <typename T> TcFn pick_tc(uint32_t g) {
     switch (g) {
+    case 1: return k_attn_tc<T, 1>;
     case 2: return k_attn_tc<T, 2>;
     case 4: return k_attn_tc<T, 4>;
     case 8: return k_attn_tc<T, 8>;
@@ -699,7 +700,8 @@ EncodeFn encoder() {
 /// The tensor-core attention applies to head_dim 128, 16-bit elements and GQA
 /// groups of 2, 4 or 8 with at most 128 far rows per slot.
 bool attn_tc_supported(const DevCtx &c) {
-    return c.hd == kHd && c.esz == 2 && (c.group == 2 || c.group == 4 || c.group == 8) && c.far_cap <= kRows &&
+    return c.hd == kHd && c.esz == 2 && (c.group == 1 || c.group == 2 || c.group == 4 || c.group == 8) &&
+           c.far_cap <= kRows &&
            c.R % kSub == 0;
 }
 

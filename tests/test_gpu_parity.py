@@ -111,7 +111,8 @@ def test_window_and_attention_lanes_payload(dtype, kvh, hd, qh):
 
 @pytest.mark.parametrize("dtype,kvh,qh,w_star", [("bf16", 2, 8, 96), ("bf16", 2, 8, 512),
                                                  ("fp16", 2, 8, 512), ("bf16", 2, 16, 512),
-                                                 ("bf16", 2, 4, 300), ("fp16", 1, 8, 200)])
+                                                 ("bf16", 2, 4, 300), ("fp16", 1, 8, 200),
+                                                 ("fp16", 2, 2, 512), ("bf16", 4, 4, 160)])
 def test_tcgen05_gqa_attention(dtype, kvh, qh, w_star):
     """The tensor-core GQA kernel (tcgen05 S = K.Q^T and O = V^T.P, TMEM
     accumulators) against the double-precision oracle, window tiles of every
