@@ -333,13 +333,14 @@ def run_b200(args, rank, local, world) -> dict | None:
     dev = d.device()
     variant = dev.attention_variant()
     step_kernels = dev.step_kernels()
+    captures = dev.graph_captures()
     dev_s_max, wall_s_max = reduce_max([dev_s, wall_s], world)
     tokens_all, gather_bytes_all = reduce_sum([float(tokens), float(gather_bytes)], world)
     out = {
         "rank": rank, "cfg": cfg, "recs": recs, "dev_s": dev_s_max, "wall_s": wall_s_max,
         "tokens": tokens_all, "attn_bytes": attn_bytes, "attn_s": attn_s,
         "gather_bytes": gather_bytes, "gather_s": gather_s, "gather_bytes_all": gather_bytes_all,
-        "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "clocks": clocks.summary(), "fill_steps": fill,
+        "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "captures": captures, "clocks": clocks.summary(), "fill_steps": fill,
         "live_mean": statistics.mean(r.live_sessions for r in recs),
         "trains_mean": statistics.mean(r.trains for r in recs),
         "dma_mean": statistics.mean(r.dma_bytes for r in recs),
@@ -447,6 +448,8 @@ def main():
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],
                 "d2h_bytes_per_step": 32},
         "gpu_launches": res["step_kernels"] * args.steps,
+        "graph": {"kernels_per_step": res["step_kernels"], "captures": res["captures"],
+                  "note": "one CUDA graph per descriptor ring slot, captured once, replayed every step"},
         "roofline": {"bound": "hbm", "achieved": attn_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
                      "frac": attn_gbs / pk["hbm_gbs"], "traffic": None,
                      "kernel": res["variant"], "peak_src": pk["src"],

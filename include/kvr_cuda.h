@@ -168,6 +168,9 @@ int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms_per_launch);
 const char *kvr_dev_attention_variant(kvr_dev *d);
 /* kernel nodes in the captured step graph (0 before the first graph launch) */
 int kvr_dev_step_kernels(kvr_dev *d, uint32_t *out);
+/* step graphs captured so far: 2 (one per descriptor ring slot) after the first two
+   steps and never more — the fixed shape means no recapture (sim_engine.cpp:33-72 audit) */
+int kvr_dev_graph_captures(kvr_dev *d, uint32_t *out);
 
 #ifdef __cplusplus
 }

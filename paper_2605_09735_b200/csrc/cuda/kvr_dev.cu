@@ -44,6 +44,7 @@ struct kvr_dev {
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     AttnPlan *attn = nullptr;
     uint32_t graph_kernels = 0; // kernel nodes in the captured step graph
+    uint32_t graph_captures = 0; // step graphs captured (one per descriptor ring slot, never again)
     uint64_t launched[2] = {0, 0};
     bool in_flight[2] = {false, false};
     uint64_t pending_write_tokens[2] = {0, 0};
@@ -337,6 +338,7 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
                     kernels += ty == cudaGraphNodeTypeKernel;
                 }
                 d->graph_kernels = kernels;
+                ++d->graph_captures;
                 ck(cudaGraphInstantiate(&d->graph[k], graph, 0), "graph instantiate");
                 cudaGraphDestroy(graph);
             }
@@ -483,6 +485,10 @@ const char *kvr_dev_attention_variant(kvr_dev *d) { return attn_variant(d->attn)
 
 int kvr_dev_step_kernels(kvr_dev *d, uint32_t *out) {
     return guard([&] { *out = d->graph_kernels; });
+}
+
+int kvr_dev_graph_captures(kvr_dev *d, uint32_t *out) {
+    return guard([&] { *out = d->graph_captures; });
 }
 
 } // extern "C"

@@ -298,6 +298,7 @@ def _bind_extras(lib: C.CDLL) -> None:
     lib.kvr_dev_attention_variant.argtypes = [vp]
     lib.kvr_dev_attention_variant.restype = C.c_char_p
     lib.kvr_dev_step_kernels.argtypes = [vp, C.POINTER(C.c_uint32)]
+    lib.kvr_dev_graph_captures.argtypes = [vp, C.POINTER(C.c_uint32)]
     lib.kvr_dev_last_error.restype = C.c_char_p
 
 
@@ -600,6 +601,12 @@ class Device:
         """Kernel nodes in the captured step graph (launches per step)."""
         n = C.c_uint32()
         check(native_lib().kvr_dev_step_kernels(self.raw(), C.byref(n)))
+        return n.value
+
+    def graph_captures(self) -> int:
+        """Step graphs captured so far (2 after warm-up, never more)."""
+        n = C.c_uint32()
+        check(native_lib().kvr_dev_graph_captures(self.raw(), C.byref(n)))
         return n.value
 
 

@@ -53,6 +53,8 @@ def test_c1_reference_bytes_on_device():
     assert d.trace() == read("c1_trace.txt")
     assert d.steps_csv() == read("c1_steps.csv")
     assert_scan_exact(d, 64)
+    # fixed shape: the two step graphs (one per descriptor ring slot) are never recaptured
+    assert d.device().graph_captures() == 2
 
 
 @pytest.mark.parametrize("name", ["audit", "adv_burst"])
