@@ -205,7 +205,17 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
 
 // Decode queries for live slots: [slot][L][Hq][hd], rounded to the KV element
 // type (kvo_fill_query in the oracle). One CTA per (slot, layer).
-__global__ void k_query(DevCtx c) {
+__global__ void __launch_bounds__(256) k_query(DevCtx c) {
+    __shared__ float val[2001]; // ((k - 1000) / 1000) rounded to the KV type, k = h % 2001
+    for (uint32_t i = threadIdx.x; i < 2001; i += blockDim.x) {
+        float v = float(int(i) - 1000) / 1000.0f;
+        if (c.elem_kind == KVR_ELEM_F16)
+            v = __half2float(__float2half_rn(v));
+        else if (c.elem_kind == KVR_ELEM_BF16)
+            v = __bfloat162float(__float2bfloat16_rn(v));
+        val[i] = v;
+    }
+    __syncthreads();
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
     const uint32_t per_layer = c.Hq * c.hd;
@@ -219,12 +229,7 @@ __global__ void k_query(DevCtx c) {
         const uint32_t hd_shift = __ffs(c.hd) - 1; // head_dim is a power of two (32/64/128)
         for (uint32_t i = threadIdx.x; i < per_layer; i += blockDim.x) {
             const uint32_t head = i >> hd_shift, d = i & (c.hd - 1);
-            float v = lane_value(splitmix64(base ^ (uint64_t(head) << 8) ^ d));
-            if (c.elem_kind == KVR_ELEM_F16)
-                v = __half2float(__float2half_rn(v));
-            else if (c.elem_kind == KVR_ELEM_BF16)
-                v = __bfloat162float(__float2bfloat16_rn(v));
-            q[i] = v;
+            q[i] = val[splitmix64(base ^ (uint64_t(head) << 8) ^ d) % 2001ull];
         }
     }
 }

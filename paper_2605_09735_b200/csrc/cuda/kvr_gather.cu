@@ -18,8 +18,8 @@ namespace kvr {
 namespace {
 
 constexpr int kStages = 8;  // stage buffers per CTA
-constexpr int kAhead = 4;   // loads in flight ahead of the stores
-constexpr uint32_t kMaxPiece = 16384; // rows larger than this move in pieces
+constexpr int kAhead = 6;   // loads in flight ahead of the stores
+constexpr uint32_t kMaxPiece = 8192; // rows larger than this move in pieces (3 CTAs per SM)
 
 __device__ inline uint32_t smem_u32(const void *p) {
     return uint32_t(__cvta_generic_to_shared(p));
@@ -66,53 +66,73 @@ struct Move {
     uint32_t bytes;
 };
 
-__device__ inline Move resolve(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_spans,
-                               uint64_t unit, uint32_t pieces, uint32_t piece_bytes) {
-    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
-    const uint32_t piece = uint32_t(unit % pieces);
-    const uint64_t row_unit = unit / pieces;
-    const uint32_t l = uint32_t(row_unit % c.L);
-    const uint64_t tok_idx = row_unit / c.L;
-    uint32_t lo = 0, hi = n_spans; // last span with tok_prefix <= tok_idx
-    while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) / 2;
-        if (c.gspans[mid].tok_prefix <= tok_idx)
-            lo = mid;
-        else
-            hi = mid;
+/// Walks this CTA's contiguous range of units (token, layer, piece) with a
+/// forward-moving span cursor: no division or search per unit.
+struct Walker {
+    uint64_t tok_idx;
+    uint32_t l, piece, cur;
+    __device__ void init(const DevCtx &c, uint32_t n_spans, uint64_t u0, uint32_t pieces) {
+        piece = uint32_t(u0 % pieces);
+        const uint64_t row_unit = u0 / pieces;
+        l = uint32_t(row_unit % c.L);
+        tok_idx = row_unit / c.L;
+        uint32_t lo = 0, hi = n_spans; // last span with tok_prefix <= tok_idx
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (c.gspans[mid].tok_prefix <= tok_idx)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        cur = lo;
     }
-    const GSpan sp = c.gspans[lo];
-    const uint64_t k = tok_idx - sp.tok_prefix;
-    Move m{nullptr, nullptr, 0};
-    if (sp.dev_slot >= c.n_slots)
+    __device__ void advance(const DevCtx &c, uint32_t n_spans, uint32_t pieces) {
+        if (++piece < pieces)
+            return;
+        piece = 0;
+        if (++l < c.L)
+            return;
+        l = 0;
+        ++tok_idx;
+        while (cur + 1 < n_spans && c.gspans[cur + 1].tok_prefix <= tok_idx)
+            ++cur;
+    }
+    __device__ Move resolve(const DevCtx &c, const kvr_slot_state *slots, uint32_t piece_bytes) const {
+        const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+        const GSpan sp = c.gspans[cur];
+        const uint64_t k = tok_idx - sp.tok_prefix;
+        Move m{nullptr, nullptr, 0};
+        if (sp.dev_slot >= c.n_slots)
+            return m;
+        const uint64_t off0 = uint64_t(piece) * piece_bytes;
+        const uint32_t bytes = uint32_t(row_bytes - off0 < piece_bytes ? row_bytes - off0 : piece_bytes);
+        m.src = c.arena + uint64_t(sp.block) * c.page_bytes + (sp.slot_begin + k) * c.token_bytes +
+                l * row_bytes + off0;
+        const uint64_t tok = sp.first_token + k;
+        if (sp.kind == 0) {
+            const uint64_t w = slots[sp.dev_slot].written;
+            const uint64_t lo_tok = w > c.W ? w - c.W : 0; // rows of [lo_tok, lo_tok + R) are live
+            if (tok < lo_tok || tok >= lo_tok + c.R)
+                return m;
+            m.dst = c.ring + (ring_row(c, sp.dev_slot, l, uint32_t(tok % c.R)) * c.esz) + off0;
+        } else {
+            if (tok < KVR_SUMMARY_BASE)
+                return m;
+            const uint64_t chunk = tok - KVR_SUMMARY_BASE;
+            if (chunk >= c.max_chunks)
+                return m;
+            m.dst = c.far + ((uint64_t(sp.dev_slot) * c.L + l) * c.max_chunks + chunk) * c.row_elems * c.esz +
+                    off0;
+        }
+        m.bytes = bytes;
         return m;
-    const uint64_t off0 = uint64_t(piece) * piece_bytes;
-    const uint32_t bytes = uint32_t(row_bytes - off0 < piece_bytes ? row_bytes - off0 : piece_bytes);
-    m.src = c.arena + uint64_t(sp.block) * c.page_bytes + (sp.slot_begin + k) * c.token_bytes +
-            l * row_bytes + off0;
-    const uint64_t tok = sp.first_token + k;
-    if (sp.kind == 0) {
-        const uint64_t w = slots[sp.dev_slot].written;
-        const uint64_t lo_tok = w > c.W ? w - c.W : 0; // rows of [lo_tok, lo_tok + R) are live
-        if (tok < lo_tok || tok >= lo_tok + c.R)
-            return m;
-        m.dst = c.ring + (ring_row(c, sp.dev_slot, l, uint32_t(tok % c.R)) * c.esz) + off0;
-    } else {
-        if (tok < KVR_SUMMARY_BASE)
-            return m;
-        const uint64_t chunk = tok - KVR_SUMMARY_BASE;
-        if (chunk >= c.max_chunks)
-            return m;
-        m.dst = c.far + ((uint64_t(sp.dev_slot) * c.L + l) * c.max_chunks + chunk) * c.row_elems * c.esz + off0;
     }
-    m.bytes = bytes;
-    return m;
-}
+};
 
-// One warp per CTA; lane 0 drives a kStages-deep ring: loads run kAhead units
-// in front of the stores, and a buffer is refilled only after the store that
-// last read it has drained (bulk_group read wait with kStages-kAhead-1 groups
-// still allowed in flight).
+// One warp per CTA; lane 0 drives a kStages-deep ring over the CTA's contiguous
+// unit range: loads run kAhead units in front of the stores, and a buffer is
+// refilled only after the store that last read it has drained (bulk_group read
+// wait with kStages-kAhead-1 groups still allowed in flight).
 __global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
     extern __shared__ __align__(128) uint8_t stage[];
     __shared__ __align__(8) uint64_t full[kStages];
@@ -124,16 +144,23 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
     const uint64_t units = c.scan->total_tokens * c.L * pieces;
     if (units == 0 || (c.scan->status & 4u) || threadIdx.x != 0)
         return;
+    const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
+    const uint64_t u0 = blockIdx.x * per, u1 = units < u0 + per ? units : u0 + per;
+    if (u0 >= u1)
+        return;
     for (int s = 0; s < kStages; ++s)
         mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    Walker wk;
+    wk.init(c, n_spans, u0, pieces);
+    uint64_t next = u0;
     Move mv[kStages];
     uint32_t phase_bits = 0;
-    uint64_t next = blockIdx.x;
     auto issue = [&](int s) {
-        while (next < units) {
-            const Move m = resolve(c, slots, n_spans, next, pieces, piece_bytes);
-            next += gridDim.x;
+        while (next < u1) {
+            const Move m = wk.resolve(c, slots, piece_bytes);
+            ++next;
+            wk.advance(c, n_spans, pieces);
             if (m.bytes) {
                 mv[s] = m;
                 mbar_expect_tx(&full[s], m.bytes);
