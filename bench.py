@@ -466,35 +466,39 @@ def main():
 
 
 def reference_arm(args, world) -> dict:
-    """The reference's CPU implementation of the step (oracle/_ref), same workload."""
+    """The reference's CPU implementation of the step (oracle/_ref) on the same
+    workload: run_scenario control plane (shrunk geometry, identical decisions),
+    memcpy of the staged bytes it schedules, and build_view + attend per
+    (session, layer, q-head) on all host threads — a sample per step,
+    extrapolated to the full batch."""
     from oracle import cpu_baseline as cb
-    cfg = c2_config(400, 0, 1)
+    cfg = CONFIGS[args.config](400, 0, 1)
     b = cfg["b200"]
-    live = cfg["workload"]["concurrency"]
-    per_step = []
-    ctl = cb.control_plane_seconds_per_step(cfg)
+    ctl = cb.control_plane(cfg)
+    live = round(ctl["live_mean"])
     gbs = cb.memcpy_gbs()
-    dma = 2 * 8 * 9 * MIB  # two merged trains of one 9-page span, as the B200 run measures
     threads = os.cpu_count() or 1
+    window = cfg["far_view"]["w_star"] + (cfg["far_view"].get("cap", 0) if cfg["far_view"].get("enabled") else 0)
     calls = live * cfg["pager"]["layers"] * b["q_heads"]
     sample = min(calls, 512 * threads)
+    per_step = []
     for i in range(args.warmup + args.steps):
-        t_attn = cb.attention_seconds(b["head_dim"], cfg["far_view"]["w_star"], sample,
-                                      threads) * calls / sample
+        t_attn = cb.attention_seconds(b["head_dim"], window, sample, threads) * calls / sample
         if i >= args.warmup:
-            per_step.append(ctl + t_attn + 2.0 * dma / (gbs * 1e9))
+            per_step.append(ctl["seconds_per_step"] + t_attn + 2.0 * ctl["dma_bytes_per_step"] / (gbs * 1e9))
     total = sum(per_step)
     value = live * len(per_step) / total
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total / len(per_step) * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64 (reference attend)",
-            "data": "synthetic", "config": {"workload": "C2 (same as the b200 arm)"},
+            "data": "synthetic", "config": {"workload": WORKLOADS[args.config] + " (same as the b200 arm)"},
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
                              "kind": "reference",
                              "sample": f"per timed step {sample} of the {calls} reference "
-                                       "build_view+attend calls of a C2 step (extrapolated), all "
-                                       "threads, + run_scenario control plane + memcpy"},
+                                       f"build_view+attend calls of a {cfg['label']} step "
+                                       "(extrapolated), all threads, + run_scenario control plane "
+                                       "(shrunk geometry) + memcpy of its staged bytes"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 

@@ -31,6 +31,13 @@ def _lib():
 
 
 def control_plane_seconds_per_step(config: dict, steps: int = 200) -> float:
+    return control_plane(config, steps)["seconds_per_step"]
+
+
+def control_plane(config: dict, steps: int = 200) -> dict:
+    """run_scenario of the reference on the shrunk geometry: wall seconds per step,
+    plus the staged (DMA) bytes per step scaled back to the real geometry and
+    the mean live batch, both from the reference's own steps.csv."""
     cfg = copy.deepcopy(config)
     cfg.pop("b200", None)
     p = cfg.setdefault("pager", {})
@@ -48,8 +55,13 @@ def control_plane_seconds_per_step(config: dict, steps: int = 200) -> float:
     t["tau_bytes"] = int(t.get("tau_bytes", 131072) // scale)
     cfg["steps"] = steps
     cfg["warmup_steps"] = 0
-    _, _, _, wall = ob.ref_scenario(cfg, trace=False)
-    return wall / steps
+    csv, _, _, wall = ob.ref_scenario(cfg, trace=False)
+    rows = [r.split(",") for r in csv.strip().split("\n")]
+    col = {name: i for i, name in enumerate(rows[0])}
+    body = rows[1 + steps // 2:]  # second half: the batch has filled
+    dma = sum(float(r[col["dma_bytes"]]) for r in body) / max(1, len(body)) * scale
+    live = sum(float(r[col["live_sessions"]]) for r in body) / max(1, len(body))
+    return {"seconds_per_step": wall / steps, "dma_bytes_per_step": dma, "live_mean": live}
 
 
 def attention_seconds(head_dim: int, window: int, calls: int, threads: int) -> float:
