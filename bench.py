@@ -273,8 +273,8 @@ def reduce_sum(vals: list[float], world: int) -> list[float]:
 def run_b200(args, rank, local, world) -> dict | None:
     import paper_2605_09735_b200 as pkg
 
-    latency = args.config == "c4"  # burst replay: per-step latency from step 0
-    fill_cap = 0 if latency else 400
+    latency = args.sync_steps  # synchronise every step: wall latency incl. host work
+    fill_cap = 0 if args.config == "c4" else 400  # burst replay runs from step 0
     cfg = CONFIGS[args.config](fill_cap + args.warmup + args.steps, rank, world)
     if args.prefill_budget:
         cfg["b200"]["prefill_budget"] = args.prefill_budget
@@ -315,11 +315,14 @@ def run_b200(args, rank, local, world) -> dict | None:
         t1 = time.perf_counter()
     barrier(world)
     recs = [d.record(s) for s in range(first, first + args.steps)]
+    # inter-token latency: successive step-end %globaltimer stamps (pipelined steps)
+    itl_ms = [(recs[i].end_ns - recs[i - 1].end_ns) / 1e6 for i in range(1, len(recs))]
     if args.dump_steps and rank == 0:  # per-step records for latency analysis
         with open(args.dump_steps, "w") as f:
             json.dump([{"step": r.step, "live": r.live_sessions, "emitted": r.emitted_tokens,
                         "trains": r.trains, "dma": r.dma_bytes, "device_ms": r.device_ms,
                         "wall_ms": lat_ms[i] if i < len(lat_ms) else None,
+                        "itl_ms": itl_ms[i - 1] if i > 0 else None,
                         "writeback_tokens": r.writeback_tokens, "h2d": r.h2d_bytes,
                         "phases": list(r.phase_ms)[:7]} for i, r in enumerate(recs)], f)
     dev_s = sum(r.device_ms for r in recs) / 1e3
@@ -350,6 +353,8 @@ def run_b200(args, rank, local, world) -> dict | None:
              "cold_write_tail"])},
         "p50_ms": nearest_rank([r.device_ms for r in recs], 0.50),
         "p99_ms": nearest_rank([r.device_ms for r in recs], 0.99),
+        "itl_p50_ms": nearest_rank(itl_ms, 0.50) if itl_ms else None,
+        "itl_p99_ms": nearest_rank(itl_ms, 0.99) if itl_ms else None,
         "wall_p50_ms": nearest_rank(lat_ms, 0.50) if lat_ms else None,
         "wall_p99_ms": nearest_rank(lat_ms, 0.99) if lat_ms else None,
         "latency_steps": len(lat_ms), "first_step": first,
@@ -397,6 +402,8 @@ def main():
                     help="c2 = the headline workload (BASELINE.json configs[1]); c3/c4/c5 = "
                          "the other B200 configs of SURVEY.md §8d")
     ap.add_argument("--dump-steps", default="", help="write per-step records (JSON) here")
+    ap.add_argument("--sync-steps", action="store_true",
+                    help="synchronise after every step and report host+device wall latency")
     ap.add_argument("--attention-kernel", default="auto", choices=["auto", "cuda_core", "tcgen05"],
                     help="b200.attention_kernel (auto: tensor cores for GQA groups >= 4)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
@@ -442,6 +449,9 @@ def main():
         "transport": {"trains_per_step": res["trains_mean"], "mean_train_bytes":
                       res["mean_train_bytes"], "live_mean": res["live_mean"]},
         "step_latency_ms": {"p50": res["p50_ms"], "p99": res["p99_ms"], "clock": "device",
+                            "itl_p50": res["itl_p50_ms"], "itl_p99": res["itl_p99_ms"],
+                            "itl_note": "inter-token latency: differences of the step-end "
+                                        "%globaltimer stamps, steps pipelined as served",
                             "wall_p50": res["wall_p50_ms"], "wall_p99": res["wall_p99_ms"],
                             "max_step": res["max_step"]},
         "step_phases_ms_mean": res["phases"],

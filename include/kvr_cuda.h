@@ -128,6 +128,7 @@ typedef struct kvr_step_stats {
     uint64_t staged_tokens;
     uint64_t writeback_tokens;
     uint64_t attn_bytes;
+    uint64_t end_ns;          /* device %globaltimer at the end of the step */
 } kvr_step_stats;
 
 typedef struct kvr_dev kvr_dev;

@@ -45,6 +45,7 @@ struct DeviceStepStats {
     uint64_t attn_bytes = 0;    // KV bytes the attention read
     uint64_t h2d_bytes = 0;     // committed descriptor bytes published this step
     uint32_t scan_status = 0;   // 0 ok; else capacity overflow flags
+    uint64_t end_ns = 0;        // device %globaltimer at the end of the step
 };
 
 class DeviceStep {

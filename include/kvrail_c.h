@@ -203,6 +203,8 @@ typedef struct kvr_step_record { /* StepRecord, sim_engine.hpp:47-63 + measured 
     uint64_t gather_bytes;     /* bytes the gather moved (read side) */
     uint64_t attn_bytes;       /* KV bytes the window attention read */
     uint64_t h2d_bytes;        /* committed step descriptor bytes copied host -> device */
+    uint64_t end_ns;           /* device %globaltimer at the end of the step: successive
+                                  differences are the inter-token latency */
 } kvr_step_record;
 
 /* ---- Pager (pager.hpp:121-183) ------------------------------------------ */

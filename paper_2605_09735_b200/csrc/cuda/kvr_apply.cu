@@ -407,6 +407,13 @@ void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold) {
 
 void launch_query(const DevCtx &c, cudaStream_t s, int sms) { k_query<<<sms * 8, 256, 0, s>>>(c); }
 
+__global__ void k_stamp(DevCtx c) {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    c.scan->end_ns = t;
+}
+void launch_stamp(const DevCtx &c, cudaStream_t s) { k_stamp<<<1, 1, 0, s>>>(c); }
+
 void launch_far(const DevCtx &c, cudaStream_t s, int sms) { k_far<<<sms * 2, 256, 0, s>>>(c); }
 void launch_map(const DevCtx &c, cudaStream_t s, int sms) { k_map<<<sms * 2, 256, 0, s>>>(c); }
 void launch_prime(const DevCtx &c, cudaStream_t s, int sms) { k_prime<<<sms * 4, 256, 0, s>>>(c); }

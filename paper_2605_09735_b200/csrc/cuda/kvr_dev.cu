@@ -130,6 +130,7 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     // (one CTA per SM on a forked branch) slowed the attention by more than the
     // overlap saved, so the step runs them after it with the whole GPU.
     launch_write(c, s, d->sms, 1);
+    launch_stamp(c, s);
     mark(7);
 }
 
@@ -396,6 +397,7 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
         out->spans = sc.spans;
         out->status = sc.status;
         out->train_bytes = sc.train_bytes;
+        out->end_ns = sc.end_ns;
         out->staged_tokens = sc.total_tokens;
         out->writeback_tokens = d->pending_write_tokens[k];
         d->in_flight[k] = false;

@@ -28,6 +28,7 @@ struct ScanCounters {
     uint32_t trains, descriptors, spans, status;
     uint64_t total_tokens;
     uint64_t train_bytes;
+    uint64_t end_ns; // %globaltimer when the step's last kernel ran (inter-token latency)
 };
 
 /// Everything a kernel needs: geometry + device buffers. Passed by value.
@@ -83,7 +84,8 @@ __device__ inline uint64_t ring_row(const DevCtx &c, uint32_t slot, uint32_t l, 
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blob
 void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold); // generated payloads
 void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
-void launch_far(const DevCtx &c, cudaStream_t s, int sms);     // far summaries
+void launch_far(const DevCtx &c, cudaStream_t s, int sms);
+void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp     // far summaries
 void launch_map(const DevCtx &c, cudaStream_t s, int sms);     // page-table edits
 void launch_prime(const DevCtx &c, cudaStream_t s, int sms);   // window priming
 void launch_scan(const DevCtx &c, cudaStream_t s);             // stage + reduce

@@ -377,6 +377,7 @@ static void fill_record(const StepRecord &r, kvr_step_record *o) {
         o->gather_bytes = r.gather_bytes;
         o->attn_bytes = r.attn_bytes;
         o->h2d_bytes = r.h2d_bytes;
+        o->end_ns = r.end_ns;
 }
 
 int kvr_driver_step(kvr_driver *d, kvr_step_record *o) {

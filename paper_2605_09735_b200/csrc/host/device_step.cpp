@@ -527,6 +527,7 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
         d.scan_status = st.status;
         d.attn_bytes = m.attn_bytes_pending[k];
         d.h2d_bytes = m.desc_bytes_pending[k];
+        d.end_ns = st.end_ns;
         m.have_done[k] = true;
     }
     uint64_t attn = 0;
@@ -575,6 +576,7 @@ DeviceStepStats DeviceStep::collect(uint64_t step) {
         d.scan_status = st.status;
         d.attn_bytes = m.attn_bytes_pending[k];
         d.h2d_bytes = m.desc_bytes_pending[k];
+        d.end_ns = st.end_ns;
         m.have_done[k] = true;
     }
     return m.done[k];

@@ -39,6 +39,19 @@ uint64_t mix64(uint64_t x) { // splitmix64 finaliser (scenario.cpp:34-39)
 }
 
 constexpr uint64_t kSummaryTok = 1ull << 40; // summary slots live outside token space
+
+/// The measured device part of a step record.
+void fill_device(StepRecord &r, const DeviceStepStats &ds) {
+    r.device_ms = ds.device_ms;
+    r.gather_ms = ds.gather_ms;
+    r.attn_ms = ds.attn_ms;
+    std::copy(ds.phase_ms, ds.phase_ms + 8, r.phase_ms);
+    r.writeback_tokens = ds.writeback_tokens;
+    r.gather_bytes = ds.train_bytes;
+    r.attn_bytes = ds.attn_bytes;
+    r.h2d_bytes = ds.h2d_bytes;
+    r.end_ns = ds.end_ns;
+}
 constexpr SessionId kHolder = 0x7fffffff;
 
 struct Fnv {
@@ -981,25 +994,11 @@ StepRecord ScenarioDriver::step() {
         if (r.step > 0) {
             const DeviceStepStats ds = m.dev->collect(r.step - 1);
             StepRecord &prev = m.records[r.step - 1];
-            prev.device_ms = ds.device_ms;
-            prev.gather_ms = ds.gather_ms;
-            prev.attn_ms = ds.attn_ms;
-            std::copy(ds.phase_ms, ds.phase_ms + 8, prev.phase_ms);
-            prev.writeback_tokens = ds.writeback_tokens;
-            prev.gather_bytes = ds.train_bytes;
-            prev.attn_bytes = ds.attn_bytes;
-            prev.h2d_bytes = ds.h2d_bytes;
+            fill_device(prev, ds);
         }
         if (m.t >= m.cfg.steps) {
             const DeviceStepStats ds = m.dev->collect(r.step);
-            r.device_ms = ds.device_ms;
-            r.gather_ms = ds.gather_ms;
-            r.attn_ms = ds.attn_ms;
-            std::copy(ds.phase_ms, ds.phase_ms + 8, r.phase_ms);
-            r.writeback_tokens = ds.writeback_tokens;
-            r.gather_bytes = ds.train_bytes;
-            r.attn_bytes = ds.attn_bytes;
-            r.h2d_bytes = ds.h2d_bytes;
+            fill_device(r, ds);
         }
     }
     m.records.push_back(r);
@@ -1015,14 +1014,7 @@ const StepRecord &ScenarioDriver::record(uint64_t step) {
     StepRecord &r = m.records[step];
     if (m.dev && r.device_ms == 0.0 && m.dev->launched(step)) {
         const DeviceStepStats ds = m.dev->collect(step);
-        r.device_ms = ds.device_ms;
-        r.gather_ms = ds.gather_ms;
-        r.attn_ms = ds.attn_ms;
-        std::copy(ds.phase_ms, ds.phase_ms + 8, r.phase_ms);
-        r.writeback_tokens = ds.writeback_tokens;
-        r.gather_bytes = ds.train_bytes;
-        r.attn_bytes = ds.attn_bytes;
-        r.h2d_bytes = ds.h2d_bytes;
+        fill_device(r, ds);
     }
     return r;
 }

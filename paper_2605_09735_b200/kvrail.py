@@ -148,7 +148,7 @@ class StepRecord(C.Structure):
                 ("emitted_tokens", C.c_uint64), ("device_ms", C.c_double),
                 ("gather_ms", C.c_double), ("attn_ms", C.c_double), ("phase_ms", C.c_double * 8),
                 ("writeback_tokens", C.c_uint64), ("gather_bytes", C.c_uint64),
-                ("attn_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64)]
+                ("attn_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64), ("end_ns", C.c_uint64)]
 
 
 class Geometry(C.Structure):
