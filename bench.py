@@ -300,20 +300,27 @@ def run_b200(args, rank, local, world) -> dict | None:
         import torch.distributed as dist
         counts = torch.zeros(3, dtype=torch.int64, device=COLL_DEVICE)
     lat_ms = []
+    pending = []  # all-reduced (live, emitted, commits) per step, checked after timing
     with Clocks(local) as clocks:
         t0 = time.perf_counter()
         for _ in range(args.steps):
             ts = time.perf_counter()
             r = d.step()
-            if counts is not None:
+            if counts is not None:  # global counts; the single-commit audit, job-wide
                 counts.copy_(torch.tensor([r.live_sessions, r.emitted_tokens, r.commits]))
                 dist.all_reduce(counts)
+                pending.append(counts.clone())
             if latency:  # host control plane + descriptor + graph, to completion
                 d.sync()
                 lat_ms.append((time.perf_counter() - ts) * 1e3)
         d.sync()
         t1 = time.perf_counter()
     barrier(world)
+    for c_ in pending:  # MultiCommit audit over all GPUs (sim_engine.cpp:41-44)
+        live_all, _, commits_all = (int(x) for x in c_.tolist())
+        if commits_all != live_all:
+            raise RuntimeError(f"global single-commit audit failed: {commits_all} commits for "
+                               f"{live_all} live sessions")
     recs = [d.record(s) for s in range(first, first + args.steps)]
     # inter-token latency: successive step-end %globaltimer stamps (pipelined steps)
     itl_ms = [(recs[i].end_ns - recs[i - 1].end_ns) / 1e6 for i in range(1, len(recs))]
