@@ -298,16 +298,17 @@ def run_b200(args, rank, local, world) -> dict | None:
     if world > 1:  # per-step completion / EOS counts: the only cross-GPU traffic
         import torch
         import torch.distributed as dist
-        counts = torch.zeros(3, dtype=torch.int64, device=COLL_DEVICE)
+        counts = torch.zeros(4, dtype=torch.int64, device=COLL_DEVICE)
     lat_ms = []
-    pending = []  # all-reduced (live, emitted, commits) per step, checked after timing
+    pending = []  # all-reduced (live, emitted, commits/session, ranks live) per step
     with Clocks(local) as clocks:
         t0 = time.perf_counter()
         for _ in range(args.steps):
             ts = time.perf_counter()
             r = d.step()
             if counts is not None:  # global counts; the single-commit audit, job-wide
-                counts.copy_(torch.tensor([r.live_sessions, r.emitted_tokens, r.commits]))
+                counts.copy_(torch.tensor([r.live_sessions, r.emitted_tokens, r.commits,
+                                           int(r.live_sessions > 0)]))
                 dist.all_reduce(counts)
                 pending.append(counts.clone())
             if latency:  # host control plane + descriptor + graph, to completion
@@ -316,11 +317,12 @@ def run_b200(args, rank, local, world) -> dict | None:
         d.sync()
         t1 = time.perf_counter()
     barrier(world)
-    for c_ in pending:  # MultiCommit audit over all GPUs (sim_engine.cpp:41-44)
-        live_all, _, commits_all = (int(x) for x in c_.tolist())
-        if commits_all != live_all:
-            raise RuntimeError(f"global single-commit audit failed: {commits_all} commits for "
-                               f"{live_all} live sessions")
+    for c_ in pending:  # single-commit audit over all GPUs (sim_engine.cpp:41-44, 60):
+        # every rank with live sessions committed exactly once per session
+        _, _, commits_all, ranks_live = (int(x) for x in c_.tolist())
+        if commits_all != ranks_live:
+            raise RuntimeError(f"global single-commit audit failed: {commits_all} commit "
+                               f"frames for {ranks_live} ranks with live sessions")
     recs = [d.record(s) for s in range(first, first + args.steps)]
     # inter-token latency: successive step-end %globaltimer stamps (pipelined steps)
     itl_ms = [(recs[i].end_ns - recs[i - 1].end_ns) / 1e6 for i in range(1, len(recs))]
@@ -369,6 +371,19 @@ def run_b200(args, rank, local, world) -> dict | None:
     }
     d.close()
     return out
+
+
+def ncu_traffic(config: str, variant: str):
+    """DRAM bytes (read + write) per launch of the attention kernel from the committed
+    `ncu --set full` capture of this config (profiles/traffic.json), when the
+    captured kernel is the one this run used."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)[config]
+    except Exception:
+        return None, None
+    same = ("k_attn_tc" in t["kernel"]) == variant.startswith("k_attn_tc")
+    return (t["traffic_bytes"], t["source"]) if same else (None, None)
 
 
 def nearest_rank(xs: list[float], q: float) -> float:
@@ -438,6 +453,7 @@ def main():
     e2e = res["tokens"] / res["wall_s"]
     attn_gbs = res["attn_bytes"] / res["attn_s"] / 1e9 if res["attn_s"] else 0.0
     gather_gbs = 2 * res["gather_bytes"] / res["gather_s"] / 1e9 if res["gather_s"] else 0.0
+    traffic, traffic_src = ncu_traffic(args.config, res["variant"])
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["dev_s"] / args.steps * 1e3,
@@ -468,7 +484,8 @@ def main():
         "graph": {"kernels_per_step": res["step_kernels"], "captures": res["captures"],
                   "note": "one CUDA graph per descriptor ring slot, captured once, replayed every step"},
         "roofline": {"bound": "hbm", "achieved": attn_gbs, "peak": pk["hbm_gbs"], "unit": "GB/s",
-                     "frac": attn_gbs / pk["hbm_gbs"], "traffic": None,
+                     "frac": attn_gbs / pk["hbm_gbs"], "traffic": traffic,
+                     "traffic_src": traffic_src,
                      "kernel": res["variant"], "peak_src": pk["src"],
                      "bytes_per_launch": res["attn_bytes"] / args.steps,
                      "ms_per_launch": res["attn_s"] / args.steps * 1e3},
