@@ -100,6 +100,14 @@ RunResult run_scenario_on(const ScenarioConfig &cfg, const std::vector<TraceEven
 std::string report_to_json(const RunResult &result);
 std::string report_to_text(const RunResult &result);
 std::string steps_to_csv(const std::vector<StepRecord> &records);
+/// The reference steps.csv columns followed by the B200 measurements of each step
+/// (device time, inter-token latency, per-phase device time, bytes moved), so a
+/// simulated run and a measured run compare column for column.
+std::string measured_steps_csv(const std::vector<StepRecord> &records);
+/// Measured counterpart of report.json over the post-warm-up steps: decode tok/s on
+/// device time, device step and inter-token latency percentiles (nearest rank,
+/// metrics.cpp:23-33) beside the modeled ones, attention and gather bandwidth.
+std::string measured_report_json(const std::vector<StepRecord> &records, uint64_t warmup_steps);
 std::string delta_to_text(const DeltaReport &d);
 void write_file(const std::string &path, const std::string &content);
 

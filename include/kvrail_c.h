@@ -303,6 +303,11 @@ int kvr_driver_progress(kvr_driver *d, uint64_t *done, uint64_t *total);
  * the steps run so far; copies min(len, cap) bytes, *len = full length. */
 int kvr_driver_steps_csv(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len);
 int kvr_driver_report_json(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len);
+/* B200 measurement formats (no reference counterpart): steps.csv
+   columns + per-step device measurements, and the measured report over post-warm-up
+   steps. Both first complete every executed step's device measurements. */
+int kvr_driver_measured_csv(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len);
+int kvr_driver_measured_json(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len);
 /* Per-step parity trace (trains, pager digest); enabled by "b200.trace". */
 int kvr_driver_trace(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len);
 /* The driver's pager (borrowed; valid until kvr_driver_destroy). */

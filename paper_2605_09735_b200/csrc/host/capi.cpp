@@ -416,6 +416,25 @@ int kvr_driver_report_json(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len
     return call([&] { *len = copy_text(report_to_json(d->d->result()), buf, cap); });
 }
 
+static void complete_records(kvr_driver *d) {
+    for (uint64_t s = 0; s < d->d->steps_done(); ++s)
+        d->d->record(s);
+}
+
+int kvr_driver_measured_csv(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len) {
+    return call([&] {
+        complete_records(d);
+        *len = copy_text(measured_steps_csv(d->d->records()), buf, cap);
+    });
+}
+
+int kvr_driver_measured_json(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len) {
+    return call([&] {
+        complete_records(d);
+        *len = copy_text(measured_report_json(d->d->records(), d->d->config().warmup_steps), buf, cap);
+    });
+}
+
 int kvr_driver_trace(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len) {
     return call([&] { *len = copy_text(d->d->trace(), buf, cap); });
 }

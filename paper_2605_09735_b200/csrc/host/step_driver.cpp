@@ -1092,6 +1092,73 @@ std::string steps_to_csv(const std::vector<StepRecord> &records) {
     return out;
 }
 
+std::string measured_steps_csv(const std::vector<StepRecord> &records) {
+    std::string out = steps_to_csv(records);
+    const size_t nl = out.find('\n');
+    std::string head = out.substr(0, nl) +
+                       ",device_ms,itl_ms,gather_ms,attn_ms,apply_ms,hot_writes_ms,far_map_prime_ms,scan_ms,"
+                       "cold_writes_ms,writeback_tokens,gather_bytes,attn_bytes,h2d_bytes\n";
+    std::string body;
+    size_t pos = nl + 1;
+    char line[512];
+    for (size_t i = 0; i < records.size(); ++i) {
+        const StepRecord &r = records[i];
+        const size_t e = out.find('\n', pos);
+        body.append(out, pos, e - pos);
+        pos = e + 1;
+        const double itl = i > 0 && r.end_ns && records[i - 1].end_ns
+                               ? double(int64_t(r.end_ns - records[i - 1].end_ns)) / 1e6
+                               : 0.0;
+        std::snprintf(line, sizeof(line), ",%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%.6f,%llu,%llu,%llu,%llu\n",
+                      r.device_ms, itl, r.gather_ms, r.attn_ms, r.phase_ms[0], r.phase_ms[1], r.phase_ms[2],
+                      r.phase_ms[3], r.phase_ms[6], (unsigned long long)r.writeback_tokens,
+                      (unsigned long long)r.gather_bytes, (unsigned long long)r.attn_bytes,
+                      (unsigned long long)r.h2d_bytes);
+        body += line;
+    }
+    return head + body;
+}
+
+std::string measured_report_json(const std::vector<StepRecord> &records, uint64_t warmup_steps) {
+    std::vector<double> dev, itl, model;
+    double tokens = 0, dev_ms = 0, attn_ms = 0, gather_ms = 0;
+    uint64_t attn_bytes = 0, gather_bytes = 0, h2d = 0;
+    for (size_t i = warmup_steps; i < records.size(); ++i) {
+        const StepRecord &r = records[i];
+        if (r.device_ms <= 0.0)
+            continue;
+        dev.push_back(r.device_ms);
+        model.push_back(r.step_latency);
+        if (i > 0 && r.end_ns && records[i - 1].end_ns)
+            itl.push_back(double(int64_t(r.end_ns - records[i - 1].end_ns)) / 1e6);
+        tokens += double(r.emitted_tokens);
+        dev_ms += r.device_ms;
+        attn_ms += r.attn_ms;
+        gather_ms += r.gather_ms;
+        attn_bytes += r.attn_bytes;
+        gather_bytes += r.gather_bytes;
+        h2d += r.h2d_bytes;
+    }
+    if (dev.empty())
+        raise(Errc::empty_run, "no measured post-warm-up steps");
+    auto pct = [](const std::vector<double> &v) {
+        return ojson{{"p50", percentile_nearest_rank(v, 0.50)},
+                     {"p99", percentile_nearest_rank(v, 0.99)},
+                     {"p999", percentile_nearest_rank(v, 0.999)}};
+    };
+    ojson j;
+    j["measured_steps"] = dev.size();
+    j["decode_tokens_per_s"] = tokens / (dev_ms / 1e3);
+    j["device_step_ms"] = pct(dev);
+    if (!itl.empty())
+        j["inter_token_latency_ms"] = pct(itl);
+    j["modeled_step_latency"] = pct(model);
+    j["attention_gbs"] = attn_ms > 0 ? double(attn_bytes) / (attn_ms / 1e3) / 1e9 : 0.0;
+    j["gather_hbm_gbs"] = gather_ms > 0 ? 2.0 * double(gather_bytes) / (gather_ms / 1e3) / 1e9 : 0.0;
+    j["descriptor_h2d_bytes_per_step"] = double(h2d) / double(dev.size());
+    return j.dump(1);
+}
+
 static ojson report_json(const RunResult &res) {
     const RunReport &r = res.report;
     ojson j;

@@ -265,6 +265,8 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_driver_sync": [vp],
         "kvr_driver_progress": [vp, U64P, U64P],
         "kvr_driver_steps_csv": [vp, C.c_char_p, C.c_uint64, U64P],
+        "kvr_driver_measured_csv": [vp, C.c_char_p, C.c_uint64, U64P],
+        "kvr_driver_measured_json": [vp, C.c_char_p, C.c_uint64, U64P],
         "kvr_driver_report_json": [vp, C.c_char_p, C.c_uint64, U64P],
         "kvr_driver_trace": [vp, C.c_char_p, C.c_uint64, U64P],
         "kvr_driver_pager": [vp, C.POINTER(vp)],
@@ -670,6 +672,14 @@ class Driver:
 
     def report_json(self) -> str:
         return self._text(native_lib().kvr_driver_report_json)
+
+    def measured_csv(self) -> str:
+        """steps.csv columns + the B200 measurements of every executed step."""
+        return self._text(native_lib().kvr_driver_measured_csv)
+
+    def measured_json(self) -> str:
+        """Measured report over the post-warm-up steps (device runs only)."""
+        return self._text(native_lib().kvr_driver_measured_json)
 
     def trace(self) -> str:
         return self._text(native_lib().kvr_driver_trace)

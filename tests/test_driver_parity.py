@@ -119,3 +119,21 @@ def test_single_commit_audit_b16_to_b128():
         rep = json.loads(d.report_json())
         assert rep["invariant_audit"]["multi_commit_steps"] == 0
         assert rep["invariant_audit"]["shape_violations"] == 0
+
+
+def test_measured_csv_extends_reference_columns():
+    """measured_steps_csv = the reference steps.csv, column for column, plus the
+    B200 measurement columns (zeros on a host-only run)."""
+    cfg = json.loads(read("c1_config.json"))
+    cfg["trace_path"] = os.path.join(GOLD, "c1_events.csv")
+    d = kv.Driver(cfg)
+    d.run()
+    ref = d.steps_csv().strip().split("\n")
+    got = d.measured_csv().strip().split("\n")
+    assert len(ref) == len(got)
+    n = len(ref[0].split(","))
+    assert got[0].split(",")[n:][:2] == ["device_ms", "itl_ms"]
+    for a, b in zip(ref, got):
+        assert b.split(",")[:n] == a.split(",")
+    with pytest.raises(kv.KvrailError):
+        d.measured_json()  # nothing measured on a host-only run

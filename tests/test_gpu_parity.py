@@ -55,6 +55,11 @@ def test_c1_reference_bytes_on_device():
     assert_scan_exact(d, 64)
     # fixed shape: the two step graphs (one per descriptor ring slot) are never recaptured
     assert d.device().graph_captures() == 2
+    m = json.loads(d.measured_json())  # measured report beside the modeled one
+    assert m["measured_steps"] == 64 and m["decode_tokens_per_s"] > 0
+    assert m["device_step_ms"]["p50"] > 0 and m["inter_token_latency_ms"]["p50"] > 0
+    rows = d.measured_csv().strip().split("\n")
+    assert len(rows) == 65 and float(rows[10].split(",")[15]) > 0  # device_ms column
 
 
 @pytest.mark.parametrize("name", ["audit", "adv_burst"])
