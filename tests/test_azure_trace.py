@@ -26,7 +26,7 @@ def test_convert_sorts_rebases_clamps_and_windows(tmp_path):
     azure_trace.main([str(src), str(out), "--window-s", "60", "--max-prompt", "1024"])
     lines = out.read_text().strip().split("\n")
     assert lines[0] == "arrival_ms,prompt_tokens,generate_tokens"
-    assert lines[1:] == ["0,374,44", "0,879,1", "4314,396,109", "4440,1024,29"]
+    assert lines[1:] == ["0,374,44", "0,879,1", "4315,396,109", "4440,1024,29"]
 
 
 def test_converted_trace_replays(tmp_path):
