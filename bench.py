@@ -479,7 +479,7 @@ def main():
                             "max_step": res["max_step"]},
         "step_phases_ms_mean": res["phases"],
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],
-                "d2h_bytes_per_step": 32},
+                "d2h_bytes_per_step": 40},  # step counters (ScanCounters) read back
         "gpu_launches": res["step_kernels"] * args.steps,
         "graph": {"kernels_per_step": res["step_kernels"], "captures": res["captures"],
                   "note": "one CUDA graph per descriptor ring slot, captured once, replayed every step"},
