@@ -345,6 +345,7 @@ def run_b200(args, rank, local, world) -> dict | None:
     dev = d.device()
     variant = dev.attention_variant()
     step_kernels = dev.step_kernels()
+    backlog, dropped = d.prefill_backlog()
     captures = dev.graph_captures()
     dev_s_max, wall_s_max = reduce_max([dev_s, wall_s], world)
     tokens_all, gather_bytes_all = reduce_sum([float(tokens), float(gather_bytes)], world)
@@ -352,7 +353,8 @@ def run_b200(args, rank, local, world) -> dict | None:
         "rank": rank, "cfg": cfg, "recs": recs, "dev_s": dev_s_max, "wall_s": wall_s_max,
         "tokens": tokens_all, "attn_bytes": attn_bytes, "attn_s": attn_s,
         "gather_bytes": gather_bytes, "gather_s": gather_s, "gather_bytes_all": gather_bytes_all,
-        "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "captures": captures, "clocks": clocks.summary(), "fill_steps": fill,
+        "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "captures": captures,
+        "prefill_backlog": backlog, "prefill_dropped": dropped, "clocks": clocks.summary(), "fill_steps": fill,
         "live_mean": statistics.mean(r.live_sessions for r in recs),
         "trains_mean": statistics.mean(r.trains for r in recs),
         "dma_mean": statistics.mean(r.dma_bytes for r in recs),
@@ -468,6 +470,12 @@ def main():
             "attention_kernel": res["variant"], "fill_steps": res["fill_steps"],
             "prefill_budget": args.prefill_budget,
         },
+        "prefill": {"budget_tokens_per_step": args.prefill_budget,
+                    "queued_tokens_at_end": res["prefill_backlog"],
+                    "never_written_tokens": res["prefill_dropped"],
+                    "note": "budget 0 writes every prompt row at admission (the reference); with a "
+                            "budget, rows behind the window are queued and dropped unwritten if "
+                            "their page is recycled before any read"},
         "gather_hbm_gbs": gather_gbs,
         "transport": {"trains_per_step": res["trains_mean"], "mean_train_bytes":
                       res["mean_train_bytes"], "live_mean": res["live_mean"]},

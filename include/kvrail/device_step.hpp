@@ -86,7 +86,8 @@ public:
     /// before a gather, far summary, page copy or host read touches it, and
     /// dropped when its page is recycled.
     void set_prefill_budget(uint64_t tokens);
-    uint64_t deferred_tokens() const;
+    uint64_t deferred_tokens() const; // queued now
+    uint64_t dropped_tokens() const;  // never written: their page was recycled before any read
 
     // ---- parity / inspection (synchronous) ----
     void read_arena(uint64_t offset, uint64_t bytes, void *out);

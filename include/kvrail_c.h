@@ -308,6 +308,9 @@ int kvr_driver_report_json(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len
    steps. Both first complete every executed step's device measurements. */
 int kvr_driver_measured_csv(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len);
 int kvr_driver_measured_json(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len);
+/* b200.prefill_budget bookkeeping: cold prompt tokens queued now, and tokens never
+   written because their page was recycled before anything read them */
+int kvr_driver_prefill_backlog(kvr_driver *d, uint64_t *queued, uint64_t *dropped);
 /* Per-step parity trace (trains, pager digest); enabled by "b200.trace". */
 int kvr_driver_trace(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len);
 /* The driver's pager (borrowed; valid until kvr_driver_destroy). */

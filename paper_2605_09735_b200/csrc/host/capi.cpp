@@ -416,6 +416,14 @@ int kvr_driver_report_json(kvr_driver *d, char *buf, uint64_t cap, uint64_t *len
     return call([&] { *len = copy_text(report_to_json(d->d->result()), buf, cap); });
 }
 
+int kvr_driver_prefill_backlog(kvr_driver *d, uint64_t *queued, uint64_t *dropped) {
+    return call([&] {
+        const DeviceStep *dev = d->d->device();
+        *queued = dev ? dev->deferred_tokens() : 0;
+        *dropped = dev ? dev->dropped_tokens() : 0;
+    });
+}
+
 static void complete_records(kvr_driver *d) {
     for (uint64_t s = 0; s < d->d->steps_done(); ++s)
         d->d->record(s);

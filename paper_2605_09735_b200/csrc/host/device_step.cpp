@@ -56,7 +56,73 @@ struct DeviceStep::Impl {
     std::vector<uint32_t> far_ids;
     std::vector<kvr_slot_state> slots;
     std::vector<std::vector<uint64_t>> far_shown; // per slot, as of the last launch
-    std::deque<kvr_write_op> deferred;            // cold prefill rows not yet written
+    /// Cold prefill rows not yet written (prefill budget). Lookups by page and by
+    /// session are O(1); removed entries are marked dead (count 0) and skipped.
+    struct Deferred {
+        std::deque<kvr_write_op> q;
+        std::vector<uint32_t> per_block;
+        std::unordered_map<SessionId, uint32_t> per_session;
+        uint64_t tokens = 0;
+        uint64_t dropped = 0; // rows whose page was recycled before anything read them
+        bool has_block(BlockId b) const { return b < per_block.size() && per_block[b] != 0; }
+        bool has_session(SessionId s) const { return per_session.count(s) != 0; }
+        void push(const kvr_write_op &w) {
+            if (per_block.size() <= w.block)
+                per_block.resize(size_t(w.block) + 1, 0);
+            q.push_back(w);
+            ++per_block[w.block];
+            ++per_session[w.session];
+            tokens += w.count;
+        }
+        void kill(kvr_write_op &w) {
+            --per_block[w.block];
+            if (--per_session[w.session] == 0)
+                per_session.erase(w.session);
+            tokens -= w.count;
+            w.count = 0;
+        }
+        void trim_front() {
+            while (!q.empty() && q.front().count == 0)
+                q.pop_front();
+        }
+        /// Remove every live entry matching `pred`, handing it to `fn` first.
+        template <class Pred, class Fn> bool extract(Pred pred, Fn fn) {
+            bool any = false;
+            for (kvr_write_op &w : q)
+                if (w.count && pred(w)) {
+                    fn(w);
+                    kill(w);
+                    any = true;
+                }
+            trim_front();
+            return any;
+        }
+        /// Up to `budget` tokens from the front (the last op taken may be split).
+        void take(uint64_t budget, std::vector<kvr_write_op> &out) {
+            while (budget && !q.empty()) {
+                kvr_write_op &w = q.front();
+                if (w.count == 0) {
+                    q.pop_front();
+                    continue;
+                }
+                if (w.count <= budget) {
+                    budget -= w.count;
+                    out.push_back(w);
+                    kill(w);
+                    q.pop_front();
+                } else {
+                    kvr_write_op x = w;
+                    x.count = uint32_t(budget);
+                    out.push_back(x);
+                    w.token += budget;
+                    w.slot += uint32_t(budget);
+                    w.count -= uint32_t(budget);
+                    tokens -= budget;
+                    budget = 0;
+                }
+            }
+        }
+    } deferred;
     uint64_t prefill_budget = 0;                  // tokens per step; 0 = no deferral
     // state
     std::vector<uint8_t> clean; // page known to be all zeros on the device
@@ -159,39 +225,23 @@ struct DeviceStep::Impl {
         if (with_step && prefill_budget) {
             // Prefill budget: cold rows join the deferred queue, which drains at
             // most `prefill_budget` tokens per step; queued rows read this step
-            // are forced out with the hot writes.
-            for (auto it = deferred.begin(); it != deferred.end();) {
-                if (read_early(*it)) {
-                    hot.push_back(*it);
-                    it = deferred.erase(it);
-                } else {
-                    ++it;
-                }
-            }
+            // are forced out with the hot writes (scanned only when a staged page
+            // or a far job's session has queued rows).
+            bool scan = false;
+            for (BlockId b : staged)
+                scan |= deferred.has_block(b);
+            for (const kvr_write_op &f : far_jobs)
+                scan |= deferred.has_session(f.session);
+            if (scan)
+                deferred.extract(read_early, [&](const kvr_write_op &w) { hot.push_back(w); });
             // A queued row lies behind its session's window for good: it never
             // touches the ring, whatever later owns its device slot.
             for (kvr_write_op w : cold) {
                 w.dev_slot = KVR_NO_SLOT;
-                deferred.push_back(w);
+                deferred.push(w);
             }
             cold.clear();
-            uint64_t left = prefill_budget;
-            while (left && !deferred.empty()) {
-                kvr_write_op &w = deferred.front();
-                if (w.count <= left) {
-                    left -= w.count;
-                    cold.push_back(w);
-                    deferred.pop_front();
-                } else { // split the op at the budget
-                    kvr_write_op x = w;
-                    x.count = uint32_t(left);
-                    cold.push_back(x);
-                    w.token += left;
-                    w.slot += uint32_t(left);
-                    w.count -= uint32_t(left);
-                    left = 0;
-                }
-            }
+            deferred.take(prefill_budget, cold);
         }
         uint64_t prefix = 0;
         for (kvr_write_op &w : hot) {
@@ -306,9 +356,14 @@ struct DeviceStep::Impl {
     }
 
     void on_alloc(BlockId head, uint32_t count) {
-        if (!deferred.empty()) // a recycled page's old deferred rows are unobservable: drop
-            for (auto it = deferred.begin(); it != deferred.end();)
-                it = (it->block >= head && it->block < head + count) ? deferred.erase(it) : std::next(it);
+        if (deferred.tokens) { // a recycled page's old deferred rows are unobservable: drop
+            bool any = false;
+            for (uint32_t i = 0; i < count && !any; ++i)
+                any = deferred.has_block(head + i);
+            if (any)
+                deferred.extract([&](const kvr_write_op &w) { return w.block >= head && w.block < head + count; },
+                                 [&](const kvr_write_op &w) { deferred.dropped += w.count; });
+        }
         for (uint32_t i = 0; i < count; ++i) {
             const BlockId p = head + i;
             if (clean[p])
@@ -325,17 +380,10 @@ struct DeviceStep::Impl {
 
     // Deferred prefill rows of `b` (all pages when b == kInvalidBlock) are written now.
     void drain_deferred(BlockId b) {
-        bool any = false;
-        for (auto it = deferred.begin(); it != deferred.end();) {
-            if (b == kInvalidBlock || it->block == b) {
-                writes.push_back(*it);
-                it = deferred.erase(it);
-                any = true;
-            } else {
-                ++it;
-            }
-        }
-        if (any)
+        if (!deferred.tokens || (b != kInvalidBlock && !deferred.has_block(b)))
+            return;
+        if (deferred.extract([&](const kvr_write_op &w) { return b == kInvalidBlock || w.block == b; },
+                             [&](const kvr_write_op &w) { writes.push_back(w); }))
             flush();
     }
 
@@ -592,12 +640,8 @@ void DeviceStep::set_prefill_budget(uint64_t tokens) {
     impl_->prefill_budget = tokens;
 }
 
-uint64_t DeviceStep::deferred_tokens() const {
-    uint64_t n = 0;
-    for (const kvr_write_op &w : impl_->deferred)
-        n += w.count;
-    return n;
-}
+uint64_t DeviceStep::deferred_tokens() const { return impl_->deferred.tokens; }
+uint64_t DeviceStep::dropped_tokens() const { return impl_->deferred.dropped; }
 
 void DeviceStep::read_arena(uint64_t offset, uint64_t bytes, void *out) {
     impl_->drain_deferred(kInvalidBlock);

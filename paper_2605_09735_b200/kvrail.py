@@ -267,6 +267,7 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_driver_steps_csv": [vp, C.c_char_p, C.c_uint64, U64P],
         "kvr_driver_measured_csv": [vp, C.c_char_p, C.c_uint64, U64P],
         "kvr_driver_measured_json": [vp, C.c_char_p, C.c_uint64, U64P],
+        "kvr_driver_prefill_backlog": [vp, U64P, U64P],
         "kvr_driver_report_json": [vp, C.c_char_p, C.c_uint64, U64P],
         "kvr_driver_trace": [vp, C.c_char_p, C.c_uint64, U64P],
         "kvr_driver_pager": [vp, C.POINTER(vp)],
@@ -676,6 +677,12 @@ class Driver:
     def measured_csv(self) -> str:
         """steps.csv columns + the B200 measurements of every executed step."""
         return self._text(native_lib().kvr_driver_measured_csv)
+
+    def prefill_backlog(self) -> tuple[int, int]:
+        """(cold prompt tokens queued, tokens dropped unwritten) under b200.prefill_budget."""
+        q, dr = C.c_uint64(), C.c_uint64()
+        check(native_lib().kvr_driver_prefill_backlog(self.h, C.byref(q), C.byref(dr)))
+        return q.value, dr.value
 
     def measured_json(self) -> str:
         """Measured report over the post-warm-up steps (device runs only)."""
