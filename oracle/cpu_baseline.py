@@ -34,18 +34,17 @@ def control_plane_seconds_per_step(config: dict, steps: int = 200) -> float:
     return control_plane(config, steps)["seconds_per_step"]
 
 
-def control_plane(config: dict, steps: int = 200) -> dict:
-    """run_scenario of the reference on the shrunk geometry: wall seconds per step,
-    plus the staged (DMA) bytes per step scaled back to the real geometry and
-    the mean live batch, both from the reference's own steps.csv."""
+def shrink_config(config: dict) -> tuple[dict, int]:
+    """The workload with kv_head_dim and page_bytes shrunk by one power of two:
+    tokens per page, page counts and tau in pages (every pager / stage / reduce
+    decision) stay identical and pages stay powers of two (also for 320 KiB
+    tokens). Far view with 16-bit lanes (a B200 extension) runs the reference's
+    fp32 far view with the same token bytes. Returns (config, byte scale)."""
     cfg = copy.deepcopy(config)
     cfg.pop("b200", None)
     p = cfg.setdefault("pager", {})
-    # Shrink kv_head_dim and page_bytes by the same power of two: tokens per
-    # page, page counts and tau in pages (every pager / stage / reduce decision)
-    # stay identical, pages stay powers of two (also for 320 KiB tokens).
+    tb = 2 * p["layers"] * p["kv_head_dim"] * p["elem_bytes"]
     if cfg.get("far_view", {}).get("enabled") and p["elem_bytes"] == 2:
-        # the reference far view is fp32-only: same token bytes as fp32 lanes
         p.update({"elem_bytes": 4, "kv_head_dim": p["kv_head_dim"] // 2})
     scale = 1
     while p["kv_head_dim"] // scale > 16 and p["kv_head_dim"] % (2 * scale) == 0:
@@ -53,6 +52,15 @@ def control_plane(config: dict, steps: int = 200) -> dict:
     p.update({"kv_head_dim": p["kv_head_dim"] // scale, "page_bytes": p["page_bytes"] // scale})
     t = cfg.setdefault("transport", {})
     t["tau_bytes"] = int(t.get("tau_bytes", 131072) // scale)
+    tb_small = 2 * p["layers"] * p["kv_head_dim"] * p["elem_bytes"]
+    return cfg, tb // tb_small
+
+
+def control_plane(config: dict, steps: int = 200) -> dict:
+    """run_scenario of the reference on the shrunk geometry: wall seconds per step,
+    plus the staged (DMA) bytes per step scaled back to the real geometry and
+    the mean live batch, both from the reference's own steps.csv."""
+    cfg, scale = shrink_config(config)
     cfg["steps"] = steps
     cfg["warmup_steps"] = 0
     csv, _, _, wall = ob.ref_scenario(cfg, trace=False)

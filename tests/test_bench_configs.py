@@ -7,7 +7,6 @@ shrunk by one power of two (the cpu_baseline recipe) without audit failures —
 an admission the arena cannot hold makes the reference fail its single-commit
 audit (MultiCommit), so this also pins the arena caps.
 """
-import copy
 import os
 import sys
 
@@ -18,22 +17,13 @@ sys.path.insert(0, ROOT)
 
 import bench  # noqa: E402
 from oracle import bindings as ob  # noqa: E402
+from oracle.cpu_baseline import shrink_config  # noqa: E402
 
 pytestmark = pytest.mark.skipif(not ob.ref_available(), reason="oracle/_ref not built")
 
 
 def scaled(cfg: dict) -> dict:
-    c = copy.deepcopy(cfg)
-    c.pop("b200", None)
-    p = c["pager"]
-    if c.get("far_view", {}).get("enabled") and p["elem_bytes"] == 2:
-        p.update({"elem_bytes": 4, "kv_head_dim": p["kv_head_dim"] // 2})
-    scale = 1
-    while p["kv_head_dim"] // scale > 16 and p["kv_head_dim"] % (2 * scale) == 0:
-        scale *= 2
-    p.update({"kv_head_dim": p["kv_head_dim"] // scale, "page_bytes": p["page_bytes"] // scale})
-    c["transport"]["tau_bytes"] //= scale
-    return c
+    return shrink_config(cfg)[0]
 
 
 @pytest.mark.parametrize("world", [1, 2, 4, 8])
