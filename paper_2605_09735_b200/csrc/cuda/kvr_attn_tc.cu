@@ -38,6 +38,10 @@ constexpr uint32_t kHalfBytes = kRows * 128; // one 64-dim half of a K or V tile
 constexpr uint32_t kStageBytes = 4 * kHalfBytes; // K half0|half1, V half0|half1
 constexpr int kStages = 3;
 constexpr uint32_t kOpBytes = kN * kHd * 2; // one Q or P operand buffer (4 KiB)
+#ifndef KVR_TC_TILE5D
+#define KVR_TC_TILE5D 1
+#endif
+constexpr bool kUseTile5d = KVR_TC_TILE5D != 0;
 constexpr int kThreads = 384; // warp 0 TMA, warp 1 MMA, warps 4-7 / 8-11 softmax warpgroups
 
 __device__ inline uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
@@ -349,9 +353,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t *wgbuf = stages + kStages * kStageBytes;         // 2 x (Q | P0 | P1)
     float *red = reinterpret_cast<float *>(wgbuf + 2 * kWgBytes); // [wg][2][4][8] tile maxima
     float *lred = red + 2 * 2 * 4 * 8;                       // [wg][4][8] row sums
-    uint64_t *full = reinterpret_cast<uint64_t *>(lred + 2 * 4 * 8);
-    uint64_t *empty = full + kStages;
-    WgBars *wb = reinterpret_cast<WgBars *>(empty + kStages);
+    // K and V halves of a stage have their own rings: K is released as soon as
+    // its S MMA completes, V after the PV MMA (which waits on the softmax)
+    uint64_t *kfull = reinterpret_cast<uint64_t *>(lred + 2 * 4 * 8);
+    uint64_t *kempty = kfull + kStages, *vfull = kempty + kStages, *vempty = vfull + kStages;
+    WgBars *wb = reinterpret_cast<WgBars *>(vempty + kStages);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wb + 2);
 
     const kvr_step_header *h = hdr(c);
@@ -366,8 +372,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         reinterpret_cast<int4 *>(smem)[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&kfull[s], 1);
+            mbar_init(&kempty[s], 1);
+            mbar_init(&vfull[s], 1);
+            mbar_init(&vempty[s], 1);
         }
         for (int w = 0; w < 2; ++w) {
             mbar_init(&wb[w].qfull, 4);
@@ -391,12 +399,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) { // ---------------- producer (whole warp; lanes issue the TMA ops of a tile) ----------------
+    if (warp == 0 || warp == 2) { // ---------------- producers: warp 0 streams K, warp 2 streams V ----------------
+        const uint32_t kv = warp == 2 ? 1u : 0u;
+        uint64_t *full = kv ? vfull : kfull, *empty = kv ? vempty : kempty;
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.ring)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.tile)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.far)) : "memory");
         }
+        const int kvh0 = int(kv * c.Hkv); // first head index of this half in the ring row
         Stream S;
         S.init(c, slots, n_items);
         uint32_t s = 0, ph = 0, w, k, row_base = 0;
@@ -407,7 +418,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 row_base = uint32_t(I.L0 % c.R); // ring row of the item's first box
             const Tile tl = tile_of(I, k);
             mbar_wait(&empty[s], ph ^ 1);
-            const uint32_t st = smem_u32(stages + s * kStageBytes);
+            const uint32_t st = smem_u32(stages + s * kStageBytes) + kv * 2 * kHalfBytes;
             // near boxes holding a live row: boxes start at or after L0 > lo - 32, so
             // a box is live iff it starts below w
             const uint64_t first_tok = tl.tok_r0 + uint64_t(kSub) * tl.box_first;
@@ -416,20 +427,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t live_boxes = ((1u << n_live) - 1u) << tl.box_first;
             const uint32_t n4 = (tl.far_rows + 3) / 4;
             if (lane == 0)
-                mbar_expect_tx(&full[s], n4 * 4 * 512 + __popc(live_boxes) * 4 * kSub * 128);
+                mbar_expect_tx(&full[s], n4 * 2 * 512 + __popc(live_boxes) * 2 * kSub * 128);
             __syncwarp();
-            if (tl.far_rows) { // far summary rows: TMA gather4, 4 rows x 64 columns; op o = 4 * group + (kv, half)
+            if (tl.far_rows) { // far summary rows: TMA gather4, 4 rows x 64 columns; op o = 2 * group + half
                 const int base = plane * int(c.max_chunks);
                 const uint32_t *ids = far_ids + I.far_begin + tl.far_off;
-                for (uint32_t o = lane; o < 4 * n4; o += 32) {
-                    const uint32_t g4 = o >> 2, kv = (o >> 1) & 1u, hf = o & 1u;
+                for (uint32_t o = lane; o < 2 * n4; o += 32) {
+                    const uint32_t g4 = o >> 1, hf = o & 1u;
                     int r[4];
 #pragma unroll
                     for (int x = 0; x < 4; ++x)
                         r[x] = base + int(ids[min(4 * g4 + x, tl.far_rows - 1)]);
-                    tma_gather4(st + (2 * kv + hf) * kHalfBytes + g4 * 512, &maps.far,
-                                int((kv ? c.Hkv + I.head : I.head) * kHd + hf * 64), r[0], r[1], r[2], r[3],
-                                &full[s]);
+                    tma_gather4(st + hf * kHalfBytes + g4 * 512, &maps.far, int((kvh0 + I.head) * kHd + hf * 64),
+                                r[0], r[1], r[2], r[3], &full[s]);
                 }
             }
             uint32_t row0 = 0; // ring row of the first box (offsets within an item stay below R)
@@ -438,18 +448,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (row0 >= c.R)
                     row0 -= c.R;
             }
-            if (live_boxes == 0xfu && row0 + kRows <= c.R) {
-                // whole tile in one op: 5-D view (64 dims, flat ring rows, half, head, K|V)
+            if (kUseTile5d && live_boxes == 0xfu && row0 + kRows <= c.R) {
+                // this half of the whole tile in one op: 5-D view (64 dims, flat ring rows, half, head, K|V)
                 if (lane == 0)
-                    tma_load_5d(st, &maps.tile, 0, int(plane * c.R + row0), 0, int(I.head), 0, &full[s]);
-            } else if (lane < 16) { // lane = box * 4 + (kv, half), 32-row boxes never straddle the ring end
-                const uint32_t bx = lane >> 2, kv = (lane >> 1) & 1u, hf = lane & 1u;
+                    tma_load_5d(st, &maps.tile, 0, int(plane * c.R + row0), 0, int(I.head), int(kv), &full[s]);
+            } else if (lane < 8) { // lane = box * 2 + half, 32-row boxes never straddle the ring end
+                const uint32_t bx = lane >> 1, hf = lane & 1u;
                 if (live_boxes >> bx & 1u) {
                     uint32_t row = row0 + (bx - tl.box_first) * kSub;
                     if (row >= c.R)
                         row -= c.R;
-                    tma_load_4d(st + (2 * kv + hf) * kHalfBytes + bx * kSub * 128, &maps.ring, int(hf * 64),
-                                int(kv ? c.Hkv + I.head : I.head), int(row), plane, &full[s]);
+                    tma_load_4d(st + hf * kHalfBytes + bx * kSub * 128, &maps.ring, int(hf * 64), kvh0 + int(I.head),
+                                int(row), plane, &full[s]);
                 }
             }
             if (++s == kStages) {
@@ -468,7 +478,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         S.init(c, slots, n_items);
         uint32_t s = 0, ph = 0, w = 0, k = 0;
         uint32_t nw0 = 0, nw1 = 0, mw0 = 0, mw1 = 0, pv0 = 0, pv1 = 0;
-        uint32_t ring0 = 0, ring1 = 0; // pending tiles per warpgroup: byte (n & 3) = stage | K steps << 2
+        uint32_t ring0 = 0, ring1 = 0; // pending tiles per warpgroup: byte (n & 3) = stage | phase << 2 | K steps << 3
+        // PVs of one stage must follow the stage's fill order: the V ring runs behind
+        // the K ring, and a warpgroup may reach the PV of a later occupant of a stage
+        // before the other warpgroup's PV of the current one — testing that stage's
+        // vfull two phases ahead would alias. Bit s = parity of PVs issued for stage s.
+        uint32_t vpar = 0;
         const uint32_t stage0 = smem_u32(stages), wg0 = smem_u32(wgbuf);
         auto ready = [&](uint64_t *bar, uint32_t par) { return __shfl_sync(0xffffffffu, mbar_test(bar, par), 0); };
         Item I;
@@ -476,7 +491,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (have || pv0 < nw0 || pv1 < nw1) {
             if (have) {
                 const uint32_t nwc = w ? nw1 : nw0, b = nwc & 1u;
-                if ((k > 0 || ready(&wb[w].qfull, (w ? mw1 : mw0) & 1u)) && ready(&full[s], ph) &&
+                if ((k > 0 || ready(&wb[w].qfull, (w ? mw1 : mw0) & 1u)) && ready(&kfull[s], ph) &&
                     ready(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u)) {
                     tc_fence_after();
                     if (elect_one()) {
@@ -487,12 +502,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                             mma_f16(tmem + 64 * w + 16 * b, a0 + (((kk >> 2) * kHalfBytes + (kk & 3u) * 32) >> 4),
                                     b0 + kk * (256 >> 4), id_s, kk > 0);
                         mma_commit(&wb[w].sfull[b]);
+                        mma_commit(&kempty[s]); // the K half is free once S is computed
                     }
                     __syncwarp();
                     if (k == 0)
                         (w ? mw1 : mw0) += 1;
                     const uint32_t nk = tile_of(I, k).nk;
-                    const uint32_t sh = 8 * (nwc & 3u), e = (s | nk << 2) << sh;
+                    const uint32_t sh = 8 * (nwc & 3u), e = (s | ph << 2 | nk << 3) << sh;
                     if (w)
                         ring1 = (ring1 & ~(0xffu << sh)) | e;
                     else
@@ -511,9 +527,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (pvn >= (x ? nw1 : nw0))
                     continue;
                 const uint32_t b = pvn & 1u, par = (pvn >> 1) & 1u;
-                if (!ready(&wb[x].pfull[b], par) || !ready(&wb[x].oempty[b], par ^ 1u))
+                const uint32_t e = ((x ? ring1 : ring0) >> (8 * (pvn & 3u))) & 0xffu, st = e & 3u,
+                               sph = (e >> 2) & 1u, nk = e >> 3;
+                if (((vpar >> st) & 1u) != sph || !ready(&wb[x].pfull[b], par) || !ready(&wb[x].oempty[b], par ^ 1u) ||
+                    !ready(&vfull[st], sph))
                     continue;
-                const uint32_t e = ((x ? ring1 : ring0) >> (8 * (pvn & 3u))) & 0xffu, st = e & 3u, nk = e >> 2;
                 tc_fence_after();
                 if (elect_one()) {
                     const uint64_t a0 = sdesc(stage0 + st * kStageBytes + 2 * kHalfBytes, kHalfBytes, 1024, 2);
@@ -522,9 +540,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                         mma_f16(tmem + 64 * x + 32 + 16 * b, a0 + kk * (2048 >> 4), b0 + kk * (256 >> 4), id_o,
                                 kk > 0);
                     mma_commit(&wb[x].ofull[b]);
-                    mma_commit(&empty[st]);
+                    mma_commit(&vempty[st]);
                 }
                 __syncwarp();
+                vpar ^= 1u << st;
                 (x ? pv1 : pv0) += 1;
             }
         }
@@ -706,7 +725,7 @@ bool attn_tc_supported(const DevCtx &c) {
 }
 
 size_t attn_tc_smem() {
-    return 1024 + kStages * kStageBytes + 2 * kWgBytes + (2 * 2 * 4 * 8 + 2 * 4 * 8) * 4 + 2 * kStages * 8 +
+    return 1024 + kStages * kStageBytes + 2 * kWgBytes + (2 * 2 * 4 * 8 + 2 * 4 * 8) * 4 + 4 * kStages * 8 +
            2 * sizeof(WgBars) + 16;
 }
 
@@ -739,10 +758,10 @@ bool attn_tc_maps(const DevCtx &c, TcMaps *maps) {
     const cuuint64_t s4[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
     const cuuint32_t b4[4] = {64, 1, uint32_t(kSub), 1};
     // whole tiles: (64 dims, flat rows = plane * R + row, half, head, K|V); the box
-    // lands as [K|V][half][128 rows][64 dims], exactly the stage layout
+    // (box kv = 1) lands as [half][128 rows][64 dims], one K or V half of a stage
     const cuuint64_t d5[5] = {64, uint64_t(c.L) * c.n_slots * c.R, 2, c.Hkv, 2};
     const cuuint64_t s5[4] = {2ull * c.Hkv * row, 128, row, uint64_t(c.Hkv) * row};
-    const cuuint32_t b5[5] = {64, uint32_t(kRows), 2, 1, 2};
+    const cuuint32_t b5[5] = {64, uint32_t(kRows), 2, 1, 1};
     // far rows: (row_elems, n_slots*L*max_chunks rows), 64 x 1 boxes for gather4
     const cuuint64_t df[2] = {c.row_elems, uint64_t(c.n_slots) * c.L * c.max_chunks};
     const cuuint64_t sf[1] = {uint64_t(c.row_elems) * c.esz};

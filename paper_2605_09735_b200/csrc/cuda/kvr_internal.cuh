@@ -102,6 +102,7 @@ const void *attn_tc_kernel(const DevCtx &c);
 struct TcMaps {
     CUtensorMap ring, tile, far;
 };
+// (tile: one K or V half of a 128-row tile per op — the two halves have separate rings)
 bool attn_tc_maps(const DevCtx &c, TcMaps *maps);
 void launch_attn_tc(const void *fn, const DevCtx &c, const TcMaps &maps, uint32_t grid, cudaStream_t s);
 void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s);

@@ -1,7 +1,7 @@
 """Full-scale parity spot check: after the bench's fill + warm-up steps, the window
 ring bytes of sampled slots equal the arena (through the pager's view), far rows
 equal their summary slots, and the attention of sampled (layer, q-head) pairs is
-within 1e-3 of the double-precision oracle. Usage: scale_parity.py [c2|c3|c5]."""
+within 1e-3 of the double-precision oracle. Usage: scale_parity.py [c2|c3|c5] [slots]."""
 import sys
 import time
 
@@ -12,6 +12,8 @@ from oracle import bindings as ob  # noqa: E402
 
 name = sys.argv[1] if len(sys.argv) > 1 else "c2"
 cfg = bench.CONFIGS[name](400)
+if len(sys.argv) > 2:  # fewer slots: same per-slot geometry, quicker check
+    cfg["workload"]["concurrency"] = int(sys.argv[2])
 d = pkg.Driver(cfg, device=0)
 width = cfg["workload"]["concurrency"]
 for i in range(400):

@@ -140,17 +140,18 @@ def test_tcgen05_gqa_attention(dtype, kvh, qh, w_star):
 
 @pytest.mark.parametrize("far", [False, True])
 def test_tcgen05_many_items_per_cta(far):
-    """More (slot, layer, kv-head) items than 2 x SMs: both softmax warpgroups
-    run interleaved item streams and one runs out first (the single-warpgroup
-    tail of the schedule)."""
+    """~14 (slot, layer, kv-head) items per CTA: both softmax warpgroups run
+    alternating item streams, one runs out first (the single-warpgroup tail),
+    and the V ring (behind the K ring) sees a warpgroup reach the PV of a later
+    occupant of a stage before the other warpgroup's PV of the current one."""
     cfg = c1()
     del cfg["trace_path"]
     cfg["steps"] = 48
-    cfg["pager"].update({"layers": 8, "kv_head_dim": 256, "page_bytes": 16 * 2 * 8 * 256 * 2})
+    cfg["pager"].update({"layers": 16, "kv_head_dim": 256, "page_bytes": 16 * 2 * 16 * 256 * 2})
     cfg["transport"]["tau_bytes"] = 8 * cfg["pager"]["page_bytes"]
-    cfg["workload"] = {"requests": 10000, "concurrency": 40, "prompt_min": 64, "prompt_max": 1024,
+    cfg["workload"] = {"requests": 10000, "concurrency": 64, "prompt_min": 64, "prompt_max": 1024,
                        "arrivals_per_window": 40.0, "seed": 1}
-    cfg["shaping"] = {"arena_pages": 6000, "staged_refresh_period": 4}
+    cfg["shaping"] = {"arena_pages": 12000, "staged_refresh_period": 4}
     if far:
         cfg["far_view"] = {"enabled": True, "w_star": 256, "cap": 16, "sv_chunk": 64}
     d = run(cfg, kv_heads=2, head_dim=128, q_heads=8, payload="lanes", dtype="bf16",

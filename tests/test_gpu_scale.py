@@ -22,3 +22,14 @@ def test_full_scale_control_plane_matches_reference(name, steps):
                          cwd=ROOT, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
     assert f"{steps} steps identical" in out.stdout
+
+
+def test_c5_geometry_attention_with_many_items_per_cta():
+    """C5 geometry (80 layers, g = 8, far rows + 512-token windows) with 4 slots:
+    ~17 items per CTA, so the two softmax warpgroups hand over items while the
+    V ring trails the K ring (a warpgroup can reach the PV of a later occupant
+    of a stage first: the MMA issuer must keep each stage's PV order)."""
+    out = subprocess.run([sys.executable, "scripts/scale_parity.py", "c5", "4"], cwd=ROOT,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "window exact" in out.stdout
