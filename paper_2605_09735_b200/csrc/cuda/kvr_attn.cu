@@ -427,7 +427,7 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
             return nullptr;
         }
         p->grid = uint32_t(sms);
-        std::snprintf(p->name, sizeof(p->name), "k_attn_tc<%s,hd%u,g%u> tcgen05 M128 N16 stages=3",
+        std::snprintf(p->name, sizeof(p->name), "k_attn_tc<%s,hd%u,g%u> tcgen05 M128 N16 K3+V3 rings",
                       c.elem_kind == KVR_ELEM_F16 ? "f16" : "bf16", c.hd, c.group);
         return p;
     }

@@ -35,8 +35,17 @@ constexpr int kHd = 128;                   // head dim (S: K, PV: M)
 constexpr int kN = 16;                     // MMA N: g hi columns + g lo columns
 constexpr int kSub = 32;                   // rows per TMA box
 constexpr uint32_t kHalfBytes = kRows * 128; // one 64-dim half of a K or V tile (16 KiB)
-constexpr uint32_t kStageBytes = 4 * kHalfBytes; // K half0|half1, V half0|half1
-constexpr int kStages = 3;
+constexpr uint32_t kSideBytes = 2 * kHalfBytes; // a K (or V) tile: two 64-dim halves, 32 KiB
+#ifndef KVR_TC_KSTAGES
+#define KVR_TC_KSTAGES 3
+#endif
+#ifndef KVR_TC_VSTAGES
+#define KVR_TC_VSTAGES 3
+#endif
+// K tiles are released as soon as their S MMA completes, V tiles after the
+// softmax and the PV MMA (measured: 3 + 3 beats 2 + 4 on C3 and C5)
+constexpr int kKStages = KVR_TC_KSTAGES, kVStages = KVR_TC_VSTAGES;
+static_assert(kVStages <= 4, "V stage index and phase are packed in 3 bits");
 constexpr uint32_t kOpBytes = kN * kHd * 2; // one Q or P operand buffer (4 KiB)
 #ifndef KVR_TC_TILE5D
 #define KVR_TC_TILE5D 1
@@ -349,15 +358,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     static_assert(2 * G <= kN, "hi/lo columns must fit N = 16");
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t *stages = smem;                                  // kStages x 64 KiB
-    uint8_t *wgbuf = stages + kStages * kStageBytes;         // 2 x (Q | P0 | P1)
+    uint8_t *kbuf = smem;                                    // kKStages x 32 KiB
+    uint8_t *vbuf = kbuf + kKStages * kSideBytes;            // kVStages x 32 KiB
+    uint8_t *wgbuf = vbuf + kVStages * kSideBytes;           // 2 x (Q | P0 | P1)
     float *red = reinterpret_cast<float *>(wgbuf + 2 * kWgBytes); // [wg][2][4][8] tile maxima
     float *lred = red + 2 * 2 * 4 * 8;                       // [wg][4][8] row sums
     // K and V halves of a stage have their own rings: K is released as soon as
     // its S MMA completes, V after the PV MMA (which waits on the softmax)
     uint64_t *kfull = reinterpret_cast<uint64_t *>(lred + 2 * 4 * 8);
-    uint64_t *kempty = kfull + kStages, *vfull = kempty + kStages, *vempty = vfull + kStages;
-    WgBars *wb = reinterpret_cast<WgBars *>(vempty + kStages);
+    uint64_t *kempty = kfull + kKStages, *vfull = kempty + kKStages, *vempty = vfull + kVStages;
+    WgBars *wb = reinterpret_cast<WgBars *>(vempty + kVStages);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wb + 2);
 
     const kvr_step_header *h = hdr(c);
@@ -368,12 +378,14 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     // zero stages and operand buffers: rows a tile does not load must hold
     // finite values (p = 0 times V), unused hi/lo columns must be 0
-    for (uint32_t i = threadIdx.x; i < (kStages * kStageBytes + 2 * kWgBytes) / 16; i += kThreads)
+    for (uint32_t i = threadIdx.x; i < ((kKStages + kVStages) * kSideBytes + 2 * kWgBytes) / 16; i += kThreads)
         reinterpret_cast<int4 *>(smem)[i] = make_int4(0, 0, 0, 0);
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
+        for (int s = 0; s < kKStages; ++s) {
             mbar_init(&kfull[s], 1);
             mbar_init(&kempty[s], 1);
+        }
+        for (int s = 0; s < kVStages; ++s) {
             mbar_init(&vfull[s], 1);
             mbar_init(&vempty[s], 1);
         }
@@ -402,6 +414,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0 || warp == 2) { // ---------------- producers: warp 0 streams K, warp 2 streams V ----------------
         const uint32_t kv = warp == 2 ? 1u : 0u;
         uint64_t *full = kv ? vfull : kfull, *empty = kv ? vempty : kempty;
+        const uint32_t n_stages = kv ? kVStages : kKStages;
+        uint8_t *ring = kv ? vbuf : kbuf;
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.ring)) : "memory");
             asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&maps.tile)) : "memory");
@@ -418,7 +432,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 row_base = uint32_t(I.L0 % c.R); // ring row of the item's first box
             const Tile tl = tile_of(I, k);
             mbar_wait(&empty[s], ph ^ 1);
-            const uint32_t st = smem_u32(stages + s * kStageBytes) + kv * 2 * kHalfBytes;
+            const uint32_t st = smem_u32(ring + s * kSideBytes);
             // near boxes holding a live row: boxes start at or after L0 > lo - 32, so
             // a box is live iff it starts below w
             const uint64_t first_tok = tl.tok_r0 + uint64_t(kSub) * tl.box_first;
@@ -462,7 +476,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 int(row), plane, &full[s]);
                 }
             }
-            if (++s == kStages) {
+            if (++s == n_stages) {
                 s = 0;
                 ph ^= 1;
             }
@@ -477,14 +491,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         Stream S;
         S.init(c, slots, n_items);
         uint32_t s = 0, ph = 0, w = 0, k = 0;
+        uint32_t sv = 0, phv = 0; // V ring position of the tile whose S is issued next
         uint32_t nw0 = 0, nw1 = 0, mw0 = 0, mw1 = 0, pv0 = 0, pv1 = 0;
-        uint32_t ring0 = 0, ring1 = 0; // pending tiles per warpgroup: byte (n & 3) = stage | phase << 2 | K steps << 3
+        uint32_t ring0 = 0, ring1 = 0; // pending tiles per warpgroup: byte (n & 3) = V stage | V phase << 2 | K steps << 3
         // PVs of one stage must follow the stage's fill order: the V ring runs behind
         // the K ring, and a warpgroup may reach the PV of a later occupant of a stage
         // before the other warpgroup's PV of the current one — testing that stage's
         // vfull two phases ahead would alias. Bit s = parity of PVs issued for stage s.
         uint32_t vpar = 0;
-        const uint32_t stage0 = smem_u32(stages), wg0 = smem_u32(wgbuf);
+        const uint32_t kbase = smem_u32(kbuf), vbase = smem_u32(vbuf), wg0 = smem_u32(wgbuf);
         auto ready = [&](uint64_t *bar, uint32_t par) { return __shfl_sync(0xffffffffu, mbar_test(bar, par), 0); };
         Item I;
         bool have = S.next(c, slots, n_items, w, k, I);
@@ -495,7 +510,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ready(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u)) {
                     tc_fence_after();
                     if (elect_one()) {
-                        const uint64_t a0 = sdesc(stage0 + s * kStageBytes, 16, 1024, 2);
+                        const uint64_t a0 = sdesc(kbase + s * kSideBytes, 16, 1024, 2);
                         const uint64_t b0 = sdesc(wg0 + w * kWgBytes, 128, 2048, 0);
 #pragma unroll
                         for (uint32_t kk = 0; kk < kHd / 16; ++kk) // K: 32 B steps in a 128-B row, then next half
@@ -508,15 +523,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if (k == 0)
                         (w ? mw1 : mw0) += 1;
                     const uint32_t nk = tile_of(I, k).nk;
-                    const uint32_t sh = 8 * (nwc & 3u), e = (s | ph << 2 | nk << 3) << sh;
+                    const uint32_t sh = 8 * (nwc & 3u), e = (sv | phv << 2 | nk << 3) << sh;
                     if (w)
                         ring1 = (ring1 & ~(0xffu << sh)) | e;
                     else
                         ring0 = (ring0 & ~(0xffu << sh)) | e;
                     (w ? nw1 : nw0) += 1;
-                    if (++s == kStages) {
+                    if (++s == kKStages) {
                         s = 0;
                         ph ^= 1;
+                    }
+                    if (++sv == kVStages) {
+                        sv = 0;
+                        phv ^= 1;
                     }
                     have = S.next(c, slots, n_items, w, k, I);
                 }
@@ -534,7 +553,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     continue;
                 tc_fence_after();
                 if (elect_one()) {
-                    const uint64_t a0 = sdesc(stage0 + st * kStageBytes + 2 * kHalfBytes, kHalfBytes, 1024, 2);
+                    const uint64_t a0 = sdesc(vbase + st * kSideBytes, kHalfBytes, 1024, 2);
                     const uint64_t b0 = sdesc(wg0 + x * kWgBytes + (1 + b) * kOpBytes, 128, 2048, 0);
                     for (uint32_t kk = 0; kk < nk; ++kk) // +2048 B (V rows) / +256 B (P cores) per K step
                         mma_f16(tmem + 64 * x + 32 + 16 * b, a0 + kk * (2048 >> 4), b0 + kk * (256 >> 4), id_o,
@@ -725,7 +744,8 @@ bool attn_tc_supported(const DevCtx &c) {
 }
 
 size_t attn_tc_smem() {
-    return 1024 + kStages * kStageBytes + 2 * kWgBytes + (2 * 2 * 4 * 8 + 2 * 4 * 8) * 4 + 4 * kStages * 8 +
+    return 1024 + (kKStages + kVStages) * kSideBytes + 2 * kWgBytes + (2 * 2 * 4 * 8 + 2 * 4 * 8) * 4 +
+           2 * (kKStages + kVStages) * 8 +
            2 * sizeof(WgBars) + 16;
 }
 
