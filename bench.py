@@ -348,10 +348,12 @@ def run_b200(args, rank, local, world) -> dict | None:
     backlog, dropped = d.prefill_backlog()
     captures = dev.graph_captures()
     dev_s_max, wall_s_max = reduce_max([dev_s, wall_s], world)
-    tokens_all, gather_bytes_all = reduce_sum([float(tokens), float(gather_bytes)], world)
+    tokens_all, gather_bytes_all, attn_bytes_all = reduce_sum(
+        [float(tokens), float(gather_bytes), float(attn_bytes)], world)
     out = {
         "rank": rank, "cfg": cfg, "recs": recs, "dev_s": dev_s_max, "wall_s": wall_s_max,
         "tokens": tokens_all, "attn_bytes": attn_bytes, "attn_s": attn_s,
+        "attn_bytes_all": attn_bytes_all,
         "gather_bytes": gather_bytes, "gather_s": gather_s, "gather_bytes_all": gather_bytes_all,
         "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "captures": captures,
         "prefill_backlog": backlog, "prefill_dropped": dropped, "clocks": clocks.summary(), "fill_steps": fill,
@@ -456,6 +458,7 @@ def main():
     attn_gbs = res["attn_bytes"] / res["attn_s"] / 1e9 if res["attn_s"] else 0.0
     gather_gbs = 2 * res["gather_bytes"] / res["gather_s"] / 1e9 if res["gather_s"] else 0.0
     traffic, traffic_src = ncu_traffic(args.config, res["variant"])
+    roof_tps = res["tokens"] / (res["attn_bytes_all"] / (world * pk["hbm_gbs"] * 1e9))
     line = {
         "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["dev_s"] / args.steps * 1e3,
@@ -477,6 +480,12 @@ def main():
                             "budget, rows behind the window are queued and dropped unwritten if "
                             "their page is recycled before any read"},
         "gather_hbm_gbs": gather_gbs,
+        # decode tok/s roofline = tokens / (KV bytes the attention must read / peak)
+        "decode_roofline": {
+            "tokens_per_s": roof_tps,
+            "frac": value / roof_tps,
+            "note": "whole step (writes, scan, gather, attention, host) against the attention's "
+                    "algorithmic KV bytes at the measured copy bandwidth"},
         "transport": {"trains_per_step": res["trains_mean"], "mean_train_bytes":
                       res["mean_train_bytes"], "live_mean": res["live_mean"]},
         "step_latency_ms": {"p50": res["p50_ms"], "p99": res["p99_ms"], "clock": "device",
