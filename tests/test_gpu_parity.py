@@ -62,6 +62,13 @@ def test_c1_reference_bytes_on_device():
     assert len(rows) == 65 and float(rows[10].split(",")[15]) > 0  # device_ms column
 
 
+def test_c1_reference_bytes_without_graph():
+    """The same step launched kernel by kernel (b200.graph = 0) gives the same trace."""
+    d = run(c1(), kv_heads=4, head_dim=64, payload="bytes", attention=False, graph=0)
+    assert d.trace() == read("c1_trace.txt")
+    assert d.device().graph_captures() == 0
+
+
 @pytest.mark.parametrize("name", ["audit", "adv_burst"])
 def test_golden_scenarios_on_device(name):
     cfg = json.loads(read(f"{name}_config.json"))
