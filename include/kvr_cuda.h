@@ -61,8 +61,8 @@ typedef struct kvr_step_header {
     uint32_t n_zero, n_cow, n_edit, n_write, n_blob, n_need, n_span, n_prime, n_far_ids;
     uint32_t n_far_jobs;    /* source-1 ops: the last n_far_jobs of the n_write ops */
     uint32_t n_cold;        /* write ops are [hot ... | cold ... | far jobs ...]; cold ops
-                               touch rows no kernel of this step reads and run on a
-                               graph branch concurrent with the attention */
+                               touch rows no kernel of this step reads and run after
+                               the attention */
     uint32_t pad_h;
     uint64_t write_tokens;  /* sum of kvr_write_op.count over hot source-0 writes */
     uint64_t write_tokens_cold; /* ... over cold source-0 writes */

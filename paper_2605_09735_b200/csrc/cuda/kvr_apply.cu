@@ -117,7 +117,7 @@ __device__ inline int4 payload16(const DevCtx &c, const LaneTable &tab, uint32_t
 }
 
 // `cold`: 0 = the hot write ops (rows read later in this step), 1 = the cold ops
-// (older prompt rows; launched on a graph branch concurrent with K-attn).
+// (older prompt rows nothing in this step reads; launched after K-attn).
 template <uint32_t kPer> // chunks per thread per unit (independent generator chains)
 __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
     __shared__ LaneTable tab;
@@ -394,13 +394,12 @@ void launch_apply(const DevCtx &c, cudaStream_t s, int sms) {
     k_blob<<<sms, 256, 0, s>>>(c);
 }
 
-// cold: 0 hot writes (whole GPU), 1 cold writes (whole GPU, apply-only path),
-// 2 cold writes beside the attention (one CTA per SM)
+// cold: 0 hot writes, 1 cold writes (both over the whole GPU)
 void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold) {
     // hot writes (few decode tokens + window rows): one chunk per thread for
     // spread; cold prompt rows: two chunks per thread for generator ILP
     if (cold)
-        k_write<2><<<cold == 2 ? sms : sms * 8, 256, 0, s>>>(c, 1);
+        k_write<2><<<sms * 8, 256, 0, s>>>(c, 1);
     else
         k_write<1><<<sms * 8, 256, 0, s>>>(c, 0);
 }

@@ -39,8 +39,6 @@ struct kvr_dev {
     ScanCounters *h_scan[2] = {nullptr, nullptr};
     cudaEvent_t ev_start[2] = {}, ev_stop[2] = {}, ev_attn[2] = {};
     cudaEvent_t ev_phase[2][8] = {}; // per ring slot: phase boundaries inside the step graph
-    cudaStream_t side = nullptr;     // graph branch for cold writes
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
     AttnPlan *attn = nullptr;
     uint32_t graph_kernels = 0; // kernel nodes in the captured step graph
@@ -173,9 +171,6 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         ck(cudaGetDeviceProperties(&prop, g.device), "cudaGetDeviceProperties");
         d->sms = prop.multiProcessorCount;
         ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
-        ck(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking), "side stream");
-        ck(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming), "event");
-        ck(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming), "event");
         for (int i = 0; i < 2; ++i) {
             ck(cudaEventCreate(&d->ev_start[i]), "event");
             ck(cudaEventCreate(&d->ev_stop[i]), "event");
@@ -291,12 +286,6 @@ int kvr_dev_close(kvr_dev *d) {
         cudaFree(p);
     if (d->attn)
         free_attn_plan(d->attn);
-    if (d->side)
-        cudaStreamDestroy(d->side);
-    if (d->ev_fork)
-        cudaEventDestroy(d->ev_fork);
-    if (d->ev_join)
-        cudaEventDestroy(d->ev_join);
     if (d->stream)
         cudaStreamDestroy(d->stream);
     delete d;
