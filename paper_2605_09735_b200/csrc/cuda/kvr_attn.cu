@@ -75,14 +75,6 @@ template <> struct Pair<__nv_bfloat16> {
     }
 };
 
-// Element-pair access for the three element types (fp32 pairs are 8 bytes).
-template <typename T> __device__ inline float2 load_pair(const T *p) {
-    return Pair<T>::f2(*reinterpret_cast<const uint32_t *>(p));
-}
-template <> __device__ inline float2 load_pair<float>(const float *p) {
-    return *reinterpret_cast<const float2 *>(p);
-}
-
 __device__ inline float warp_max(float v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1)

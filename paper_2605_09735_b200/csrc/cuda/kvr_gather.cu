@@ -57,7 +57,6 @@ template <int N> __device__ inline void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
 __device__ inline void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-__device__ inline void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 /// Resolve unit -> (src, dst, bytes); bytes == 0 when the row is masked out.
 struct Move {
