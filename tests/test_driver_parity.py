@@ -137,3 +137,21 @@ def test_measured_csv_extends_reference_columns():
         assert b.split(",")[:n] == a.split(",")
     with pytest.raises(kv.KvrailError):
         d.measured_json()  # nothing measured on a host-only run
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_random_workloads_match_reference(seed, has_ref):
+    """Random small workloads (geometry, window, far view, transport knobs, regimes,
+    sharing, EOS bursts; tests/test_gpu_fuzz.py:random_config) — steps.csv,
+    report.json and the parity trace byte-identical to the reference Driver."""
+    if not has_ref:
+        pytest.skip("oracle/_ref not built")
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from test_gpu_fuzz import random_config
+    cfg = random_config(seed)
+    csv, rep, tr, _ = ob.ref_scenario(cfg, trace=True)
+    d = mine(dict(cfg, b200={"trace": True}))
+    assert d.steps_csv() == csv
+    assert d.report_json() == rep
+    assert d.trace() == tr
