@@ -93,3 +93,39 @@ def test_random_workload_attention_lanes(seed):
     checked, bad, first = d.device_check()
     assert bad == 0, first
     assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
+@pytest.mark.parametrize("seed", range(200, 210))
+def test_random_workload_tensor_core_attention(seed):
+    """The tcgen05 kernel on random windows, GQA groups 1-8, far views (bf16 far
+    rows are a B200 extension, so these runs are checked against the oracle only)."""
+    rng = random.Random(seed)
+    kvh = rng.choice([1, 2])
+    g = rng.choice([1, 2, 4, 8])
+    tpp = rng.choice([8, 16])
+    layers = rng.choice([1, 2, 4])
+    tb = 2 * layers * kvh * 128 * 2
+    page = 1
+    while page < tpp * tb:
+        page *= 2
+    tpp = page // tb
+    far = rng.random() < 0.5
+    cfg = {
+        "label": f"tc{seed}", "seed": seed, "steps": rng.choice([40, 80]), "warmup_steps": 0,
+        "pager": {"page_bytes": page, "layers": layers, "kv_head_dim": kvh * 128, "elem_bytes": 2},
+        "transport": {"tau_bytes": 8 * page},
+        "far_view": {"enabled": far, "w_star": rng.choice([64, 128, 160, 256, 512])},
+        "workload": {"requests": 10000, "concurrency": rng.choice([8, 16, 32]), "prompt_min": 16,
+                     "prompt_max": rng.choice([512, 1500]), "arrivals_per_window": 40.0, "seed": 1},
+        "shaping": {"staged_refresh_period": 4, "shared_prefix_tokens": tpp * 4},
+        "b200": {"payload": "lanes", "dtype": rng.choice(["bf16", "fp16"]), "kv_heads": kvh,
+                 "head_dim": 128, "q_heads": kvh * g, "attention_kernel": "tcgen05", "check": True},
+    }
+    if far:
+        cfg["far_view"].update({"cap": rng.choice([8, 32, 64, 96]), "sv_chunk": tpp * rng.choice([2, 4])})
+    d = kv.Driver(cfg, device=0)
+    d.run()
+    assert "tc" in d.device().attention_variant()
+    checked, bad, first = d.device_check()
+    assert bad == 0, first
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
