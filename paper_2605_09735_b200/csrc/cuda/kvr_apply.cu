@@ -9,6 +9,8 @@
 //
 // All loops are grid-stride with 16-byte vector accesses; grids are multiples
 // of the SM count and sized for the worst case so the step graph never changes.
+#include <type_traits>
+
 #include "kvr_internal.cuh"
 
 namespace kvr {
@@ -82,26 +84,34 @@ struct LaneTable {
     __device__ uint32_t operator()(uint64_t h) const { return v[h % 2001ull]; }
 };
 
+/// x % 2001 for x < 2^16: (x * 33538) >> 26 == x / 2001 for every 16-bit x
+/// (checked exhaustively), so the remainder is two IMADs and a shift.
+__device__ __forceinline__ uint32_t mod2001_u16(uint32_t x) { return x - ((x * 33538u) >> 26) * 2001u; }
+
+enum PayloadKind { kBytes = 0, kLanes16 = 1, kLanes32 = 2 };
+
 // 16 payload bytes starting at byte `b0` of token `tok` of session `sid`.
-__device__ inline int4 payload16(const DevCtx &c, const LaneTable &tab, uint32_t sid, uint64_t tok,
-                                 uint64_t b0) {
+template <int kKind>
+__device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab, uint32_t sid, uint64_t tok,
+                                          uint64_t b0) {
     const uint64_t base = c.seed ^ (uint64_t(sid) << 32) ^ (tok << 8);
     uint32_t w[4];
-    if (c.esz == 4) { // float lanes (reference pattern for elem_bytes == 4)
+    if constexpr (kKind == kLanes32) { // float lanes (reference pattern for elem_bytes == 4)
         const uint64_t lane0 = b0 / 4;
 #pragma unroll
         for (int i = 0; i < 4; ++i)
             w[i] = tab(splitmix64(base ^ (lane0 + i)));
-    } else if (c.payload_mode == KVR_PAYLOAD_LANES) {
+    } else if constexpr (kKind == kLanes16) {
         // 2-byte lanes (B200 extension, kvo_fill_token_lanes): one splitmix64 per
         // 4 lanes, lane value from its 16 bits mod 2001, rounded to fp16/bf16
-        const uint64_t g0 = (b0 / 2) >> 2; // 16 bytes = 8 lanes = 2 groups
+        const uint64_t key = base ^ 0x8000000000000000ull;
+        const uint64_t g0 = b0 >> 3; // 16 bytes = 8 lanes = 2 groups of 4
 #pragma unroll
         for (int gi = 0; gi < 2; ++gi) {
-            const uint64_t x = splitmix64(base ^ (g0 + gi) ^ 0x8000000000000000ull);
+            const uint64_t x = splitmix64(key ^ (g0 + gi));
             const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
-            w[2 * gi] = tab.v[(lo & 0xffffu) % 2001u] | (tab.v[(lo >> 16) % 2001u] << 16);
-            w[2 * gi + 1] = tab.v[(hi & 0xffffu) % 2001u] | (tab.v[(hi >> 16) % 2001u] << 16);
+            w[2 * gi] = tab.v[mod2001_u16(lo & 0xffffu)] | (tab.v[mod2001_u16(lo >> 16)] << 16);
+            w[2 * gi + 1] = tab.v[mod2001_u16(hi & 0xffffu)] | (tab.v[mod2001_u16(hi >> 16)] << 16);
         }
     } else { // reference byte pattern: one splitmix per byte
 #pragma unroll
@@ -118,7 +128,7 @@ __device__ inline int4 payload16(const DevCtx &c, const LaneTable &tab, uint32_t
 
 // `cold`: 0 = the hot write ops (rows read later in this step), 1 = the cold ops
 // (older prompt rows nothing in this step reads; launched after K-attn).
-template <uint32_t kPer> // chunks per thread per unit (independent generator chains)
+template <uint32_t kPer, int kKind> // chunks per thread per unit; payload kind
 __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
     __shared__ LaneTable tab;
     const kvr_step_header *h = hdr(c);
@@ -182,7 +192,7 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
 #pragma unroll
             for (uint32_t x = 0; x < kPer; ++x) {
                 const uint32_t q = (slice * kPer + x) * blockDim.x + q_base;
-                v[x] = q < chunks ? payload16(c, tab, op.session, tok, 16ull * q) : int4{};
+                v[x] = q < chunks ? payload16<kKind>(c, tab, op.session, tok, 16ull * q) : int4{};
             }
 #pragma unroll
             for (uint32_t x = 0; x < kPer; ++x) {
@@ -398,10 +408,20 @@ void launch_apply(const DevCtx &c, cudaStream_t s, int sms) {
 void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold) {
     // hot writes (few decode tokens + window rows): one chunk per thread for
     // spread; cold prompt rows: two chunks per thread for generator ILP
-    if (cold)
-        k_write<2><<<sms * 8, 256, 0, s>>>(c, 1);
+    const int kind = c.esz == 4 ? kLanes32 : c.payload_mode == KVR_PAYLOAD_LANES ? kLanes16 : kBytes;
+    auto go = [&](auto per, auto kk) {
+        k_write<decltype(per)::value, decltype(kk)::value><<<sms * 8, 256, 0, s>>>(c, cold);
+    };
+    using std::integral_constant;
+    if (kind == kLanes16)
+        cold ? go(integral_constant<uint32_t, 2>{}, integral_constant<int, kLanes16>{})
+             : go(integral_constant<uint32_t, 1>{}, integral_constant<int, kLanes16>{});
+    else if (kind == kLanes32)
+        cold ? go(integral_constant<uint32_t, 2>{}, integral_constant<int, kLanes32>{})
+             : go(integral_constant<uint32_t, 1>{}, integral_constant<int, kLanes32>{});
     else
-        k_write<1><<<sms * 8, 256, 0, s>>>(c, 0);
+        cold ? go(integral_constant<uint32_t, 2>{}, integral_constant<int, kBytes>{})
+             : go(integral_constant<uint32_t, 1>{}, integral_constant<int, kBytes>{});
 }
 
 void launch_query(const DevCtx &c, cudaStream_t s, int sms) { k_query<<<sms * 8, 256, 0, s>>>(c); }
