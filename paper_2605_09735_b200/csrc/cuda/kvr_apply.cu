@@ -23,14 +23,17 @@ __device__ inline void zero16(uint8_t *p) { *reinterpret_cast<int4 *>(p) = make_
 // K-apply: zero ops, then COW copies, then host blobs (three launches: a
 // recycled page may be a COW source in the same step).
 
+// Every op is spread over the whole grid (a zero run or a page copy can be
+// megabytes: one CTA per op left most SMs idle on span reservations).
 __global__ void k_zero(DevCtx c) {
     const kvr_step_header *h = hdr(c);
     const kvr_zero_op *ops = section<kvr_zero_op>(c, h->off_zero);
-    for (uint32_t i = blockIdx.x; i < h->n_zero; i += gridDim.x) {
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint32_t i = 0; i < h->n_zero; ++i) {
         const kvr_zero_op op = ops[i];
         uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot_begin) * c.token_bytes;
         const uint64_t n16 = uint64_t(op.slot_count) * c.token_bytes / 16;
-        for (uint64_t k = threadIdx.x; k < n16; k += blockDim.x)
+        for (uint64_t k = tid; k < n16; k += stride)
             zero16(dst + 16 * k);
     }
 }
@@ -38,10 +41,11 @@ __global__ void k_zero(DevCtx c) {
 __global__ void k_cow(DevCtx c) {
     const kvr_step_header *h = hdr(c);
     const kvr_cow_op *ops = section<kvr_cow_op>(c, h->off_cow);
-    for (uint32_t i = blockIdx.x; i < h->n_cow; i += gridDim.x) {
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint32_t i = 0; i < h->n_cow; ++i) {
         const int4 *src = reinterpret_cast<const int4 *>(c.arena + uint64_t(ops[i].src) * c.page_bytes);
         int4 *dst = reinterpret_cast<int4 *>(c.arena + uint64_t(ops[i].dst) * c.page_bytes);
-        for (uint64_t k = threadIdx.x; k < c.page_bytes / 16; k += blockDim.x)
+        for (uint64_t k = tid; k < c.page_bytes / 16; k += stride)
             dst[k] = src[k];
     }
 }
