@@ -542,14 +542,24 @@ struct ScenarioDriver::Impl {
             std::vector<float> chunk;
             if (!dev)
                 chunk.resize(size_t(fv.chunk_tokens) * lanes);
+            // Same per-token additions as the reference (bit-identical sum); the
+            // entry walk and the per-block score lookup are cached across tokens.
+            const ViewEntry *e = nullptr;
+            BlockId scored = kInvalidBlock;
+            double block_score = 0.0;
             for (uint64_t tok = lo; tok < hi; ++tok) {
-                const ViewEntry *e = view.find(tok);
+                if (!e || tok < e->tokens.begin || tok >= e->tokens.end)
+                    e = view.find(tok);
                 if (!e)
                     raise(Errc::unmapped_range, "chunk source token unmapped");
                 if (!dev)
                     pager->read_slots(e->block, e->slot_begin + uint32_t(tok - e->tokens.begin), 1,
                                       reinterpret_cast<std::byte *>(chunk.data() + (tok - lo) * lanes));
-                score += tracker->score(e->block, t);
+                if (e->block != scored) {
+                    scored = e->block;
+                    block_score = tracker->score(scored, t);
+                }
+                score += block_score;
             }
             r.chunk_scores.push_back(score);
             if (r.n_summaries == r.summary_room) {
