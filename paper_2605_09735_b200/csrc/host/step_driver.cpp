@@ -11,6 +11,8 @@
 //   * every step ends in DeviceStep::launch — one committed descriptor, one
 //     H2D copy, one graph replay — instead of the cost-model stub.
 #include <algorithm>
+#include <chrono>
+#include <cstdlib>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -594,7 +596,33 @@ struct ScenarioDriver::Impl {
     }
 
     // ---- the step (scenario.cpp:450-682) ----
+    // Host time per step section (KVR_HOST_PROFILE=1: printed when the driver ends).
+    struct HostProfile {
+        bool on = std::getenv("KVR_HOST_PROFILE") != nullptr;
+        double ms[8] = {};
+        std::chrono::steady_clock::time_point t0;
+        void start() {
+            if (on)
+                t0 = std::chrono::steady_clock::now();
+        }
+        void lap(int i) {
+            if (!on)
+                return;
+            const auto t1 = std::chrono::steady_clock::now();
+            ms[i] += std::chrono::duration<double, std::milli>(t1 - t0).count();
+            t0 = t1;
+        }
+        ~HostProfile() {
+            if (on)
+                std::fprintf(stderr,
+                             "host ms: retire %.1f admit %.1f sessions %.1f placement %.1f commit %.1f "
+                             "stage %.1f device %.1f trace/engine %.1f\n",
+                             ms[0], ms[1], ms[2], ms[3], ms[4], ms[5], ms[6], ms[7]);
+        }
+    } prof;
+
     StepRecord step() {
+        prof.start();
         // Shift: retire sessions that finished last step (swap-remove).
         for (size_t i = 0; i < live.size();) {
             if (!live[i].eos) {
@@ -628,7 +656,9 @@ struct ScenarioDriver::Impl {
         }
         for (Req &r : live)
             r.admitted_now = false;
+        prof.lap(0);
         admissions();
+        prof.lap(1);
 
         std::vector<StageNeed> far_needs;
         std::vector<std::pair<BlockId, double>> obs;
@@ -675,6 +705,7 @@ struct ScenarioDriver::Impl {
             }
         }
 
+        prof.lap(2);
         // Placement: rank staging candidates and take the cold set.
         std::vector<size_t> refresh;
         const uint32_t period = cfg.pager_enabled ? cfg.staged_refresh_period
@@ -712,6 +743,7 @@ struct ScenarioDriver::Impl {
                 pager->trim(sid, ranges);
         }
 
+        prof.lap(3);
         // One frame commit per live session.
         uint64_t commits = 0;
         if (cfg.pager_enabled) {
@@ -727,6 +759,7 @@ struct ScenarioDriver::Impl {
             commits = order.size();
         }
 
+        prof.lap(4);
         // Stage needs.
         std::vector<StageNeed> needs;
         std::vector<std::vector<uint64_t>> need_first; // device: logical first token per span
@@ -809,16 +842,19 @@ struct ScenarioDriver::Impl {
             arena.free_pages = 0;
             arena.live_pages = static_arena_pages;
         }
+        prof.lap(5);
         if (dev) { // publish first: the trace then reads the bytes this step produced
             device_step(needs, need_first, now);
             if (cfg.b200.check)
                 check_device_scan(trains);
         }
+        prof.lap(6);
         if (cfg.b200.trace)
             trace_step(trains);
         StepRecord rec = engine.execute_step(t, trains, cfg.compiled_width(), uint32_t(order.size()),
                                              commits, emitted, arena);
         ++t;
+        prof.lap(7);
         return rec;
     }
 
