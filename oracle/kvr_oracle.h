@@ -35,9 +35,11 @@ void kvo_fill_token_payload(uint64_t seed, uint32_t session, uint64_t token, uin
 void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint64_t lanes,
                           int elem_kind, void *out);
 
-/* Synthetic decode query for (seed, session, step, layer, q_head): hd floats
- * ((h % 2001) - 1000) / 1000 with h = splitmix64(seed ^ 0x51<<56 ^ session<<32
- * ^ step<<20 ^ layer<<12 ^ head<<8 ^ d)). Rounded to elem_kind like K/V. */
+/* Synthetic decode query for (seed, session, step, layer, q_head): hd floats,
+ * lane d = ((v % 2001) - 1000) / 1000 with v the 16-bit field d & 3 of
+ * h = splitmix64(seed ^ 0x51<<56 ^ session<<32 ^ step<<20 ^ layer<<12 ^ head<<8
+ * ^ (d >> 2)) — one hash per 4 lanes, like the 2-byte KV lanes. Rounded to
+ * elem_kind like K/V. (A B200-side synthetic input: the reference has no query.) */
 void kvo_fill_query(uint64_t seed, uint32_t session, uint64_t step, uint32_t layer,
                     uint32_t head, uint32_t head_dim, int elem_kind, float *out);
 

@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
 // Decode queries for live slots: [slot][L][Hq][hd], rounded to the KV element
 // type (kvo_fill_query in the oracle). One CTA per (slot, layer).
 __global__ void __launch_bounds__(256) k_query(DevCtx c) {
-    __shared__ float val[2001]; // ((k - 1000) / 1000) rounded to the KV type, k = h % 2001
+    __shared__ float val[2001]; // ((k - 1000) / 1000) rounded to the KV type, k = v % 2001
     for (uint32_t i = threadIdx.x; i < 2001; i += blockDim.x) {
         float v = float(int(i) - 1000) / 1000.0f;
         if (c.elem_kind == KVR_ELEM_F16)
@@ -239,11 +239,13 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
             continue;
         const uint64_t base = c.seed ^ (0x51ull << 56) ^ (uint64_t(slots[s].session) << 32) ^
                               (h->step << 20) ^ (uint64_t(l) << 12);
-        float *q = c.q + uint64_t(sl) * per_layer;
+        float4 *q = reinterpret_cast<float4 *>(c.q + uint64_t(sl) * per_layer);
         const uint32_t hd_shift = __ffs(c.hd) - 1; // head_dim is a power of two (32/64/128)
-        for (uint32_t i = threadIdx.x; i < per_layer; i += blockDim.x) {
-            const uint32_t head = i >> hd_shift, d = i & (c.hd - 1);
-            q[i] = val[splitmix64(base ^ (uint64_t(head) << 8) ^ d) % 2001ull];
+        for (uint32_t i = threadIdx.x; i < per_layer / 4; i += blockDim.x) { // 4 lanes per hash
+            const uint32_t head = (4 * i) >> hd_shift, d4 = i & ((c.hd >> 2) - 1);
+            const uint64_t x = splitmix64(base ^ (uint64_t(head) << 8) ^ d4);
+            q[i] = make_float4(val[mod2001_u16(uint32_t(x) & 0xffffu)], val[mod2001_u16(uint32_t(x) >> 16)],
+                               val[mod2001_u16(uint32_t(x >> 32) & 0xffffu)], val[mod2001_u16(uint32_t(x >> 48))]);
         }
     }
 }
