@@ -63,11 +63,13 @@ typedef struct kvr_step_header {
     uint32_t n_cold;        /* write ops are [hot ... | cold ... | far jobs ...]; cold ops
                                touch rows no kernel of this step reads and run after
                                the attention */
-    uint32_t pad_h;
+    uint32_t n_presum;      /* far chunks summarised while their prompt rows are written */
     uint64_t write_tokens;  /* sum of kvr_write_op.count over hot source-0 writes */
     uint64_t write_tokens_cold; /* ... over cold source-0 writes */
     uint64_t off_zero, off_cow, off_edit, off_write, off_blob_ops, off_blob, off_need, off_span,
         off_prime, off_far_ids, off_slots;
+    uint64_t off_presum, off_presum_runs;
+    uint32_t n_presum_runs, pad_h;
     uint64_t total_bytes;
 } kvr_step_header;
 
@@ -81,7 +83,9 @@ typedef struct kvr_edit_op {
 } kvr_edit_op;
 /* payload generated in place: source 0 = synthetic token payload of
  * (session, token..token+count); source 1 = far summary of chunk tokens
- * [aux, aux + chunk_tokens) of `dev_slot` written to (block, slot). */
+ * [aux, aux + chunk_tokens) of `dev_slot` written to (block, slot); source 2 =
+ * the same summary, already computed by K-presum into the stash row
+ * (dev_slot, aux / chunk_tokens), copied to (block, slot). */
 typedef struct kvr_write_op {
     uint64_t token;
     uint64_t aux;
@@ -90,6 +94,13 @@ typedef struct kvr_write_op {
     uint32_t dev_slot;      /* KVR_NO_SLOT: arena only */
     uint32_t source;
 } kvr_write_op;
+/* K-presum: a far-view chunk whose prompt rows are all written this step, by one
+ * session, is generated column by column in token order (runs [run_begin,
+ * run_begin + run_count) of the run list) and its mean kept in the stash row
+ * (dev_slot, chunk): the far job a step later copies it instead of re-reading the
+ * chunk_tokens rows (bit-identical: the same double sums in the same order). */
+typedef struct kvr_presum_op { uint32_t session, dev_slot, chunk, run_begin, run_count, pad; } kvr_presum_op;
+typedef struct kvr_presum_run { uint64_t token; uint32_t block, slot, count, pad; } kvr_presum_run;
 /* host payload bytes (Pager::write_tokens) carried in the descriptor blob */
 typedef struct kvr_blob_op {
     uint64_t blob_offset;

@@ -274,6 +274,23 @@ template <int E> __device__ inline void add_chunk(const DevCtx &c, int4 v, doubl
     }
 }
 
+/// float(acc * (1/count)) per lane, rounded to the element type (far_view.cpp:36-46).
+template <int E> __device__ inline void store_mean(const DevCtx &c, uint8_t *dst, const double (&acc)[16 / E]) {
+    const double inv = 1.0 / double(c.chunk_tokens);
+    if constexpr (E == 4) {
+        *reinterpret_cast<float4 *>(dst) = make_float4(float(acc[0] * inv), float(acc[1] * inv),
+                                                       float(acc[2] * inv), float(acc[3] * inv));
+    } else {
+        uint16_t o[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const float m = float(acc[i] * inv);
+            o[i] = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(m) : f2h_bits(m);
+        }
+        *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(o);
+    }
+}
+
 /// One CTA per (far job, 4 KiB column block): every thread streams one 16-byte
 /// column of the chunk's rows (row offsets staged in shared memory).
 template <int E> __device__ void far_columns(const DevCtx &c, const kvr_write_op &op, uint64_t col,
@@ -297,20 +314,7 @@ template <int E> __device__ void far_columns(const DevCtx &c, const kvr_write_op
     for (; k < n_rows; ++k)
         if (rows[k] != ~0ull)
             add_chunk<E>(c, __ldcs(reinterpret_cast<const int4 *>(c.arena + rows[k] + col)), acc);
-    uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot) * c.token_bytes + col;
-    const double inv = 1.0 / double(c.chunk_tokens);
-    if constexpr (E == 4) {
-        *reinterpret_cast<float4 *>(dst) = make_float4(float(acc[0] * inv), float(acc[1] * inv),
-                                                       float(acc[2] * inv), float(acc[3] * inv));
-    } else {
-        uint16_t o[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const float m = float(acc[i] * inv);
-            o[i] = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(m) : f2h_bits(m);
-        }
-        *reinterpret_cast<uint4 *>(dst) = *reinterpret_cast<const uint4 *>(o);
-    }
+    store_mean<E>(c, c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot) * c.token_bytes + col, acc);
 }
 
 constexpr uint32_t kFarRows = 512; // chunk rows staged in shared memory
@@ -327,6 +331,17 @@ __global__ void __launch_bounds__(256) k_far(DevCtx c) {
     for (uint64_t u = blockIdx.x; u < work; u += gridDim.x) {
         const kvr_write_op op = ops[u / col_blocks];
         __syncthreads(); // rows[] of the previous unit consumed
+        if (op.source == 2) { // summarised by K-presum when its rows were written: copy
+            const uint64_t col = (u % col_blocks) * blockDim.x + threadIdx.x;
+            if (col < cols) {
+                const uint64_t chunk = op.aux / c.chunk_tokens;
+                const int4 v = *reinterpret_cast<const int4 *>(
+                    c.stash + (uint64_t(op.dev_slot) * c.max_chunks + chunk) * c.token_bytes + 16 * col);
+                *reinterpret_cast<int4 *>(c.arena + uint64_t(op.block) * c.page_bytes +
+                                          uint64_t(op.slot) * c.token_bytes + 16 * col) = v;
+            }
+            continue;
+        }
         if (op.source != 1)
             continue;
         const uint32_t *tm = c.tmap + uint64_t(op.dev_slot) * c.max_tokens;
@@ -343,6 +358,47 @@ __global__ void __launch_bounds__(256) k_far(DevCtx c) {
             far_columns<4>(c, op, col * 16, rows, n_rows);
         else
             far_columns<2>(c, op, col * 16, rows, n_rows);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K-presum: prompt rows of whole far-view chunks, generated column by column in
+// token order (one CTA per (chunk, 4 KiB column block)), written to the arena and
+// summed on the fly — the far job of the next step copies the mean from the
+// stash instead of re-reading chunk_tokens rows (same double sums, same order).
+
+template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c) {
+    __shared__ LaneTable tab;
+    const kvr_step_header *h = hdr(c);
+    if (h->n_presum == 0)
+        return;
+    tab.fill(c);
+    constexpr int E = kKind == kLanes32 ? 4 : 2;
+    const kvr_presum_op *ops = section<kvr_presum_op>(c, h->off_presum);
+    const kvr_presum_run *runs = section<kvr_presum_run>(c, h->off_presum_runs);
+    const uint64_t cols = c.token_bytes / 16;
+    const uint64_t col_blocks = (cols + blockDim.x - 1) / blockDim.x;
+    const uint64_t work = uint64_t(h->n_presum) * col_blocks;
+    for (uint64_t u = blockIdx.x; u < work; u += gridDim.x) {
+        const kvr_presum_op op = ops[u / col_blocks];
+        const uint64_t col = (u % col_blocks) * blockDim.x + threadIdx.x;
+        if (col >= cols)
+            continue;
+        double acc[16 / E];
+#pragma unroll
+        for (int i = 0; i < 16 / E; ++i)
+            acc[i] = 0.0;
+        for (uint32_t r = op.run_begin; r < op.run_begin + op.run_count; ++r) {
+            const kvr_presum_run run = runs[r];
+            uint8_t *dst = c.arena + uint64_t(run.block) * c.page_bytes + uint64_t(run.slot) * c.token_bytes + 16 * col;
+            for (uint32_t k = 0; k < run.count; ++k) {
+                const int4 v = payload16<kKind>(c, tab, op.session, run.token + k, 16 * col);
+                *reinterpret_cast<int4 *>(dst + uint64_t(k) * c.token_bytes) = v;
+                add_chunk<E>(c, v, acc);
+            }
+        }
+        store_mean<E>(c, c.stash + (uint64_t(op.dev_slot) * c.max_chunks + op.chunk) * c.token_bytes + 16 * col,
+                      acc);
     }
 }
 
@@ -408,6 +464,17 @@ void launch_apply(const DevCtx &c, cudaStream_t s, int sms) {
     k_zero<<<sms * 4, 256, 0, s>>>(c);
     k_cow<<<sms * 4, 256, 0, s>>>(c);
     k_blob<<<sms, 256, 0, s>>>(c);
+}
+
+void launch_presum(const DevCtx &c, cudaStream_t s, int sms) {
+    if (!c.stash)
+        return;
+    if (c.esz == 4)
+        k_presum<kLanes32><<<sms * 4, 256, 0, s>>>(c);
+    else if (c.payload_mode == KVR_PAYLOAD_LANES)
+        k_presum<kLanes16><<<sms * 4, 256, 0, s>>>(c);
+    else
+        k_presum<kBytes><<<sms * 4, 256, 0, s>>>(c);
 }
 
 // cold: 0 hot writes, 1 cold writes (both over the whole GPU)

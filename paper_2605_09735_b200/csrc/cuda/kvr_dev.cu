@@ -128,6 +128,7 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     // (one CTA per SM on a forked branch) slowed the attention by more than the
     // overlap saved, so the step runs them after it with the whole GPU.
     launch_write(c, s, d->sms, 1);
+    launch_presum(c, s, d->sms);
     launch_stamp(c, s);
     mark(7);
 }
@@ -222,6 +223,9 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         const uint64_t far_elems = uint64_t(c.n_slots) * c.L * c.max_chunks * c.row_elems;
         c.far = static_cast<uint8_t *>(dalloc(d.get(), far_elems * c.esz, "far"));
         ck(cudaMemsetAsync(c.far, 0, far_elems * c.esz, d->stream), "far zero");
+        c.stash = c.far_cap ? static_cast<uint8_t *>(dalloc(d.get(), uint64_t(c.n_slots) * c.max_chunks * c.token_bytes,
+                                                            "presum stash"))
+                            : nullptr;
         const uint64_t qn = uint64_t(c.n_slots) * c.L * c.Hq * c.hd;
         c.q = static_cast<float *>(dalloc(d.get(), qn * 4, "q"));
         c.out = static_cast<float *>(dalloc(d.get(), qn * 4, "out"));

@@ -42,6 +42,7 @@ struct DevCtx {
     uint32_t *tmap;   // [slot][max_tokens]
     uint32_t *smap;   // [slot][smap_cap]
     uint8_t *far;     // [slot][L][max_chunks][row_elems] elements
+    uint8_t *stash;   // [slot][max_chunks][token_bytes]: K-presum chunk means (far view only)
     float *q;         // [slot][L][Hq][hd]
     float *out;       // [slot][L][Hq][hd]
     const uint8_t *desc; // device copy of the step descriptor
@@ -85,7 +86,8 @@ void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blo
 void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold); // generated payloads
 void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
 void launch_far(const DevCtx &c, cudaStream_t s, int sms);
-void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp     // far summaries
+void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp
+void launch_presum(const DevCtx &c, cudaStream_t s, int sms); // prompt rows + their far chunk means     // far summaries
 void launch_map(const DevCtx &c, cudaStream_t s, int sms);     // page-table edits
 void launch_prime(const DevCtx &c, cudaStream_t s, int sms);   // window priming
 void launch_scan(const DevCtx &c, cudaStream_t s);             // stage + reduce

@@ -56,6 +56,82 @@ struct DeviceStep::Impl {
     std::vector<uint32_t> far_ids;
     std::vector<kvr_slot_state> slots;
     std::vector<std::vector<uint64_t>> far_shown; // per slot, as of the last launch
+    // K-presum: chunks summarised while their prompt rows were written (far view)
+    std::vector<kvr_presum_op> presum_ops;
+    std::vector<kvr_presum_run> presum_runs;
+    std::unordered_set<uint64_t> presummed; // session << 32 | chunk, stash row valid
+    static uint64_t presum_key(SessionId s, uint64_t chunk) { return uint64_t(s) << 32 | chunk; }
+
+    /// Move whole far-view chunks out of this step's cold writes into K-presum ops:
+    /// a chunk qualifies when its chunk_tokens rows are all cold rows of one bound
+    /// session written this step (a prompt), so K-presum can generate and sum them.
+    void extract_presums(std::vector<kvr_write_op> &cold) {
+        presum_ops.clear();
+        presum_runs.clear();
+        if (!g.far_cap || !g.chunk_tokens || cold.empty())
+            return;
+        const uint64_t ct = g.chunk_tokens;
+        std::vector<size_t> idx(cold.size());
+        for (size_t i = 0; i < idx.size(); ++i)
+            idx[i] = i;
+        std::sort(idx.begin(), idx.end(), [&](size_t a, size_t b) {
+            return cold[a].session != cold[b].session ? cold[a].session < cold[b].session
+                                                      : cold[a].token < cold[b].token;
+        });
+        std::vector<kvr_write_op> keep;
+        // pieces of the current chunk (all from one session, contiguous tokens)
+        std::vector<kvr_write_op> cur;
+        uint64_t cur_chunk = ~0ull, cur_next = 0;
+        SessionId cur_sess = 0;
+        auto flush_chunk = [&]() {
+            uint64_t n = 0;
+            for (const kvr_write_op &w : cur)
+                n += w.count;
+            if (n == ct && cur.front().dev_slot != KVR_NO_SLOT && cur.front().token == cur_chunk * ct) {
+                kvr_presum_op op{};
+                op.session = cur_sess;
+                op.dev_slot = cur.front().dev_slot;
+                op.chunk = uint32_t(cur_chunk);
+                op.run_begin = uint32_t(presum_runs.size());
+                op.run_count = uint32_t(cur.size());
+                for (const kvr_write_op &w : cur)
+                    presum_runs.push_back({w.token, w.block, w.slot, w.count, 0});
+                presum_ops.push_back(op);
+                presummed.insert(presum_key(cur_sess, cur_chunk));
+            } else {
+                keep.insert(keep.end(), cur.begin(), cur.end());
+            }
+            cur.clear();
+            cur_chunk = ~0ull;
+        };
+        for (size_t i : idx) {
+            kvr_write_op w = cold[i];
+            if (w.source != 0 || w.dev_slot == KVR_NO_SLOT || w.dev_slot >= g.n_slots) {
+                keep.push_back(w);
+                continue;
+            }
+            while (w.count) { // split at chunk boundaries
+                const uint64_t c = w.token / ct;
+                const uint32_t n = uint32_t(std::min<uint64_t>(w.count, (c + 1) * ct - w.token));
+                kvr_write_op piece = w;
+                piece.count = n;
+                if (c != cur_chunk || w.session != cur_sess || w.token != cur_next) {
+                    if (!cur.empty())
+                        flush_chunk();
+                    cur_chunk = c;
+                    cur_sess = w.session;
+                }
+                cur.push_back(piece);
+                cur_next = w.token + n;
+                w.token += n;
+                w.slot += n;
+                w.count -= n;
+            }
+        }
+        if (!cur.empty())
+            flush_chunk();
+        cold.swap(keep);
+    }
     /// Cold prefill rows not yet written (prefill budget). Lookups by page and by
     /// session are O(1); removed entries are marked dead (count 0) and skipped.
     struct Deferred {
@@ -222,6 +298,12 @@ struct DeviceStep::Impl {
         } else {
             hot = writes;
         }
+        if (with_step)
+            extract_presums(cold);
+        else {
+            presum_ops.clear();
+            presum_runs.clear();
+        }
         if (with_step && prefill_budget) {
             // Prefill budget: cold rows join the deferred queue, which drains at
             // most `prefill_budget` tokens per step; queued rows read this step
@@ -283,6 +365,10 @@ struct DeviceStep::Impl {
         h.n_far_ids = uint32_t(fi.size());
         h.off_far_ids = place(fi.size() * sizeof(uint32_t));
         h.off_slots = place(slots.size() * sizeof(kvr_slot_state));
+        h.n_presum = uint32_t(presum_ops.size());
+        h.off_presum = place(presum_ops.size() * sizeof(kvr_presum_op));
+        h.n_presum_runs = uint32_t(presum_runs.size());
+        h.off_presum_runs = place(presum_runs.size() * sizeof(kvr_presum_run));
         h.total_bytes = off;
         if (off > g.max_desc_bytes)
             throw std::runtime_error("step descriptor exceeds max_desc_bytes");
@@ -303,6 +389,8 @@ struct DeviceStep::Impl {
         put(h.off_prime, primes.data(), primes.size() * sizeof(kvr_prime_op));
         put(h.off_far_ids, fi.data(), fi.size() * sizeof(uint32_t));
         put(h.off_slots, slots.data(), slots.size() * sizeof(kvr_slot_state));
+        put(h.off_presum, presum_ops.data(), presum_ops.size() * sizeof(kvr_presum_op));
+        put(h.off_presum_runs, presum_runs.data(), presum_runs.size() * sizeof(kvr_presum_run));
         return off;
     }
 
@@ -426,9 +514,14 @@ struct DeviceStep::Impl {
             op.session = w.session;
             op.dev_slot = slot;
             op.source = 1;
+            if (g.chunk_tokens && presummed.erase(presum_key(w.session, w.aux / g.chunk_tokens)))
+                op.source = 2; // K-presum computed this mean when the rows were written
             far_jobs.push_back(op);
             return;
         }
+        if (!presummed.empty() && g.chunk_tokens) // rewritten rows: the stashed mean is stale
+            for (uint64_t c = w.token / g.chunk_tokens; c * g.chunk_tokens < w.token + w.count; ++c)
+                presummed.erase(presum_key(w.session, c));
         note_slots(w.block, w.slot, w.count);
         if (!writes.empty()) { // coalesce consecutive tokens of one block
             kvr_write_op &b = writes.back();
@@ -514,7 +607,12 @@ void DeviceStep::bind(SessionId sid, uint32_t slot) {
         throw std::runtime_error("device slot out of range");
     impl_->bound[sid] = slot;
 }
-void DeviceStep::unbind(SessionId sid) { impl_->bound.erase(sid); }
+void DeviceStep::unbind(SessionId sid) {
+    impl_->bound.erase(sid);
+    auto &ps = impl_->presummed; // its stash rows may be reused by the slot's next session
+    for (auto it = ps.begin(); it != ps.end();)
+        it = (*it >> 32) == sid ? ps.erase(it) : std::next(it);
+}
 
 void DeviceStep::slot_state(uint32_t slot, SessionId sid, uint64_t written, bool live) {
     kvr_slot_state &s = impl_->slots.at(slot);
