@@ -346,7 +346,7 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
         ck(cudaEventRecord(d->ev_stop[k], d->stream), "event");
         d->launched[k] = h->step;
         d->in_flight[k] = true;
-        d->pending_write_tokens[k] = h->write_tokens + h->write_tokens_cold;
+        d->pending_write_tokens[k] = h->write_tokens + h->write_tokens_cold + uint64_t(h->n_presum) * c.chunk_tokens;
     });
 }
 
