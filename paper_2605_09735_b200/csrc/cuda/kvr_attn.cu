@@ -434,13 +434,16 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
     }
     // kv heads per CTA: largest G <= 4 dividing Hkv with a <= 64 KiB stage
     const size_t row = size_t(c.hd) * c.esz;
+    // (measured on C2: G = 4 / 2 / 1 -> 2.48 / 3.36 / 6.62 ms: consumer warps matter)
     for (uint32_t g : {4u, 2u, 1u})
         if (c.Hkv % g == 0 && 2 * kTile * g * row <= (64u << 10)) {
             p->G = g;
             break;
         }
     const size_t stage = 2 * kTile * p->G * row;
-    p->stages = stage * 3 <= (200u << 10) ? 3 : 2;
+    p->stages = uint32_t(std::min<size_t>(8, (192u << 10) / stage)); // deeper rings for smaller stages
+    if (p->stages < 2)
+        p->stages = 2;
     p->smem = p->stages * stage + size_t(kMaxG) * 32 * c.group * (2 + c.hd / 32) * 4 +
               2 * p->stages * 8 + 16;
     p->grid = uint32_t(sms);
