@@ -6,14 +6,15 @@
 // masked. Definition: attend() of far_view.cpp:113-155 per (layer, q-head)
 // with GQA q-head j -> kv-head j / group, fp32 accumulation (1e-3 rel. bound).
 //
-// Per CTA (persistent): one producer warp streams K and V half-tiles (16 rows x G
-// heads) out of the ring with 4-D TMA tensor loads (cp.async.bulk.tensor,
-// mbarrier completion) into a 3-stage shared-memory ring, skipping halves with no
-// live row; 2*G consumer warps, a pair per kv head, take 16 rows each. QK^T: lane
-// <-> head dims with q in registers, the 16 per-row partial dot products are
-// reduce-scattered by a halving shuffle butterfly (lane l ends with row l >> 1).
-// PV: lane <-> head dims, probabilities broadcast by shuffles. Online softmax in
-// base 2; the pair merges its states through shared memory at item end. At g = 1
+// Per CTA (persistent): one producer warp streams K and V tiles (32 rows x G heads)
+// out of the ring with 4-D TMA tensor loads (cp.async.bulk.tensor, mbarrier
+// completion) into a shared-memory ring (192 KiB of stages) — at the window edges
+// as 8-row boxes, skipping those with no live row; WPH*G consumer warps, WPH per kv head (4 for q-groups
+// <= 2, else 2), take 32/WPH rows of each tile. QK^T: lane <-> head dims with q in
+// registers, the per-row partial dot products are reduce-scattered by a halving
+// shuffle butterfly. PV: lane <-> head dims, probabilities broadcast by shuffles.
+// Online softmax in base 2; a head's warps merge their states through shared
+// memory at item end. At g = 1
 // this is a warp GEMV at the HBM roofline; GQA groups g >= 4 with head_dim 128 use
 // the tcgen05 kernel in kvr_attn_tc.cu.
 #include <algorithm>
@@ -27,7 +28,7 @@ namespace kvr {
 namespace {
 
 constexpr int kTile = 32; // tokens per tile (one per lane)
-constexpr int kMaxG = 4;  // kv heads per CTA (a pair of consumer warps each)
+constexpr int kMaxG = 4;  // kv heads per CTA
 
 __device__ inline uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ inline void mbar_init(uint64_t *bar, uint32_t count) {
@@ -114,15 +115,21 @@ template <typename T, int N> __device__ inline void load_dims(const T *p, float 
     }
 }
 
-constexpr int kHalf = 16; // tokens per consumer warp per tile
+constexpr int kEdge = 8; // rows per TMA box at window edges (quarters with no live row are skipped)
 
-/// Online-softmax state of one consumer warp for QG q-heads sharing one kv head.
-/// QK^T: lane <-> head dims (q kept in registers), the 16 per-token partial dot
-/// products are reduce-scattered across the warp by a halving butterfly so lane
-/// l ends with the score of token l >> 1. PV: lane <-> head dims, the token
-/// probabilities are broadcast with shuffles.
-template <typename T, int HD, int QG> struct Attn {
+/// Consumer warps per kv head: 4 (8 rows each) for small q-groups, where the warp
+/// count — not registers — limits latency hiding; 2 (16 rows each) otherwise.
+template <int QG> constexpr int warps_per_head() { return QG <= 2 ? 4 : 2; }
+
+/// Online-softmax state of one consumer warp for QG q-heads sharing one kv head,
+/// over R rows of each tile. QK^T: lane <-> head dims (q kept in registers), the R
+/// per-row partial dot products are reduce-scattered across the warp by a halving
+/// butterfly so lane l ends with the score of row l >> kShift. PV: lane <-> head
+/// dims, the row probabilities are broadcast with shuffles.
+template <typename T, int HD, int QG, int R> struct Attn {
     static constexpr int DPL = HD / 32;
+    static constexpr int kShift = R == 16 ? 1 : 2; // lanes per row after the butterfly: 2 / 4
+    static_assert(R == 16 || R == 8, "rows per warp");
     float q[QG][DPL];
     float m[QG], lsum[QG], acc[QG][DPL];
 
@@ -140,14 +147,14 @@ template <typename T, int HD, int QG> struct Attn {
         }
     }
 
-    // 16 rows: row(r) -> K row pointer (V row = + v_off elements); valid bit r of `mask`.
-    // FULL: all 16 rows valid (the common case) — no per-row predicates at all.
+    // R rows: row(r) -> K row pointer (V row = + v_off elements); valid bit r of `mask`.
+    // FULL: all R rows valid (the common case) — no per-row predicates at all.
     template <bool FULL, typename RowFn>
     __device__ void block(RowFn row, uint32_t v_off, uint32_t mask, float scale_log2) {
         const int lane = threadIdx.x & 31;
-        float part[QG][kHalf];
+        float part[QG][R];
 #pragma unroll
-        for (int r = 0; r < kHalf; ++r) {
+        for (int r = 0; r < R; ++r) {
             float k[DPL];
             if (FULL || (mask >> r & 1u)) {
                 load_dims<T, DPL>(row(r) + DPL * lane, k);
@@ -165,12 +172,13 @@ template <typename T, int HD, int QG> struct Attn {
                 part[g][r] = a;
             }
         }
-        // halving butterfly: 16 values -> 1 per lane (token lane >> 1)
+        // halving butterfly: R values -> 1 per lane (row lane >> kShift), then the
+        // remaining kShift lane bits are summed
         float s[QG];
 #pragma unroll
         for (int g = 0; g < QG; ++g) {
 #pragma unroll
-            for (int w = kHalf / 2, bit = 16; w >= 1; w >>= 1, bit >>= 1) {
+            for (int w = R / 2, bit = 16; w >= 1; w >>= 1, bit >>= 1) {
                 const bool hi = lane & bit;
 #pragma unroll
                 for (int j = 0; j < w; ++j) {
@@ -179,9 +187,14 @@ template <typename T, int HD, int QG> struct Attn {
                     part[g][j] = keep + __shfl_xor_sync(0xffffffffu, send, bit);
                 }
             }
-            s[g] = (part[g][0] + __shfl_xor_sync(0xffffffffu, part[g][0], 1)) * scale_log2;
+            float v = part[g][0];
+#pragma unroll
+            for (int b = 1 << (kShift - 1); b >= 1; b >>= 1)
+                v += __shfl_xor_sync(0xffffffffu, v, b);
+            s[g] = v * scale_log2;
         }
-        const bool valid = FULL || (mask >> (lane >> 1) & 1u);
+        const bool valid = FULL || (mask >> (lane >> kShift) & 1u);
+        const bool leader = (lane & ((1 << kShift) - 1)) == 0; // one lane per row sums l
         float p[QG];
 #pragma unroll
         for (int g = 0; g < QG; ++g) {
@@ -189,21 +202,21 @@ template <typename T, int HD, int QG> struct Attn {
             const float mn = fmaxf(m[g], warp_max(sv));
             const float alpha = mn == -INFINITY ? 1.f : exp2f(m[g] - mn);
             p[g] = valid ? exp2f(sv - mn) : 0.f;
-            lsum[g] = lsum[g] * alpha + ((lane & 1) ? 0.f : p[g]);
+            lsum[g] = lsum[g] * alpha + (leader ? p[g] : 0.f);
             m[g] = mn;
 #pragma unroll
             for (int i = 0; i < DPL; ++i)
                 acc[g][i] *= alpha;
         }
 #pragma unroll
-        for (int r = 0; r < kHalf; ++r) {
+        for (int r = 0; r < R; ++r) {
             if (!FULL && !(mask >> r & 1u))
                 continue; // warp-uniform; masked rows may hold non-finite garbage
             float v[DPL];
             load_dims<T, DPL>(row(r) + v_off + DPL * lane, v);
 #pragma unroll
             for (int g = 0; g < QG; ++g) {
-                const float pr = __shfl_sync(0xffffffffu, p[g], 2 * r);
+                const float pr = __shfl_sync(0xffffffffu, p[g], r << kShift);
 #pragma unroll
                 for (int i = 0; i < DPL; ++i)
                     acc[g][i] = fmaf(pr, v[i], acc[g][i]);
@@ -213,15 +226,18 @@ template <typename T, int HD, int QG> struct Attn {
 };
 
 template <typename T, int HD, int QG>
-__global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
-    k_attn(DevCtx c, const __grid_constant__ CUtensorMap ring_map, uint32_t G, uint32_t stages) {
-    using A = Attn<T, HD, QG>;
+__global__ void __launch_bounds__(32 * (warps_per_head<QG>() * kMaxG + 1), 1)
+    k_attn(DevCtx c, const __grid_constant__ CUtensorMap tile_map, const __grid_constant__ CUtensorMap edge_map,
+           uint32_t G, uint32_t stages) {
+    constexpr int WPH = warps_per_head<QG>(), RW = kTile / WPH; // warps per kv head, rows each
+    using A = Attn<T, HD, QG, RW>;
     constexpr int DPL = A::DPL;
+    constexpr int kState = 32 * QG * (2 + DPL); // floats of one warp's (m, l, acc) state
     extern __shared__ __align__(128) uint8_t smem[];
     const uint32_t tile_elems = kTile * G * HD;
     T *tiles = reinterpret_cast<T *>(smem);                                  // [stages][K|V][32][G][HD]
-    float *xchg = reinterpret_cast<float *>(tiles + size_t(stages) * 2 * tile_elems); // pair merge
-    uint64_t *full = reinterpret_cast<uint64_t *>(xchg + kMaxG * 32 * QG * (2 + DPL));
+    float *xchg = reinterpret_cast<float *>(tiles + size_t(stages) * 2 * tile_elems); // head merge
+    uint64_t *full = reinterpret_cast<uint64_t *>(xchg + kMaxG * (WPH - 1) * kState);
     uint64_t *empty = full + stages;
 
     const kvr_step_header *h = hdr(c);
@@ -234,7 +250,7 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
     if (threadIdx.x == 0) {
         for (uint32_t s = 0; s < stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 2 * G);
+            mbar_init(&empty[s], WPH * G);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -247,10 +263,11 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
         n_tiles = w > t0 ? uint32_t((w - t0 + kTile - 1) / kTile) : 0;
     };
 
-    if (warp == 2 * kMaxG) { // ---------------- producer: TMA tile loads ----------------
+    if (warp == WPH * kMaxG) { // ---------------- producer: TMA tile loads ----------------
         if (lane != 0)
             return;
-        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&ring_map)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tile_map)) : "memory");
+        asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&edge_map)) : "memory");
         uint32_t s = 0, phase = 0;
         const uint32_t bytes = 2 * tile_elems * sizeof(T);
         for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -264,18 +281,27 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
             for (uint32_t k = 0; k < n_tiles; ++k) {
                 mbar_wait(&empty[s], phase ^ 1);
                 const uint64_t tk = t0 + uint64_t(k) * kTile;
-                // 16-row halves with no live row (window edges) are not loaded
-                const bool h0 = tk < w && tk + kHalf > lo, h1 = tk + kHalf < w && tk + kTile > lo;
+                // interior tiles: one 32-row box each for K and V; window-edge tiles: only
+                // the 8-row quarters holding a live row
+                const int row0 = int(tk % c.R), z = int(slot * c.L + l);
                 T *kt = tiles + size_t(s) * 2 * tile_elems;
-                mbar_expect_tx(&full[s], (uint32_t(h0) + uint32_t(h1)) * (bytes / 2));
-                for (int hf = 0; hf < 2; ++hf) {
-                    if (!(hf ? h1 : h0))
-                        continue;
-                    const int row0 = int((tk + hf * kHalf) % c.R);
-                    T *dst = kt + size_t(hf) * kHalf * G * HD;
-                    tma_load_4d(dst, &ring_map, 0, int(hg * G), row0, int(slot * c.L + l), &full[s]);
-                    tma_load_4d(dst + tile_elems, &ring_map, 0, int(c.Hkv + hg * G), row0,
-                                int(slot * c.L + l), &full[s]);
+                if (tk >= lo && tk + kTile <= w) {
+                    mbar_expect_tx(&full[s], bytes);
+                    tma_load_4d(kt, &tile_map, 0, int(hg * G), row0, z, &full[s]);
+                    tma_load_4d(kt + tile_elems, &tile_map, 0, int(c.Hkv + hg * G), row0, z, &full[s]);
+                } else {
+                    uint32_t n_q = 0;
+                    for (int j = 0; j < kTile / kEdge; ++j)
+                        n_q += uint32_t(tk + j * kEdge < w && tk + (j + 1) * kEdge > lo);
+                    mbar_expect_tx(&full[s], n_q * (bytes / (kTile / kEdge)));
+                    for (int j = 0; j < kTile / kEdge; ++j) {
+                        if (!(tk + j * kEdge < w && tk + (j + 1) * kEdge > lo))
+                            continue;
+                        T *dst = kt + size_t(j) * kEdge * G * HD;
+                        tma_load_4d(dst, &edge_map, 0, int(hg * G), row0 + j * kEdge, z, &full[s]);
+                        tma_load_4d(dst + tile_elems, &edge_map, 0, int(c.Hkv + hg * G), row0 + j * kEdge, z,
+                                    &full[s]);
+                    }
                 }
                 if (++s == stages) {
                     s = 0;
@@ -285,13 +311,13 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
         }
         return;
     }
-    const uint32_t head_local = uint32_t(warp) >> 1, half = uint32_t(warp) & 1u;
+    const uint32_t head_local = uint32_t(warp) / WPH, part = uint32_t(warp) % WPH;
     if (head_local >= G)
         return;
 
-    // ---------- consumers: warp pair (2h, 2h+1) owns kv head hg*G + h; each takes 16 rows ----------
+    // ---------- consumers: warps WPH*h .. WPH*h+WPH-1 own kv head hg*G + h; RW rows each ----------
     const float scale_log2 = 1.4426950408889634f / sqrtf(float(HD));
-    float *mine = xchg + size_t(head_local) * 32 * QG * (2 + DPL);
+    float *states = xchg + size_t(head_local) * (WPH - 1) * kState; // parts 1.. park their state here
     uint32_t s = 0, phase = 0;
     for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
         const uint32_t hg = it % groups, l = (it / groups) % c.L, slot = it / (groups * c.L);
@@ -308,14 +334,14 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
         // far summaries: rows straight from global memory
         const T *far_base = reinterpret_cast<const T *>(c.far) +
                             (uint64_t(slot) * c.L + l) * c.max_chunks * c.row_elems + uint64_t(kvh) * HD;
-        for (uint32_t f0 = half * kHalf; f0 < st.far_count; f0 += 2 * kHalf) {
-            const uint32_t n = min(uint32_t(kHalf), st.far_count - f0);
+        for (uint32_t f0 = part * RW; f0 < st.far_count; f0 += kTile) {
+            const uint32_t n = min(uint32_t(RW), st.far_count - f0);
             const uint32_t mask = n >= 32 ? 0xffffffffu : (1u << n) - 1u;
             const uint32_t *ids = far_ids + st.far_begin + f0;
             auto far_row = [&](int r) {
                 return far_base + uint64_t(ids[r < int(n) ? r : 0]) * c.row_elems;
             };
-            if (mask == 0xffffu)
+            if (mask == (1u << RW) - 1u)
                 at.template block<true>(far_row, c.d_kv, mask, scale_log2);
             else
                 at.template block<false>(far_row, c.d_kv, mask, scale_log2);
@@ -324,16 +350,16 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
         for (uint32_t k = 0; k < n_tiles; ++k) {
             mbar_wait(&full[s], phase);
             const T *kt = tiles + size_t(s) * 2 * tile_elems;
-            const uint64_t tok0 = t0 + uint64_t(k) * kTile + half * kHalf;
+            const uint64_t tok0 = t0 + uint64_t(k) * kTile + part * RW;
             uint32_t mask = 0;
 #pragma unroll
-            for (int r = 0; r < kHalf; ++r)
+            for (int r = 0; r < RW; ++r)
                 mask |= uint32_t(tok0 + r >= lo && tok0 + r < w) << r;
-            const T *base = kt + (size_t(half) * kHalf * G + head_local) * HD;
+            const T *base = kt + (size_t(part) * RW * G + head_local) * HD;
             auto tile_row = [&](int r) { return base + size_t(r) * G * HD; };
-            if (mask == 0xffffu)
+            if (mask == (1u << RW) - 1u)
                 at.template block<true>(tile_row, tile_elems, mask, scale_log2);
-            else if (mask) // a fully masked half was not even loaded
+            else if (mask) // a quarter with no live row was not even loaded
                 at.template block<false>(tile_row, tile_elems, mask, scale_log2);
             __syncwarp();
             if (lane == 0)
@@ -343,9 +369,10 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
                 phase ^= 1;
             }
         }
-        // merge the pair's states, then normalise
+        // merge the head's WPH states, then normalise
         const uint32_t bar = 1 + head_local;
-        if (half) {
+        if (part) {
+            float *mine = states + size_t(part - 1) * kState;
 #pragma unroll
             for (int g = 0; g < QG; ++g) {
                 mine[(g * (2 + DPL) + 0) * 32 + lane] = at.m[g];
@@ -355,30 +382,42 @@ __global__ void __launch_bounds__(32 * (2 * kMaxG + 1), 1)
                     mine[(g * (2 + DPL) + 2 + i) * 32 + lane] = at.acc[g][i];
             }
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
-        if (!half) {
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * WPH) : "memory");
+        if (!part) {
             float *o = c.out + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD;
 #pragma unroll
             for (int g = 0; g < QG; ++g) {
-                const float m1 = mine[(g * (2 + DPL) + 0) * 32 + lane];
-                const float l1 = mine[(g * (2 + DPL) + 1) * 32 + lane];
-                const float mn = fmaxf(at.m[g], m1);
+                float mn = at.m[g];
+#pragma unroll
+                for (int j = 0; j < WPH - 1; ++j)
+                    mn = fmaxf(mn, states[j * kState + (g * (2 + DPL) + 0) * 32 + lane]);
                 const float a0 = mn == -INFINITY ? 0.f : exp2f(at.m[g] - mn);
-                const float a1 = mn == -INFINITY ? 0.f : exp2f(m1 - mn);
-                const float z = warp_sum(at.lsum[g] * a0 + l1 * a1);
+                float z = at.lsum[g] * a0, sum[DPL];
+#pragma unroll
+                for (int i = 0; i < DPL; ++i)
+                    sum[i] = at.acc[g][i] * a0;
+#pragma unroll
+                for (int j = 0; j < WPH - 1; ++j) {
+                    const float *st = states + j * kState + g * (2 + DPL) * 32 + lane;
+                    const float a = mn == -INFINITY ? 0.f : exp2f(st[0] - mn);
+                    z += st[32] * a;
+#pragma unroll
+                    for (int i = 0; i < DPL; ++i)
+                        sum[i] = fmaf(st[(2 + i) * 32], a, sum[i]);
+                }
+                z = warp_sum(z);
                 const float inv = z > 0.f ? 1.f / z : 0.f;
 #pragma unroll
                 for (int i = 0; i < DPL; ++i)
-                    o[g * HD + DPL * lane + i] =
-                        (at.acc[g][i] * a0 + mine[(g * (2 + DPL) + 2 + i) * 32 + lane] * a1) * inv;
+                    o[g * HD + DPL * lane + i] = sum[i] * inv;
             }
         }
-        asm volatile("bar.sync %0, 64;" ::"r"(bar) : "memory");
+        asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(32 * WPH) : "memory");
     }
 }
 
 
-using AttnFn = void (*)(DevCtx, const CUtensorMap, uint32_t, uint32_t);
+using AttnFn = void (*)(DevCtx, const CUtensorMap, const CUtensorMap, uint32_t, uint32_t);
 
 template <typename T, int HD> AttnFn pick_group(uint32_t g) {
     switch (g) {
@@ -403,9 +442,9 @@ template <typename T> AttnFn pick_hd(uint32_t hd, uint32_t g) {
 struct AttnPlan {
     AttnFn fn = nullptr;
     const void *tc = nullptr; // tensor-core kernel (kvr_attn_tc.cu) when chosen
-    CUtensorMap map{};
+    CUtensorMap map{}, edge_map{}; // 32-row tile boxes / 8-row edge boxes
     TcMaps tc_maps{};      // tensor-core kernel descriptors
-    uint32_t G = 1, stages = 2, grid = 1;
+    uint32_t G = 1, stages = 2, grid = 1, threads = 0;
     size_t smem = 0;
     char name[96] = {0};
 };
@@ -444,7 +483,9 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
     p->stages = uint32_t(std::min<size_t>(8, (192u << 10) / stage)); // deeper rings for smaller stages
     if (p->stages < 2)
         p->stages = 2;
-    p->smem = p->stages * stage + size_t(kMaxG) * 32 * c.group * (2 + c.hd / 32) * 4 +
+    const uint32_t wph = c.group <= 2 ? 4 : 2; // == warps_per_head<group>()
+    p->threads = 32 * (wph * kMaxG + 1);
+    p->smem = p->stages * stage + size_t(kMaxG) * (wph - 1) * 32 * c.group * (2 + c.hd / 32) * 4 +
               2 * p->stages * 8 + 16;
     p->grid = uint32_t(sms);
     cudaFuncSetAttribute(p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem));
@@ -460,20 +501,24 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
     }
     const cuuint64_t dims[4] = {c.hd, 2ull * c.Hkv, c.R, uint64_t(c.L) * c.n_slots};
     const cuuint64_t strides[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
-    const cuuint32_t box[4] = {c.hd, p->G, uint32_t(kHalf), 1}; // 16-row halves
+    const cuuint32_t box[4] = {c.hd, p->G, uint32_t(kTile), 1};
+    const cuuint32_t edge_box[4] = {c.hd, p->G, uint32_t(kEdge), 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};
     const CUtensorMapDataType dt =
         c.esz == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_UINT16;
     const CUresult r = encode(&p->map, dt, 4, c.ring, dims, strides, box, estr,
                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
+    const CUresult r2 = encode(&p->edge_map, dt, 4, c.ring, dims, strides, edge_box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS || r2 != CUDA_SUCCESS || c.R % kTile) {
         delete p;
         return nullptr;
     }
-    std::snprintf(p->name, sizeof(p->name), "k_attn<%s,hd%u,g%u> G=%u stages=%u",
+    std::snprintf(p->name, sizeof(p->name), "k_attn<%s,hd%u,g%u> G=%u stages=%u warps/head=%u",
                   c.elem_kind == KVR_ELEM_F16 ? "f16" : c.elem_kind == KVR_ELEM_BF16 ? "bf16" : "f32",
-                  c.hd, c.group, p->G, p->stages);
+                  c.hd, c.group, p->G, p->stages, wph);
     (void)device;
     return p;
 }
@@ -483,7 +528,7 @@ void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s) {
         launch_attn_tc(p->tc, c, p->tc_maps, p->grid, s);
         return;
     }
-    p->fn<<<p->grid, 32 * (2 * kMaxG + 1), p->smem, s>>>(c, p->map, p->G, p->stages);
+    p->fn<<<p->grid, p->threads, p->smem, s>>>(c, p->map, p->edge_map, p->G, p->stages);
 }
 
 void free_attn_plan(AttnPlan *p) { delete p; }

@@ -339,8 +339,9 @@ struct ScenarioDriver::Impl {
         g.near_window = cfg.far_view.near_window;
         const uint32_t need_rows = cfg.far_view.near_window + span_tokens + 32;
         g.ring_rows = b.ring_rows ? b.ring_rows : (need_rows + 31) / 32 * 32;
-        if (g.ring_rows < need_rows)
-            raise(Errc::bad_config, "b200.ring_rows must cover W* + the staged span + 32 rows");
+        if (g.ring_rows < need_rows || g.ring_rows % 32)
+            raise(Errc::bad_config,
+                  "b200.ring_rows must be a multiple of 32 covering W* + the staged span + 32 rows");
         g.far_cap = cfg.far_view.enabled ? cfg.far_view.cap : 0;
         g.chunk_tokens = cfg.far_view.chunk_tokens;
         if (cfg.far_view.enabled && g.chunk_tokens > 512)

@@ -106,7 +106,7 @@ def test_far_view_fp32_on_device():
 
 @pytest.mark.parametrize("dtype,kvh,hd,qh", [("fp16", 4, 64, 4), ("bf16", 4, 64, 16),
                                              ("fp16", 2, 128, 2), ("bf16", 2, 128, 16),
-                                             ("fp16", 8, 32, 8)])
+                                             ("fp16", 8, 32, 8), ("bf16", 4, 64, 8)])
 def test_window_and_attention_lanes_payload(dtype, kvh, hd, qh):
     cfg = c1()
     cfg["steps"] = 40
