@@ -280,6 +280,8 @@ def run_b200(args, rank, local, world) -> dict | None:
         cfg["b200"]["prefill_budget"] = args.prefill_budget
     if args.attention_kernel != "auto":
         cfg["b200"]["attention_kernel"] = args.attention_kernel
+    if args.utility != "synthetic":
+        cfg["b200"]["utility"] = args.utility
     d = pkg.Driver(cfg, device=local)
     width = cfg["workload"]["concurrency"]
     # fill the fixed-width batch (admissions write whole prompts), then warm up
@@ -434,6 +436,8 @@ def main():
                     help="b200.attention_kernel (auto: tensor cores for GQA groups >= 4)")
     ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
                     help="torch.distributed backend for the per-step counts (N > 1)")
+    ap.add_argument("--utility", default="synthetic", choices=["synthetic", "attention"],
+                    help="b200.utility: placement observations (attention = measured by K-mass)")
     ap.add_argument("--prefill-budget", type=int, default=0,
                     help="b200.prefill_budget: cold prompt rows written per step (0 = all)")
     args = ap.parse_args()
@@ -471,7 +475,7 @@ def main():
             "requests_shard": "request_id % n_gpus", "l2": "inputs larger than L2 "
             f"(~{res['attn_bytes'] / args.steps / 2**30:.1f} GiB of window KV read per step vs 126 MB L2)",
             "attention_kernel": res["variant"], "fill_steps": res["fill_steps"],
-            "prefill_budget": args.prefill_budget,
+            "prefill_budget": args.prefill_budget, "utility": args.utility,
         },
         "prefill": {"budget_tokens_per_step": args.prefill_budget,
                     "queued_tokens_at_end": res["prefill_backlog"],

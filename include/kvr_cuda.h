@@ -49,7 +49,13 @@ typedef struct kvr_geometry {
     uint64_t max_desc_bytes;/* capacity of one step descriptor */
     uint32_t max_scan_descs;/* K-scan capacity (descriptors / spans) */
     uint32_t max_trains;
+    uint32_t utility;       /* 1: K-mass measures attention-utility observations each step */
+    uint32_t utility_layer; /* probe layer of K-mass */
 } kvr_geometry;
+
+/* K-mass output: one run of window rows mapped to one arena block, with the
+ * softmax weight the probe layer's q-heads put on it (mean over q-heads). */
+typedef struct kvr_mass_run { uint32_t block; float mass; } kvr_mass_run;
 
 /* ---- committed step descriptor ------------------------------------------ */
 typedef struct kvr_step_header {
@@ -178,6 +184,10 @@ int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms_per_launch);
 int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms_per_launch);
 /* name of the attention kernel variant chosen for this geometry */
 const char *kvr_dev_attention_variant(kvr_dev *d);
+/* attention-utility observations of the step launched from `ring_slot` (call after
+ * kvr_dev_wait for it; valid until that ring slot is launched again): runs
+ * [slot * near_window, + counts[slot]) of `out` (n_slots * near_window entries) */
+int kvr_dev_utility(kvr_dev *d, uint32_t ring_slot, kvr_mass_run *out, uint32_t *counts);
 /* kernel nodes in the captured step graph (0 before the first graph launch) */
 int kvr_dev_step_kernels(kvr_dev *d, uint32_t *out);
 /* step graphs captured so far: 2 (one per descriptor ring slot) after the first two

@@ -22,6 +22,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <memory>
 #include <span>
 #include <vector>
@@ -79,6 +80,13 @@ public:
     void sync();
     /// Whether `step` is the last step launched from its ring slot.
     bool launched(uint64_t step) const;
+    /// Attention-utility observations K-mass measured in `step` (geometry.utility):
+    /// (block, softmax mass of the probe layer, mean over q-heads) per run of window
+    /// rows, for the slots whose session `keep` accepts. Waits for the step.
+    std::vector<std::pair<BlockId, double>> utility(uint64_t step,
+                                                    const std::function<bool(SessionId)> &keep);
+    /// The same, per device slot (empty for slots that were not live).
+    std::vector<std::vector<kvr_mass_run>> utility_runs(uint64_t step);
     /// Flush byte ops queued outside a step (Pager API use without a Driver).
     void flush();
     /// Write at most `tokens` cold prompt rows per step (0 = all of them, the

@@ -42,6 +42,9 @@ struct B200Config {
     uint32_t graph = 1;            // replay the step as a captured CUDA graph
     bool check = false;            // compare the device K-scan with host reduce() every step
     uint64_t prefill_budget = 0;   // cold prompt rows written per step (deferred queue); 0 = all
+    std::string utility = "synthetic"; // placement observations: "synthetic" (the reference's,
+                                       // scenario.cpp:526-529) | "attention" (K-mass, measured)
+    int32_t utility_layer = -1;    // K-mass probe layer; < 0 = the last layer
     uint32_t shard_rank = 0;       // requests shard by sequence across GPUs:
     uint32_t shard_world = 1;      //   this rank keeps request_id % world == rank
 };

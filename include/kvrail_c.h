@@ -349,6 +349,11 @@ int kvr_device_far_selection(kvr_device *d, uint32_t slot, uint64_t *out, uint64
                              uint64_t *n_out);
 int kvr_device_read_scan(kvr_device *d, kvr_train *trains, uint64_t train_cap, uint64_t *n_trains,
                          kvr_descriptor *descs, uint64_t desc_cap, uint64_t *n_descs);
+/* b200.utility = attention: the K-mass observations of `step` (waits for it; valid
+ * until step + 2 is launched) — runs[slot * near_window, + counts[slot]) of
+ * {block, mass}: the probe layer's softmax weight on each block of the slot's
+ * window, mean over q-heads (the placement tracker's observations). */
+int kvr_device_utility(kvr_device *d, uint64_t step, struct kvr_mass_run *runs, uint32_t *counts);
 
 #ifdef __cplusplus
 }

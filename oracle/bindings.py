@@ -42,6 +42,9 @@ def oracle() -> C.CDLL:
         lib.kvo_attend_window.argtypes = [C.c_void_p, C.c_uint64, f, C.c_uint64, C.c_uint32,
                                           C.c_uint32, C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
                                           f, f]
+        lib.kvo_attention_weights.argtypes = [C.c_void_p, C.c_uint64, f, C.c_uint64, C.c_uint32,
+                                              C.c_uint32, C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
+                                              f, C.POINTER(C.c_double)]
         lib.kvo_fnv1a.argtypes = [C.c_void_p, C.c_uint64, C.c_uint64]
         lib.kvo_fnv1a.restype = C.c_uint64
         lib.kvo_half_to_float.argtypes = [C.c_uint16]
@@ -102,6 +105,66 @@ def attend_window(window: bytes, n_near: int, layers: int, kv_heads: int, head_d
     oracle().kvo_attend_window(window, n_near, far, n_far, layers, kv_heads, head_dim, elem_kind,
                                layer, kv_head, q, out)
     return list(out)
+
+
+def attention_weights(window: bytes, n_near: int, layers: int, kv_heads: int, head_dim: int,
+                      elem_kind: int, layer: int, kv_head: int, query, far_images=None, n_far=0):
+    q = (C.c_float * head_dim)(*query)
+    out = (C.c_double * max(1, n_far + n_near))()
+    far = (C.c_float * max(1, len(far_images or [])))(*(far_images or []))
+    oracle().kvo_attention_weights(window, n_near, far, n_far, layers, kv_heads, head_dim, elem_kind,
+                                   layer, kv_head, q, out)
+    return list(out)[:n_far + n_near]
+
+
+def check_driver_utility(driver, layer=None) -> float:
+    """K-mass runs of the last step == the oracle's softmax weights of the probe
+    layer, averaged over q-heads and summed per block of the committed view (same
+    blocks in window order). Returns the worst absolute mass error."""
+    dev = driver.device()
+    g = dev.geometry
+    layer = g.layers - 1 if layer is None else layer
+    pager = driver.pager()
+    tb = g.token_bytes
+    group = g.q_heads // g.kv_heads
+    done, _ = driver.progress()
+    step = done - 1
+    runs = dev.utility(step)
+    worst = 0.0
+    checked = 0
+    for slot, session, written in driver.live():
+        if pager.session_eos(session):
+            continue
+        view = pager.active_view(session)
+        lo = max(0, written - g.near_window)
+        window, blocks = b"", []
+        for t in range(lo, written):
+            window += token_bytes_via_view(pager, view, t, tb)
+            blocks.append(next(blk for b, e, blk, sb in view["entries"] if b <= t < e))
+        far = dev.far_selection(slot)
+        far_imgs = []
+        for chunk in far:
+            far_imgs += as_floats(dev.far_row(slot, chunk), g.elem_kind)
+        rows = [0.0] * (written - lo)
+        for qh in range(g.q_heads):
+            q = fill_query(g.seed, session, step, layer, qh, g.head_dim, g.elem_kind)
+            w = attention_weights(window, written - lo, g.layers, g.kv_heads, g.head_dim, g.elem_kind,
+                                  layer, qh // group, q, far_imgs, len(far))
+            for i in range(written - lo):
+                rows[i] += w[len(far) + i] / g.q_heads
+        want = []
+        for i, b in enumerate(blocks):
+            if want and want[-1][0] == b:
+                want[-1][1] += rows[i]
+            else:
+                want.append([b, rows[i]])
+        got = runs[slot]
+        assert [b for b, _ in got] == [b for b, _ in want], f"slot {slot}: block runs differ"
+        for (_, m1), (_, m2) in zip(got, want):
+            worst = max(worst, abs(m1 - m2))
+        checked += 1
+    assert checked > 0
+    return worst
 
 
 def rel_error(got, want) -> float:

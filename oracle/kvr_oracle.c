@@ -417,6 +417,39 @@ void kvo_attend_window(const void *window, uint64_t n_near, const float *far_ima
     free(v);
 }
 
+void kvo_attention_weights(const void *window, uint64_t n_near, const float *far_images,
+                           uint64_t n_far, uint32_t layers, uint32_t kv_heads, uint32_t head_dim,
+                           int elem_kind, uint32_t layer, uint32_t kv_head, const float *query,
+                           double *weights) {
+    /* attend's logits (q.k)/sqrt(d) in double, max-subtracted softmax
+     * (far_view.cpp:128-150), over build_view's slot order [far..., near...] */
+    const uint64_t d_kv = (uint64_t)kv_heads * head_dim;
+    const uint64_t lanes = 2 * (uint64_t)layers * d_kv;
+    const uint64_t n = n_far + n_near;
+    const uint64_t k_off = 2 * (uint64_t)layer * d_kv + (uint64_t)kv_head * head_dim;
+    const double scale = 1.0 / sqrt((double)head_dim);
+    if (n == 0)
+        return;
+    for (uint64_t s = 0; s < n; ++s) {
+        double dot = 0.0;
+        for (uint32_t i = 0; i < head_dim; ++i) {
+            const double k = s < n_far ? (double)far_images[s * lanes + k_off + i]
+                                       : (double)load_lane(window, (s - n_far) * lanes + k_off + i, elem_kind);
+            dot += (double)query[i] * k;
+        }
+        weights[s] = dot * scale;
+    }
+    double m = weights[0], denom = 0.0;
+    for (uint64_t s = 0; s < n; ++s)
+        m = weights[s] > m ? weights[s] : m;
+    for (uint64_t s = 0; s < n; ++s) {
+        weights[s] = exp(weights[s] - m);
+        denom += weights[s];
+    }
+    for (uint64_t s = 0; s < n; ++s)
+        weights[s] /= denom;
+}
+
 uint64_t kvo_fnv1a(const void *data, uint64_t n, uint64_t h) {
     const uint8_t *p = (const uint8_t *)data;
     if (h == 0)

@@ -81,6 +81,14 @@ void kvo_attend_window(const void *window, uint64_t n_near, const float *far_ima
                        int elem_kind, uint32_t layer, uint32_t kv_head, const float *query,
                        float *out);
 
+/* The softmax weights attend() (far_view.cpp:113-155) puts on each of the
+ * n_far + n_near view slots of kvo_attend_window's view, in view order (far
+ * summaries first), in double — the oracle of K-mass (kvr_mass.cu). */
+void kvo_attention_weights(const void *window, uint64_t n_near, const float *far_images,
+                           uint64_t n_far, uint32_t layers, uint32_t kv_heads, uint32_t head_dim,
+                           int elem_kind, uint32_t layer, uint32_t kv_head, const float *query,
+                           double *weights);
+
 /* FNV-1a 64 over bytes (the hash used by the parity traces). */
 uint64_t kvo_fnv1a(const void *data, uint64_t n, uint64_t seed_h);
 

@@ -12,6 +12,7 @@
 //   q/out  [slot][layer][q_head][head_dim] f32
 //   desc   3 x max_desc_bytes               step descriptors (2 ring slots + apply-only)
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -37,6 +38,8 @@ struct kvr_dev {
     uint8_t *d_desc[3] = {nullptr, nullptr, nullptr};
     void *h_desc[3] = {nullptr, nullptr, nullptr};
     ScanCounters *h_scan[2] = {nullptr, nullptr};
+    kvr_mass_run *h_mass[2] = {nullptr, nullptr}; // K-mass runs per ring slot (pinned)
+    uint32_t *h_mass_count[2] = {nullptr, nullptr};
     cudaEvent_t ev_start[2] = {}, ev_stop[2] = {}, ev_attn[2] = {};
     cudaEvent_t ev_phase[2][8] = {}; // per ring slot: phase boundaries inside the step graph
     cudaGraphExec_t graph[2] = {nullptr, nullptr};
@@ -123,6 +126,8 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     if (d->g.attention && d->attn)
         launch_attn(d->attn, c, s);
     mark(6);
+    if (c.utility)
+        launch_mass(c, s);
     // Cold writes (older prompt rows nothing in this step reads) go last: measured
     // on B200, co-running this int-bound generation beside the HBM-bound attention
     // (one CTA per SM on a forked branch) slowed the attention by more than the
@@ -246,6 +251,27 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
             ck(cudaMallocHost(&p, sizeof(ScanCounters)), "pinned stats");
             d->h_scan[i] = static_cast<ScanCounters *>(p);
         }
+        if (g.utility) {
+            if (!g.attention || g.utility_layer >= g.layers || c.group > mass_max_group())
+                throw std::runtime_error("utility: needs attention, utility_layer < layers and q-group <= 16");
+            c.utility = 1;
+            c.util_layer = g.utility_layer;
+            c.mass_sc = static_cast<float *>(dalloc(d.get(), mass_scratch_floats(c) * 4, "mass scores"));
+            c.mass_part = static_cast<float2 *>(dalloc(d.get(), mass_part_entries(c) * sizeof(float2), "mass parts"));
+            c.mass_runs = static_cast<kvr_mass_run *>(
+                dalloc(d.get(), uint64_t(c.n_slots) * c.W * sizeof(kvr_mass_run), "mass runs"));
+            c.mass_count = static_cast<uint32_t *>(dalloc(d.get(), uint64_t(c.n_slots) * 4, "mass count"));
+            ck(cudaMemsetAsync(c.mass_count, 0, uint64_t(c.n_slots) * 4, d->stream), "mass count zero");
+            for (int i = 0; i < 2; ++i) {
+                void *p;
+                ck(cudaMallocHost(&p, uint64_t(c.n_slots) * c.W * sizeof(kvr_mass_run)), "pinned mass");
+                d->h_mass[i] = static_cast<kvr_mass_run *>(p);
+                ck(cudaMallocHost(&p, uint64_t(c.n_slots) * 4), "pinned mass count");
+                d->h_mass_count[i] = static_cast<uint32_t *>(p);
+            }
+            if (!prepare_mass(c))
+                throw std::runtime_error("utility: head_dim must be 32, 64 or 128 and (W* + q_heads) * 8 bytes <= 200 KiB");
+        }
         prepare_scan(c.max_scan);
         prepare_gather(c);
         if (g.attention) {
@@ -282,6 +308,10 @@ int kvr_dev_close(kvr_dev *d) {
                 cudaEventDestroy(d->ev_phase[i][j]);
         if (d->h_scan[i])
             cudaFreeHost(d->h_scan[i]);
+        if (d->h_mass[i])
+            cudaFreeHost(d->h_mass[i]);
+        if (d->h_mass_count[i])
+            cudaFreeHost(d->h_mass_count[i]);
     }
     for (int i = 0; i < 3; ++i)
         if (d->h_desc[i])
@@ -343,6 +373,14 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
         }
         ck(cudaMemcpyAsync(d->h_scan[k], c.scan, sizeof(ScanCounters), cudaMemcpyDeviceToHost, d->stream),
            "stats D2H");
+        if (c.utility) {
+            ck(cudaMemcpyAsync(d->h_mass_count[k], c.mass_count, uint64_t(c.n_slots) * 4, cudaMemcpyDeviceToHost,
+                               d->stream),
+               "mass count D2H");
+            ck(cudaMemcpyAsync(d->h_mass[k], c.mass_runs, uint64_t(c.n_slots) * c.W * sizeof(kvr_mass_run),
+                               cudaMemcpyDeviceToHost, d->stream),
+               "mass D2H");
+        }
         ck(cudaEventRecord(d->ev_stop[k], d->stream), "event");
         d->launched[k] = h->step;
         d->in_flight[k] = true;
@@ -477,6 +515,22 @@ int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms) { return time
 int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms) { return time_kernel(d, iters, ms, false); }
 
 const char *kvr_dev_attention_variant(kvr_dev *d) { return attn_variant(d->attn); }
+
+int kvr_dev_utility(kvr_dev *d, uint32_t k, kvr_mass_run *out, uint32_t *counts) {
+    return guard([&] {
+        if (k > 1)
+            throw std::runtime_error("step ring slot must be 0 or 1");
+        if (!d->base.utility)
+            throw std::runtime_error("utility observations are off (geometry.utility = 0)");
+        if (d->in_flight[k])
+            throw std::runtime_error("the step of this ring slot has not been waited for");
+        const DevCtx &c = d->base;
+        std::memcpy(counts, d->h_mass_count[k], uint64_t(c.n_slots) * 4);
+        for (uint32_t s = 0; s < c.n_slots; ++s)
+            std::memcpy(out + uint64_t(s) * c.W, d->h_mass[k] + uint64_t(s) * c.W,
+                        std::min<uint32_t>(counts[s], c.W) * sizeof(kvr_mass_run));
+    });
+}
 
 int kvr_dev_step_kernels(kvr_dev *d, uint32_t *out) {
     return guard([&] { *out = d->graph_kernels; });

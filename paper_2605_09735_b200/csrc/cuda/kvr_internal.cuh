@@ -50,6 +50,12 @@ struct DevCtx {
     kvr_descriptor *descs;
     GSpan *gspans;
     ScanCounters *scan;
+    // K-mass (b200.utility = attention): probe layer, per-row scratch, per-slot runs
+    uint32_t utility, util_layer;
+    float *mass_sc;          // [slot][Hq][W + far_cap] scores in view order
+    float2 *mass_part;       // [slot][Hq][row splits] (max, sum of exp)
+    kvr_mass_run *mass_runs; // [slot][W]
+    uint32_t *mass_count;    // [slot]
 };
 
 __host__ __device__ inline const kvr_step_header *hdr(const DevCtx &c) {
@@ -87,7 +93,12 @@ void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold); // genera
 void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
 void launch_far(const DevCtx &c, cudaStream_t s, int sms);
 void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp
-void launch_presum(const DevCtx &c, cudaStream_t s, int sms); // prompt rows + their far chunk means     // far summaries
+void launch_presum(const DevCtx &c, cudaStream_t s, int sms); // prompt rows + their far chunk means
+void launch_mass(const DevCtx &c, cudaStream_t s);             // attention-utility observations
+bool prepare_mass(const DevCtx &c); // false: no K-mass for this geometry
+size_t mass_scratch_floats(const DevCtx &c);
+size_t mass_part_entries(const DevCtx &c);
+uint32_t mass_max_group();
 void launch_map(const DevCtx &c, cudaStream_t s, int sms);     // page-table edits
 void launch_prime(const DevCtx &c, cudaStream_t s, int sms);   // window priming
 void launch_scan(const DevCtx &c, cudaStream_t s);             // stage + reduce

@@ -93,6 +93,7 @@ int kvr_abi_struct_sizes(uint64_t *out, uint64_t cap, uint64_t *n) {
         sizeof(kvr_cow_op),       sizeof(kvr_edit_op),     sizeof(kvr_write_op),
         sizeof(kvr_blob_op),      sizeof(kvr_need_rec),    sizeof(kvr_span_rec),
         sizeof(kvr_prime_op),     sizeof(kvr_slot_state),  sizeof(kvr_step_stats),
+        sizeof(kvr_mass_run),
     };
     const uint64_t k = sizeof(sz) / sizeof(sz[0]);
     for (uint64_t i = 0; out && i < k && i < cap; ++i)
@@ -533,6 +534,18 @@ int kvr_device_far_selection(kvr_device *d, uint32_t slot, uint64_t *out, uint64
         for (uint64_t i = 0; out && i < v.size() && i < cap; ++i)
             out[i] = v[i];
         *n_out = v.size();
+    });
+}
+int kvr_device_utility(kvr_device *d, uint64_t step, kvr_mass_run *runs, uint32_t *counts) {
+    return call([&] {
+        if (!DS->launched(step))
+            throw Error(Errc::bad_config, "step " + std::to_string(step) + " is not in a ring slot");
+        const auto v = DS->utility_runs(step);
+        const uint32_t W = DS->geometry().near_window;
+        for (size_t s = 0; s < v.size(); ++s) {
+            counts[s] = uint32_t(v[s].size());
+            std::copy(v[s].begin(), v[s].end(), runs + s * W);
+        }
     });
 }
 int kvr_device_read_scan(kvr_device *d, kvr_train *trains, uint64_t train_cap, uint64_t *n_trains,

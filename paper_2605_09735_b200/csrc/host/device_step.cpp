@@ -206,6 +206,7 @@ struct DeviceStep::Impl {
     DeviceStepStats done[2];
     bool have_done[2] = {false, false};
     uint64_t launched_step[2] = {~0ull, ~0ull};
+    std::vector<kvr_slot_state> launched_slots[2]; // slot states of the step in each ring slot
     uint64_t attn_bytes_pending[2] = {0, 0};
     uint64_t desc_bytes_pending[2] = {0, 0};
 
@@ -692,6 +693,7 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
     const uint64_t bytes = m.pack(buf, step, now, &tc, true);
     ck(kvr_dev_launch(m.dev, k, bytes));
     m.launched_step[k] = step;
+    m.launched_slots[k] = m.slots;
     m.have_done[k] = false;
     m.attn_bytes_pending[k] = attn;
     m.desc_bytes_pending[k] = bytes;
@@ -726,6 +728,34 @@ DeviceStepStats DeviceStep::collect(uint64_t step) {
         m.have_done[k] = true;
     }
     return m.done[k];
+}
+
+std::vector<std::vector<kvr_mass_run>> DeviceStep::utility_runs(uint64_t step) {
+    Impl &m = *impl_;
+    collect(step);
+    const uint32_t k = uint32_t(step & 1);
+    const uint32_t W = m.g.near_window;
+    std::vector<kvr_mass_run> runs(uint64_t(m.g.n_slots) * W);
+    std::vector<uint32_t> counts(m.g.n_slots);
+    ck(kvr_dev_utility(m.dev, k, runs.data(), counts.data()));
+    std::vector<std::vector<kvr_mass_run>> out(m.g.n_slots);
+    const std::vector<kvr_slot_state> &slots = m.launched_slots[k];
+    for (uint32_t s = 0; s < m.g.n_slots && s < slots.size(); ++s)
+        if (slots[s].live)
+            out[s].assign(runs.begin() + uint64_t(s) * W, runs.begin() + uint64_t(s) * W + std::min(counts[s], W));
+    return out;
+}
+
+std::vector<std::pair<BlockId, double>> DeviceStep::utility(uint64_t step,
+                                                            const std::function<bool(SessionId)> &keep) {
+    const std::vector<std::vector<kvr_mass_run>> runs = utility_runs(step);
+    const std::vector<kvr_slot_state> &slots = impl_->launched_slots[step & 1];
+    std::vector<std::pair<BlockId, double>> obs;
+    for (size_t s = 0; s < runs.size(); ++s)
+        if (!runs[s].empty() && keep(slots[s].session))
+            for (const kvr_mass_run &r : runs[s])
+                obs.emplace_back(r.block, double(r.mass));
+    return obs;
 }
 
 void DeviceStep::sync() { ck(kvr_dev_sync(impl_->dev)); }

@@ -21,6 +21,7 @@
 #include <set>
 #include <sstream>
 #include <unordered_map>
+#include <unordered_set>
 
 #include <json.hpp>
 
@@ -240,6 +241,7 @@ struct ScenarioDriver::Impl {
     std::set<uint32_t> free_slots;
     size_t next_event = 0;
     bool admission_halted = false;
+    bool measured_utility = false; // b200.utility = attention: K-mass observations
     uint64_t commits_before = 0;
     uint32_t static_slot_blocks = 0;
     uint64_t static_arena_pages = 0;
@@ -368,6 +370,12 @@ struct ScenarioDriver::Impl {
         if (b.attention_kernel != "auto" && b.attention_kernel != "cuda_core" && b.attention_kernel != "tcgen05")
             raise(Errc::bad_config, "b200.attention_kernel must be auto, cuda_core or tcgen05");
         g.use_graph = b.graph;
+        if (b.utility != "synthetic" && b.utility != "attention")
+            raise(Errc::bad_config, "b200.utility must be synthetic or attention");
+        g.utility = b.utility == "attention";
+        g.utility_layer = b.utility_layer < 0 ? g.layers - 1 : uint32_t(b.utility_layer);
+        if (g.utility && (!b.attention || g.utility_layer >= g.layers))
+            raise(Errc::bad_config, "b200.utility = attention needs the attention and utility_layer < layers");
         g.max_desc_bytes = 0;
         g.max_scan_descs = 0;
         g.max_trains = 0;
@@ -380,8 +388,11 @@ struct ScenarioDriver::Impl {
         if (cfg.b200.device >= 0) {
             dev = std::make_unique<DeviceStep>(geometry(pc.arena_pages));
             dev->set_prefill_budget(cfg.b200.prefill_budget);
+            measured_utility = cfg.b200.utility == "attention";
             pager = std::make_unique<Pager>(pc, dev->store());
         } else {
+            if (cfg.b200.utility != "synthetic")
+                raise(Errc::bad_config, "b200.utility = attention needs a device (b200.device >= 0)");
             pager = std::make_unique<Pager>(pc);
         }
         tracker = std::make_unique<UtilityTracker>(cfg.placement.alpha);
@@ -692,7 +703,7 @@ struct ScenarioDriver::Impl {
             }
             ++r.written;
             ++emitted;
-            if (!r.span.empty())
+            if (!r.span.empty() && !measured_utility)
                 obs.emplace_back(r.span.back(),
                                  1.0 + double(pattern(r.id, r.written, 7) % 997) / 4000.0);
             if (r.written - r.prompt >= r.target) {
@@ -707,6 +718,15 @@ struct ScenarioDriver::Impl {
         }
 
         prof.lap(2);
+        if (measured_utility && t >= 2 && dev->launched(t - 2)) {
+            // attention-utility observations measured by K-mass two steps back (the
+            // newest step the device has finished), for sessions still decoding
+            std::unordered_set<SessionId> decoding;
+            for (const Req &r : live)
+                if (!r.eos)
+                    decoding.insert(r.id);
+            obs = dev->utility(t - 2, [&](SessionId s) { return decoding.count(s) > 0; });
+        }
         // Placement: rank staging candidates and take the cold set.
         std::vector<size_t> refresh;
         const uint32_t period = cfg.pager_enabled ? cfg.staged_refresh_period
@@ -1408,6 +1428,8 @@ static ScenarioConfig config_from_json(const ojson &j) {
         take(p, "graph", c.b200.graph);
         take(p, "check", c.b200.check);
         take(p, "prefill_budget", c.b200.prefill_budget);
+        take(p, "utility", c.b200.utility);
+        take(p, "utility_layer", c.b200.utility_layer);
         take(p, "shard_rank", c.b200.shard_rank);
         take(p, "shard_world", c.b200.shard_world);
     }

@@ -162,7 +162,13 @@ class Geometry(C.Structure):
                 ("chunk_tokens", C.c_uint32), ("max_chunks", C.c_uint32),
                 ("max_tokens", C.c_uint64), ("seed", C.c_uint64), ("attention", C.c_uint32),
                 ("use_graph", C.c_uint32), ("max_desc_bytes", C.c_uint64),
-                ("max_scan_descs", C.c_uint32), ("max_trains", C.c_uint32)]
+                ("max_scan_descs", C.c_uint32), ("max_trains", C.c_uint32),
+                ("utility", C.c_uint32), ("utility_layer", C.c_uint32)]
+
+
+class MassRun(C.Structure):
+    """kvr_mass_run (include/kvr_cuda.h): one block's attention-utility mass."""
+    _fields_ = [("block", C.c_uint32), ("mass", C.c_float)]
 
 
 ELEM_F32, ELEM_F16, ELEM_BF16 = 0, 1, 2
@@ -289,6 +295,7 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_device_far_selection": [vp, C.c_uint32, U64P, C.c_uint64, U64P],
         "kvr_device_read_scan": [vp, C.POINTER(Train), C.c_uint64, U64P, C.POINTER(Descriptor),
                                  C.c_uint64, U64P],
+        "kvr_device_utility": [vp, C.c_uint64, C.POINTER(MassRun), U32P],
         "kvr_dev_count": [C.POINTER(C.c_int)],
         "kvr_dev_time_attention": [vp, C.c_uint32, C.POINTER(C.c_double)],
         "kvr_dev_time_gather": [vp, C.c_uint32, C.POINTER(C.c_double)],
@@ -556,6 +563,15 @@ class Device:
         n = C.c_uint64()
         check(native_lib().kvr_device_far_selection(self.h, slot, buf, 4096, C.byref(n)))
         return list(buf)[:n.value]
+
+    def utility(self, step: int) -> list[list[tuple[int, float]]]:
+        """K-mass observations of `step` per device slot: [(block, mass), ...]."""
+        g = self.geometry
+        runs = (MassRun * (g.n_slots * g.near_window))()
+        counts = (C.c_uint32 * g.n_slots)()
+        check(native_lib().kvr_device_utility(self.h, step, runs, counts))
+        return [[(runs[s * g.near_window + i].block, runs[s * g.near_window + i].mass)
+                 for i in range(counts[s])] for s in range(g.n_slots)]
 
     def page_table(self, slot: int, begin: int, count: int):
         buf = (C.c_uint32 * max(1, count))()

@@ -52,7 +52,8 @@ def test_struct_layouts_match_headers():
     mirrors = {0: kv.PagerConfig, 1: kv.TokenRange, 2: kv.ViewEntry, 3: kv.ViewInfo,
                4: kv.ReservedBlock, 5: kv.ArenaStats, 6: kv.WorkCounters, 7: kv.FreeRun,
                8: kv.FrameDelta, 9: kv.StagedSpan, 10: kv.StageNeed, 11: kv.Descriptor,
-               12: kv.TransportConfig, 13: kv.Train, 14: kv.StepRecord, 15: kv.Geometry}
+               12: kv.TransportConfig, 13: kv.Train, 14: kv.StepRecord, 15: kv.Geometry,
+               27: kv.MassRun}
     for i, cls in mirrors.items():
         assert ctypes.sizeof(cls) == sizes[i], cls.__name__
 
