@@ -392,6 +392,22 @@ def ncu_traffic(config: str, variant: str):
     return (t["traffic_bytes"], t["source"]) if same else (None, None)
 
 
+def read_stream_context(traffic, s_per_launch) -> dict:
+    """Context next to the copy-bandwidth roofline: K-attn only reads, so its ceiling
+    is the read-stream rate of this pool's B200s (scripts/read_peak.cu, best of a
+    TMA-bulk and a vector-load stream over 16 GiB; profiles/r1/read_peak.json). The
+    fraction uses the kernel's measured DRAM bytes (ncu) over its in-graph time."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1", "read_peak.json")) as f:
+            peak = max(json.loads(line)["read_gbs"] for line in f if line.strip())
+    except Exception:
+        return {}
+    out = {"read_stream_peak_gbs": peak, "read_stream_src": "profiles/r1/read_peak.json"}
+    if traffic and s_per_launch:
+        out["read_stream_frac"] = traffic / s_per_launch / 1e9 / peak
+    return out
+
+
 def nearest_rank(xs: list[float], q: float) -> float:
     """Nearest-rank percentile (the reference's metrics.cpp:23-33 rule)."""
     v = sorted(xs)
@@ -509,7 +525,8 @@ def main():
                      "traffic_src": traffic_src,
                      "kernel": res["variant"], "peak_src": pk["src"],
                      "bytes_per_launch": res["attn_bytes"] / args.steps,
-                     "ms_per_launch": res["attn_s"] / args.steps * 1e3},
+                     "ms_per_launch": res["attn_s"] / args.steps * 1e3,
+                     **read_stream_context(traffic, res["attn_s"] / args.steps)},
         "clocks": res["clocks"],
     }
     if world == 1 and not args.no_cpu_baseline and args.config != "c4":
