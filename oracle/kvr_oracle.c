@@ -131,12 +131,13 @@ void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint6
             store_lane(out, l, lane_value(pattern(seed, session, token, l)), elem_kind);
         return;
     }
-    /* 2-byte lanes: one splitmix64 per group of 4 lanes (tweaked by bit 63),
-     * lane j of the group takes bits [16j, 16j+16) mod 2001 */
+    /* 2-byte lanes: one splitmix64 per group of 8 lanes (16 bytes; tweaked by
+     * bit 62), lane j of the group takes byte j: (b - 128) / 128, exact in fp16
+     * and bf16 */
     for (uint64_t l = 0; l < lanes; ++l) {
-        const uint64_t x = pattern(seed, session, token, (l >> 2) ^ 0x8000000000000000ull);
-        const uint32_t v = (uint32_t)((x >> (16 * (l & 3))) & 0xffffu) % 2001u;
-        store_lane(out, l, (float)((int)v - 1000) / 1000.0f, elem_kind);
+        const uint64_t x = pattern(seed, session, token, (l >> 3) ^ 0x4000000000000000ull);
+        const uint32_t b = (uint32_t)((x >> (8 * (l & 7))) & 0xffu);
+        store_lane(out, l, (float)((int)b - 128) / 128.0f, elem_kind);
     }
 }
 

@@ -29,9 +29,10 @@ uint64_t kvo_splitmix64(uint64_t x);
 void kvo_fill_token_payload(uint64_t seed, uint32_t session, uint64_t token, uint64_t token_bytes,
                             uint32_t elem_bytes, void *out);
 
-/* B200 extension ("lanes" payload mode): the float lane pattern
- * of scenario.cpp:198-201 rounded to the element type (RNE). elem_kind: 0 f32,
- * 1 f16, 2 bf16. For f32 this equals kvo_fill_token_payload. */
+/* B200 extension ("lanes" payload mode). elem_kind 0 (f32): the
+ * float lane pattern of scenario.cpp:198-201, equal to kvo_fill_token_payload.
+ * 2-byte lanes (1 f16, 2 bf16): one splitmix64 per 8 lanes, lane j of the group
+ * = byte j: (b - 128) / 128, exact in both types. */
 void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint64_t lanes,
                           int elem_kind, void *out);
 

@@ -77,11 +77,16 @@ __device__ inline uint16_t f2b_bits(float v) { return __bfloat16_as_ushort(__flo
 // division and the rounding on the hot path (bit-identical by construction).
 struct LaneTable {
     uint32_t v[2001];
+    uint32_t v8[256]; // 2-byte lanes: (b - 128) / 128 in the element encoding (exact)
     __device__ void fill(const DevCtx &c) {
         for (uint32_t i = threadIdx.x; i < 2001; i += blockDim.x) {
             const float f = float(int(i) - 1000) / 1000.0f;
             v[i] = c.esz == 4 ? __float_as_uint(f)
                               : (c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(f) : f2h_bits(f));
+        }
+        for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
+            const float f = float(int(i) - 128) / 128.0f;
+            v8[i] = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(f) : f2h_bits(f);
         }
         __syncthreads();
     }
@@ -107,15 +112,14 @@ __device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab,
             w[i] = tab(splitmix64(base ^ (lane0 + i)));
     } else if constexpr (kKind == kLanes16) {
         // 2-byte lanes (B200 extension, kvo_fill_token_lanes): one splitmix64 per
-        // 4 lanes, lane value from its 16 bits mod 2001, rounded to fp16/bf16
-        const uint64_t key = base ^ 0x8000000000000000ull;
-        const uint64_t g0 = b0 >> 3; // 16 bytes = 8 lanes = 2 groups of 4
+        // 8 lanes (16 bytes), lane j = byte j: (b - 128) / 128, exact in fp16 / bf16
+        const uint64_t x = splitmix64(base ^ 0x4000000000000000ull ^ (b0 >> 4));
+        const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
 #pragma unroll
-        for (int gi = 0; gi < 2; ++gi) {
-            const uint64_t x = splitmix64(key ^ (g0 + gi));
-            const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
-            w[2 * gi] = tab.v[mod2001_u16(lo & 0xffffu)] | (tab.v[mod2001_u16(lo >> 16)] << 16);
-            w[2 * gi + 1] = tab.v[mod2001_u16(hi & 0xffffu)] | (tab.v[mod2001_u16(hi >> 16)] << 16);
+        for (int i = 0; i < 4; ++i) {
+            const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);
+            w[i] = __byte_perm(tab.v8[__byte_perm(src, 0, 0x4440 | k)], tab.v8[__byte_perm(src, 0, 0x4440 | (k + 1))],
+                               0x5410);
         }
     } else { // reference byte pattern: one splitmix per byte
 #pragma unroll

@@ -282,10 +282,10 @@ struct ScenarioDriver::Impl {
                 if (cfg.pager.elem_bytes == 4) { // reference float pattern
                     const float v = float(int64_t(pattern(id, tok, l) % 2001) - 1000) / 1000.0f;
                     std::memcpy(out + 4 * l, &v, 4);
-                } else { // 2-byte lanes: 16 bits of one splitmix per 4 lanes
-                    const uint64_t x = pattern(id, tok, (l >> 2) ^ 0x8000000000000000ull);
-                    const uint32_t r = uint32_t((x >> (16 * (l & 3))) & 0xffffu) % 2001u;
-                    const float v = float(int(r) - 1000) / 1000.0f;
+                } else { // 2-byte lanes: byte l % 8 of one splitmix per 8 lanes
+                    const uint64_t x = pattern(id, tok, (l >> 3) ^ 0x4000000000000000ull);
+                    const uint32_t r = uint32_t((x >> (8 * (l & 7))) & 0xffu);
+                    const float v = float(int(r) - 128) / 128.0f;
                     const uint16_t h = ekind == KVR_ELEM_BF16 ? to_bf16(v) : to_half(v);
                     std::memcpy(out + 2 * l, &h, 2);
                 }
