@@ -146,8 +146,8 @@ void kvo_fill_query(uint64_t seed, uint32_t session, uint64_t step, uint32_t lay
     for (uint32_t d = 0; d < head_dim; ++d) {
         uint64_t h = kvo_splitmix64(seed ^ (0x51ull << 56) ^ ((uint64_t)session << 32) ^
                                     (step << 20) ^ ((uint64_t)layer << 12) ^
-                                    ((uint64_t)head << 8) ^ (d >> 2));
-        float v = lane_value((h >> (16 * (d & 3))) & 0xffffull);
+                                    ((uint64_t)head << 8) ^ (d >> 3));
+        float v = (float)((int)((h >> (8 * (d & 7))) & 0xffull) - 128) / 128.0f; /* exact in every type */
         if (elem_kind == 1)
             v = kvo_half_to_float(kvo_float_to_half(v));
         else if (elem_kind == 2)

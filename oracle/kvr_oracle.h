@@ -37,10 +37,10 @@ void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint6
                           int elem_kind, void *out);
 
 /* Synthetic decode query for (seed, session, step, layer, q_head): hd floats,
- * lane d = ((v % 2001) - 1000) / 1000 with v the 16-bit field d & 3 of
+ * lane d = (b - 128) / 128 with b the byte d & 7 of
  * h = splitmix64(seed ^ 0x51<<56 ^ session<<32 ^ step<<20 ^ layer<<12 ^ head<<8
- * ^ (d >> 2)) — one hash per 4 lanes, like the 2-byte KV lanes. Rounded to
- * elem_kind like K/V. (A B200-side synthetic input: the reference has no query.) */
+ * ^ (d >> 3)) — one hash per 8 lanes, like the 2-byte KV lanes; exact in every
+ * element type. (A B200-side synthetic input: the reference has no query.) */
 void kvo_fill_query(uint64_t seed, uint32_t session, uint64_t step, uint32_t layer,
                     uint32_t head, uint32_t head_dim, int elem_kind, float *out);
 

@@ -221,18 +221,12 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
     }
 }
 
-// Decode queries for live slots: [slot][L][Hq][hd], rounded to the KV element
-// type (kvo_fill_query in the oracle). One CTA per (slot, layer).
+// Decode queries for live slots: [slot][L][Hq][hd], exact in the KV element type
+// (kvo_fill_query in the oracle). One CTA per (slot, layer); one hash per 8 lanes.
 __global__ void __launch_bounds__(256) k_query(DevCtx c) {
-    __shared__ float val[2001]; // ((k - 1000) / 1000) rounded to the KV type, k = v % 2001
-    for (uint32_t i = threadIdx.x; i < 2001; i += blockDim.x) {
-        float v = float(int(i) - 1000) / 1000.0f;
-        if (c.elem_kind == KVR_ELEM_F16)
-            v = __half2float(__float2half_rn(v));
-        else if (c.elem_kind == KVR_ELEM_BF16)
-            v = __bfloat162float(__float2bfloat16_rn(v));
-        val[i] = v;
-    }
+    __shared__ float val[256]; // (b - 128) / 128
+    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
+        val[i] = float(int(i) - 128) / 128.0f;
     __syncthreads();
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
@@ -245,11 +239,12 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
                               (h->step << 20) ^ (uint64_t(l) << 12);
         float4 *q = reinterpret_cast<float4 *>(c.q + uint64_t(sl) * per_layer);
         const uint32_t hd_shift = __ffs(c.hd) - 1; // head_dim is a power of two (32/64/128)
-        for (uint32_t i = threadIdx.x; i < per_layer / 4; i += blockDim.x) { // 4 lanes per hash
-            const uint32_t head = (4 * i) >> hd_shift, d4 = i & ((c.hd >> 2) - 1);
-            const uint64_t x = splitmix64(base ^ (uint64_t(head) << 8) ^ d4);
-            q[i] = make_float4(val[mod2001_u16(uint32_t(x) & 0xffffu)], val[mod2001_u16(uint32_t(x) >> 16)],
-                               val[mod2001_u16(uint32_t(x >> 32) & 0xffffu)], val[mod2001_u16(uint32_t(x >> 48))]);
+        for (uint32_t i = threadIdx.x; i < per_layer / 8; i += blockDim.x) { // 8 lanes per hash
+            const uint32_t head = (8 * i) >> hd_shift, d8 = i & ((c.hd >> 3) - 1);
+            const uint64_t x = splitmix64(base ^ (uint64_t(head) << 8) ^ d8);
+            const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+            q[2 * i] = make_float4(val[lo & 0xffu], val[(lo >> 8) & 0xffu], val[(lo >> 16) & 0xffu], val[lo >> 24]);
+            q[2 * i + 1] = make_float4(val[hi & 0xffu], val[(hi >> 8) & 0xffu], val[(hi >> 16) & 0xffu], val[hi >> 24]);
         }
     }
 }

@@ -159,6 +159,8 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         kvr_geometry g = *geo;
         if (g.token_bytes % 16 || (2ull * g.kv_heads * g.head_dim * g.elem_bytes) % 16)
             throw std::runtime_error("token and layer rows must be multiples of 16 bytes");
+        if (g.head_dim < 8 || (g.head_dim & (g.head_dim - 1)))
+            throw std::runtime_error("head_dim must be a power of two >= 8");
         if (g.kv_heads == 0 || g.q_heads % g.kv_heads)
             throw std::runtime_error("q_heads must be a multiple of kv_heads");
         if (g.ring_rows % 32 || g.ring_rows < g.near_window)

@@ -333,8 +333,8 @@ struct ScenarioDriver::Impl {
         g.q_heads = b.q_heads ? b.q_heads : g.kv_heads;
         if (g.kv_heads * g.head_dim != cfg.pager.kv_head_dim)
             raise(Errc::bad_config, "b200.kv_heads * b200.head_dim must equal pager.kv_head_dim");
-        if (g.head_dim == 0 || (g.head_dim & (g.head_dim - 1)))
-            raise(Errc::bad_config, "b200.head_dim must be a power of two");
+        if (g.head_dim < 8 || (g.head_dim & (g.head_dim - 1)))
+            raise(Errc::bad_config, "b200.head_dim must be a power of two >= 8");
         if (g.q_heads % g.kv_heads)
             raise(Errc::bad_config, "b200.q_heads must be a multiple of b200.kv_heads");
         g.n_slots = width;
