@@ -77,25 +77,17 @@ __device__ inline uint16_t f2b_bits(float v) { return __bfloat16_as_ushort(__flo
 // division and the rounding on the hot path (bit-identical by construction).
 struct LaneTable {
     uint32_t v[2001];
-    uint32_t v8[256]; // 2-byte lanes: (b - 128) / 128 in the element encoding (exact)
     __device__ void fill(const DevCtx &c) {
         for (uint32_t i = threadIdx.x; i < 2001; i += blockDim.x) {
             const float f = float(int(i) - 1000) / 1000.0f;
             v[i] = c.esz == 4 ? __float_as_uint(f)
                               : (c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(f) : f2h_bits(f));
         }
-        for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x) {
-            const float f = float(int(i) - 128) / 128.0f;
-            v8[i] = c.elem_kind == KVR_ELEM_BF16 ? f2b_bits(f) : f2h_bits(f);
-        }
         __syncthreads();
     }
     __device__ uint32_t operator()(uint64_t h) const { return v[h % 2001ull]; }
 };
 
-/// x % 2001 for x < 2^16: (x * 33538) >> 26 == x / 2001 for every 16-bit x
-/// (checked exhaustively), so the remainder is two IMADs and a shift.
-__device__ __forceinline__ uint32_t mod2001_u16(uint32_t x) { return x - ((x * 33538u) >> 26) * 2001u; }
 
 enum PayloadKind { kBytes = 0, kLanes16 = 1, kLanes32 = 2 };
 
@@ -113,13 +105,23 @@ __device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab,
     } else if constexpr (kKind == kLanes16) {
         // 2-byte lanes (B200 extension, kvo_fill_token_lanes): one splitmix64 per
         // 8 lanes (16 bytes), lane j = byte j: (b - 128) / 128, exact in fp16 / bf16
+        // (arithmetic, no table: byte_perm places byte b in the mantissa of 2^23 + b,
+        // one exact FFMA maps it to (b - 128) / 128, and a pack converts two lanes)
         const uint64_t x = splitmix64(base ^ 0x4000000000000000ull ^ (b0 >> 4));
         const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+        const bool bf = c.elem_kind == KVR_ELEM_BF16;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);
-            w[i] = __byte_perm(tab.v8[__byte_perm(src, 0, 0x4440 | k)], tab.v8[__byte_perm(src, 0, 0x4440 | (k + 1))],
-                               0x5410);
+            const float v0 = fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | k)), 0.0078125f, -65537.f);
+            const float v1 = fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | (k + 1))), 0.0078125f, -65537.f);
+            if (bf) {
+                const __nv_bfloat162 p = __floats2bfloat162_rn(v0, v1);
+                w[i] = *reinterpret_cast<const uint32_t *>(&p);
+            } else {
+                const __half2 p = __floats2half2_rn(v0, v1);
+                w[i] = *reinterpret_cast<const uint32_t *>(&p);
+            }
         }
     } else { // reference byte pattern: one splitmix per byte
 #pragma unroll
