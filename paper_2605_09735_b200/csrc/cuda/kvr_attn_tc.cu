@@ -46,6 +46,7 @@ constexpr uint32_t kSideBytes = 2 * kHalfBytes; // a K (or V) tile: two 64-dim h
 // softmax and the PV MMA (measured: 3 + 3 beats 2 + 4 on C3 and C5)
 constexpr int kKStages = KVR_TC_KSTAGES, kVStages = KVR_TC_VSTAGES;
 static_assert(kVStages <= 4, "V stage index and phase are packed in 3 bits");
+static_assert(kKStages <= kVStages, "a K ring deeper than the V ring stalls the PV order (4 + 2 hung on B200)");
 constexpr uint32_t kOpBytes = kN * kHd * 2; // one Q or P operand buffer (4 KiB)
 #ifndef KVR_TC_TILE5D
 #define KVR_TC_TILE5D 1
