@@ -458,12 +458,11 @@ def main():
                     help="b200.prefill_budget: cold prompt rows written per step (0 = all)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
-    rank, local, world = dist_setup(args.backend)
-
-    if args.impl == "reference":
-        if rank == 0:
-            print(json.dumps(reference_arm(args, world)), flush=True)
+    if args.impl == "reference":  # CPU only: rank 0 runs it, no process group, no GPU
+        if int(os.environ.get("RANK", "0")) == 0:
+            print(json.dumps(reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")))), flush=True)
         return
+    rank, local, world = dist_setup(args.backend)
 
     res = run_b200(args, rank, local, world)
     if rank != 0:
