@@ -498,14 +498,36 @@ __global__ void __launch_bounds__(kThreads, 1)
         // vfull two phases ahead would alias. Bit s = parity of PVs issued for stage s.
         uint32_t vpar = 0;
         const uint32_t kbase = smem_u32(kbuf), vbase = smem_u32(vbuf), wg0 = smem_u32(wgbuf);
-        auto ready = [&](uint64_t *bar, uint32_t par) { return __shfl_sync(0xffffffffu, mbar_test(bar, par), 0); };
         Item I;
         bool have = S.next(c, slots, n_items, w, k, I);
         while (have || pv0 < nw0 || pv1 < nw1) {
+            // every barrier this iteration may act on is tested at once (independent
+            // test_waits overlap their latency) and broadcast with one shuffle: bit 0
+            // S issue, bit 1 + x PV issue of warpgroup x
+            uint32_t go = 0;
             if (have) {
                 const uint32_t nwc = w ? nw1 : nw0, b = nwc & 1u;
-                if ((k > 0 || ready(&wb[w].qfull, (w ? mw1 : mw0) & 1u)) && ready(&kfull[s], ph) &&
-                    ready(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u)) {
+                const bool q = k > 0 || mbar_test(&wb[w].qfull, (w ? mw1 : mw0) & 1u);
+                const bool kf = mbar_test(&kfull[s], ph);
+                const bool se = mbar_test(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u);
+                go |= uint32_t(q && kf && se);
+            }
+#pragma unroll
+            for (uint32_t x = 0; x < 2; ++x) {
+                const uint32_t pvn = x ? pv1 : pv0;
+                if (pvn >= (x ? nw1 : nw0))
+                    continue;
+                const uint32_t b = pvn & 1u, par = (pvn >> 1) & 1u;
+                const uint32_t e = ((x ? ring1 : ring0) >> (8 * (pvn & 3u))) & 0xffu, st = e & 3u, sph = (e >> 2) & 1u;
+                const bool pf = mbar_test(&wb[x].pfull[b], par);
+                const bool oe = mbar_test(&wb[x].oempty[b], par ^ 1u);
+                const bool vf = mbar_test(&vfull[st], sph);
+                go |= uint32_t(((vpar >> st) & 1u) == sph && pf && oe && vf) << (1 + x);
+            }
+            go = __shfl_sync(0xffffffffu, go, 0);
+            if (have) {
+                const uint32_t nwc = w ? nw1 : nw0, b = nwc & 1u;
+                if (go & 1u) {
                     tc_fence_after();
                     if (elect_one()) {
                         const uint64_t a0 = sdesc(kbase + s * kSideBytes, 16, 1024, 2);
@@ -543,11 +565,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint32_t pvn = x ? pv1 : pv0;
                 if (pvn >= (x ? nw1 : nw0))
                     continue;
-                const uint32_t b = pvn & 1u, par = (pvn >> 1) & 1u;
-                const uint32_t e = ((x ? ring1 : ring0) >> (8 * (pvn & 3u))) & 0xffu, st = e & 3u,
-                               sph = (e >> 2) & 1u, nk = e >> 3;
-                if (((vpar >> st) & 1u) != sph || !ready(&wb[x].pfull[b], par) || !ready(&wb[x].oempty[b], par ^ 1u) ||
-                    !ready(&vfull[st], sph))
+                const uint32_t b = pvn & 1u;
+                const uint32_t e = ((x ? ring1 : ring0) >> (8 * (pvn & 3u))) & 0xffu, st = e & 3u, nk = e >> 3;
+                if (!((go >> (1 + x)) & 1u) || pvn >= (x ? nw1 : nw0))
                     continue;
                 tc_fence_after();
                 if (elect_one()) {
