@@ -210,10 +210,15 @@ struct Tile {
     uint32_t nk;                 // PV K steps (16 rows each) covering every used row
     uint64_t tok_r0;             // token of smem row 0 for the near rows (mod 2^64)
 };
+__device__ inline bool item_fill(const DevCtx &c, const kvr_slot_state *slots, Item &I);
 __device__ inline bool item_of(const DevCtx &c, const kvr_slot_state *slots, uint32_t it, Item &I) {
     I.head = it % c.Hkv;
     I.layer = (it / c.Hkv) % c.L;
     I.slot = it / (c.Hkv * c.L);
+    return item_fill(c, slots, I);
+}
+/// Item fields from (slot, layer, head); false if the slot is not live.
+__device__ inline bool item_fill(const DevCtx &c, const kvr_slot_state *slots, Item &I) {
     const kvr_slot_state st = slots[I.slot];
     if (!st.live)
         return false;
@@ -292,15 +297,32 @@ __device__ inline bool elect_one() {
 }
 
 /// The j-th active item (live, >= 1 tile) of a CTA belongs to warpgroup j % 2.
+/// (slot, layer, head) of item `it` advance incrementally by gridDim.x: no
+/// divisions on the item stream.
 struct Cursor {
-    uint32_t it, j;
-    __device__ void init() { it = blockIdx.x, j = 0; }
+    uint32_t it, j, slot, layer, head, ds, dl, dh;
+    __device__ void init(const DevCtx &c) {
+        it = blockIdx.x, j = 0;
+        head = it % c.Hkv, layer = (it / c.Hkv) % c.L, slot = it / (c.Hkv * c.L);
+        dh = gridDim.x % c.Hkv, dl = (gridDim.x / c.Hkv) % c.L, ds = gridDim.x / (c.Hkv * c.L);
+    }
+    __device__ void step(const DevCtx &c) {
+        it += gridDim.x;
+        head += dh;
+        layer += dl;
+        if (head >= c.Hkv)
+            head -= c.Hkv, ++layer;
+        slot += ds;
+        if (layer >= c.L)
+            layer -= c.L, ++slot;
+    }
     __device__ bool next(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items, uint32_t w, Item &I) {
-        for (; it < n_items; it += gridDim.x) {
-            if (!item_of(c, slots, it, I) || I.n_tiles == 0)
+        for (; it < n_items; step(c)) {
+            I.slot = slot, I.layer = layer, I.head = head;
+            if (!item_fill(c, slots, I) || I.n_tiles == 0)
                 continue;
             if ((j++ & 1u) == w) {
-                it += gridDim.x;
+                step(c);
                 return true;
             }
         }
@@ -318,8 +340,8 @@ struct Stream { // (no arrays indexed by w: everything stays in registers)
     bool h0, h1;
     uint32_t k0, k1, turn;
     __device__ void init(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items) {
-        c0.init();
-        c1.init();
+        c0.init(c);
+        c1.init(c);
         h0 = c0.next(c, slots, n_items, 0, I0);
         h1 = c1.next(c, slots, n_items, 1, I1);
         k0 = k1 = turn = 0;
@@ -610,7 +632,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         uint32_t n = 0, m_items = 0;
         Cursor cur;
-        cur.init();
+        cur.init(c);
         Item I, In;
         // the next item and its Q are fetched one item ahead (their global loads
         // overlap this item's tiles instead of stalling the item start;
