@@ -52,7 +52,7 @@ constexpr uint32_t kOpBytes = kN * kHd * 2; // one Q or P operand buffer (4 KiB)
 #define KVR_TC_TILE5D 1
 #endif
 constexpr bool kUseTile5d = KVR_TC_TILE5D != 0;
-constexpr int kThreads = 384; // warp 0 TMA, warp 1 MMA, warps 4-7 / 8-11 softmax warpgroups
+constexpr int kThreads = 384; // warp 0 K TMA, 1 S MMA, 2 V TMA, 3 PV MMA, warps 4-7 / 8-11 softmax
 
 __device__ inline uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
 __device__ inline void mbar_init(uint64_t *bar, uint32_t count) {
@@ -501,96 +501,107 @@ __global__ void __launch_bounds__(kThreads, 1)
                 ph ^= 1;
             }
         }
-    } else if (warp == 1) { // ---------------- MMA issuer (whole warp, one elected lane issues) ----------------
+    } else if (warp == 1) { // ---------------- S issuer (whole warp, one elected lane issues) ----------------
+        // S^T = K . Q^T for every tile of the stream, in stream order, as soon as its K
+        // tile, the warpgroup's S buffer and (first tile of an item) its Q are ready.
+        // The PVs are issued by warp 3: two issuing warps halve the per-tile event-loop
+        // latency that bounded the kernel with one.
         constexpr uint32_t fmt = std::is_same_v<T, __nv_bfloat16> ? 1u : 0u;
         constexpr uint32_t id_s = idesc(fmt, 0, 1, kRows, kN); // S^T = K . Q^T (Q MN-major)
-        constexpr uint32_t id_o = idesc(fmt, 1, 1, kHd, kN);   // O^T = V^T . P (both MN-major)
-        // Event loop over mbarrier states (uniform across the warp): issue S for
-        // the next tile of the stream as soon as its K tile, S buffer and Q are
-        // ready, and each warpgroup's oldest pending PV as soon as its P is.
         Stream S;
         S.init(c, slots, n_items);
         uint32_t s = 0, ph = 0, w = 0, k = 0;
-        uint32_t sv = 0, phv = 0; // V ring position of the tile whose S is issued next
-        uint32_t nw0 = 0, nw1 = 0, mw0 = 0, mw1 = 0, pv0 = 0, pv1 = 0;
-        uint32_t ring0 = 0, ring1 = 0; // pending tiles per warpgroup: byte (n & 3) = V stage | V phase << 2 | K steps << 3
-        // PVs of one stage must follow the stage's fill order: the V ring runs behind
-        // the K ring, and a warpgroup may reach the PV of a later occupant of a stage
-        // before the other warpgroup's PV of the current one — testing that stage's
-        // vfull two phases ahead would alias. Bit s = parity of PVs issued for stage s.
-        uint32_t vpar = 0;
-        const uint32_t kbase = smem_u32(kbuf), vbase = smem_u32(vbuf), wg0 = smem_u32(wgbuf);
+        uint32_t nw0 = 0, nw1 = 0, mw0 = 0, mw1 = 0;
+        const uint32_t kbase = smem_u32(kbuf), wg0 = smem_u32(wgbuf);
         Item I;
         bool have = S.next(c, slots, n_items, w, k, I);
-        while (have || pv0 < nw0 || pv1 < nw1) {
-            // every barrier this iteration may act on is tested at once (independent
-            // test_waits overlap their latency) and broadcast with one shuffle: bit 0
-            // S issue, bit 1 + x PV issue of warpgroup x
-            uint32_t go = 0;
-            if (have) {
-                const uint32_t nwc = w ? nw1 : nw0, b = nwc & 1u;
-                const bool q = k > 0 || mbar_test(&wb[w].qfull, (w ? mw1 : mw0) & 1u);
-                const bool kf = mbar_test(&kfull[s], ph);
-                const bool se = mbar_test(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u);
-                go |= uint32_t(q && kf && se);
+        while (have) {
+            const uint32_t nwc = w ? nw1 : nw0, b = nwc & 1u;
+            // the three barriers tested at once, one shuffle
+            const bool q = k > 0 || mbar_test(&wb[w].qfull, (w ? mw1 : mw0) & 1u);
+            const bool kf = mbar_test(&kfull[s], ph);
+            const bool se = mbar_test(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u);
+            if (!__shfl_sync(0xffffffffu, uint32_t(q && kf && se), 0))
+                continue;
+            tc_fence_after();
+            if (elect_one()) {
+                const uint64_t a0 = sdesc(kbase + s * kSideBytes, 16, 1024, 2);
+                const uint64_t b0 = sdesc(wg0 + w * kWgBytes, 128, 2048, 0);
+#pragma unroll
+                for (uint32_t kk = 0; kk < kHd / 16; ++kk) // K: 32 B steps in a 128-B row, then next half
+                    mma_f16(tmem + 64 * w + 16 * b, a0 + (((kk >> 2) * kHalfBytes + (kk & 3u) * 32) >> 4),
+                            b0 + kk * (256 >> 4), id_s, kk > 0);
+                mma_commit(&wb[w].sfull[b]);
+                mma_commit(&kempty[s]); // the K half is free once S is computed
             }
+            __syncwarp();
+            if (k == 0)
+                (w ? mw1 : mw0) += 1;
+            (w ? nw1 : nw0) += 1;
+            if (++s == kKStages) {
+                s = 0;
+                ph ^= 1;
+            }
+            have = S.next(c, slots, n_items, w, k, I);
+        }
+    } else if (warp == 3) { // ---------------- PV issuer (whole warp, one elected lane issues) ----------------
+        // O^T = V^T . P per tile, per warpgroup in its tile order, as soon as P, the O
+        // buffer and the V tile are ready. The tile stream is walked in the same order
+        // as the S issuer's, giving each tile its V ring position and K-step count.
+        constexpr uint32_t fmt = std::is_same_v<T, __nv_bfloat16> ? 1u : 0u;
+        constexpr uint32_t id_o = idesc(fmt, 1, 1, kHd, kN); // O^T = V^T . P (both MN-major)
+        constexpr uint32_t kFifo = 8; // queued tiles per warpgroup (byte entries of a u64)
+        Stream S;
+        S.init(c, slots, n_items);
+        uint32_t w = 0, k = 0, sv = 0, phv = 0;
+        uint32_t fw0 = 0, fw1 = 0, pv0 = 0, pv1 = 0; // tiles queued / PVs issued per warpgroup
+        uint64_t ring0 = 0, ring1 = 0; // byte (n % 8) = V stage | V phase << 2 | K steps << 3
+        // PVs of one stage must follow the stage's fill order: a warpgroup may reach the
+        // PV of a later occupant of a stage before the other warpgroup's PV of the current
+        // one — testing that stage's vfull two phases ahead would alias. Bit s = parity of
+        // PVs issued for stage s.
+        uint32_t vpar = 0;
+        const uint32_t vbase = smem_u32(vbuf), wg0 = smem_u32(wgbuf);
+        Item I;
+        bool have = S.next(c, slots, n_items, w, k, I);
+        while (have || pv0 < fw0 || pv1 < fw1) {
+            // queue stream tiles while the next one's warpgroup has room
+            while (have && (w ? fw1 - pv1 : fw0 - pv0) < kFifo) {
+                const uint32_t nk = tile_of(I, k).nk;
+                const uint32_t sh = 8 * ((w ? fw1 : fw0) % kFifo);
+                const uint64_t e = uint64_t(sv | phv << 2 | nk << 3) << sh;
+                if (w)
+                    ring1 = (ring1 & ~(uint64_t(0xff) << sh)) | e, ++fw1;
+                else
+                    ring0 = (ring0 & ~(uint64_t(0xff) << sh)) | e, ++fw0;
+                if (++sv == kVStages) {
+                    sv = 0;
+                    phv ^= 1;
+                }
+                have = S.next(c, slots, n_items, w, k, I);
+            }
+            uint32_t go = 0;
 #pragma unroll
             for (uint32_t x = 0; x < 2; ++x) {
                 const uint32_t pvn = x ? pv1 : pv0;
-                if (pvn >= (x ? nw1 : nw0))
+                if (pvn >= (x ? fw1 : fw0))
                     continue;
                 const uint32_t b = pvn & 1u, par = (pvn >> 1) & 1u;
-                const uint32_t e = ((x ? ring1 : ring0) >> (8 * (pvn & 3u))) & 0xffu, st = e & 3u, sph = (e >> 2) & 1u;
+                const uint32_t e = uint32_t(((x ? ring1 : ring0) >> (8 * (pvn % kFifo))) & 0xffu), st = e & 3u,
+                               sph = (e >> 2) & 1u;
                 const bool pf = mbar_test(&wb[x].pfull[b], par);
                 const bool oe = mbar_test(&wb[x].oempty[b], par ^ 1u);
                 const bool vf = mbar_test(&vfull[st], sph);
-                go |= uint32_t(((vpar >> st) & 1u) == sph && pf && oe && vf) << (1 + x);
+                go |= uint32_t(((vpar >> st) & 1u) == sph && pf && oe && vf) << x;
             }
             go = __shfl_sync(0xffffffffu, go, 0);
-            if (have) {
-                const uint32_t nwc = w ? nw1 : nw0, b = nwc & 1u;
-                if (go & 1u) {
-                    tc_fence_after();
-                    if (elect_one()) {
-                        const uint64_t a0 = sdesc(kbase + s * kSideBytes, 16, 1024, 2);
-                        const uint64_t b0 = sdesc(wg0 + w * kWgBytes, 128, 2048, 0);
-#pragma unroll
-                        for (uint32_t kk = 0; kk < kHd / 16; ++kk) // K: 32 B steps in a 128-B row, then next half
-                            mma_f16(tmem + 64 * w + 16 * b, a0 + (((kk >> 2) * kHalfBytes + (kk & 3u) * 32) >> 4),
-                                    b0 + kk * (256 >> 4), id_s, kk > 0);
-                        mma_commit(&wb[w].sfull[b]);
-                        mma_commit(&kempty[s]); // the K half is free once S is computed
-                    }
-                    __syncwarp();
-                    if (k == 0)
-                        (w ? mw1 : mw0) += 1;
-                    const uint32_t nk = tile_of(I, k).nk;
-                    const uint32_t sh = 8 * (nwc & 3u), e = (sv | phv << 2 | nk << 3) << sh;
-                    if (w)
-                        ring1 = (ring1 & ~(0xffu << sh)) | e;
-                    else
-                        ring0 = (ring0 & ~(0xffu << sh)) | e;
-                    (w ? nw1 : nw0) += 1;
-                    if (++s == kKStages) {
-                        s = 0;
-                        ph ^= 1;
-                    }
-                    if (++sv == kVStages) {
-                        sv = 0;
-                        phv ^= 1;
-                    }
-                    have = S.next(c, slots, n_items, w, k, I);
-                }
-            }
 #pragma unroll
             for (uint32_t x = 0; x < 2; ++x) {
-                const uint32_t pvn = x ? pv1 : pv0;
-                if (pvn >= (x ? nw1 : nw0))
+                if (!((go >> x) & 1u))
                     continue;
-                const uint32_t b = pvn & 1u;
-                const uint32_t e = ((x ? ring1 : ring0) >> (8 * (pvn & 3u))) & 0xffu, st = e & 3u, nk = e >> 3;
-                if (!((go >> (1 + x)) & 1u) || pvn >= (x ? nw1 : nw0))
-                    continue;
+                const uint32_t pvn = x ? pv1 : pv0, b = pvn & 1u;
+                const uint32_t e = uint32_t(((x ? ring1 : ring0) >> (8 * (pvn % kFifo))) & 0xffu), st = e & 3u,
+                               nk = e >> 3;
                 tc_fence_after();
                 if (elect_one()) {
                     const uint64_t a0 = sdesc(vbase + st * kSideBytes, kHalfBytes, 1024, 2);
@@ -606,10 +617,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 (x ? pv1 : pv0) += 1;
             }
         }
-#ifdef KVR_HANG_CHECK
-        if (blockIdx.x == 40 && lane == 0)
-            printf("mma done: tiles %u %u items %u %u\n", nw0, nw1, mw0, mw1);
-#endif
     } else if (warp >= 4) { // ---------------- softmax / correction warpgroups ----------------
         const uint32_t w = uint32_t(warp - 4) >> 2;     // warpgroup 0: warps 4-7, 1: warps 8-11
         const uint32_t t = threadIdx.x - 128 - 128 * w; // TMEM lane: token row of S, head dim of O
