@@ -282,6 +282,7 @@ def run_b200(args, rank, local, world) -> dict | None:
         cfg["b200"]["attention_kernel"] = args.attention_kernel
     if args.utility != "synthetic":
         cfg["b200"]["utility"] = args.utility
+        cfg["b200"]["utility_every"] = args.utility_every
     d = pkg.Driver(cfg, device=local)
     width = cfg["workload"]["concurrency"]
     # fill the fixed-width batch (admissions write whole prompts), then warm up
@@ -454,6 +455,8 @@ def main():
                     help="torch.distributed backend for the per-step counts (N > 1)")
     ap.add_argument("--utility", default="synthetic", choices=["synthetic", "attention"],
                     help="b200.utility: placement observations (attention = measured by K-mass)")
+    ap.add_argument("--utility-every", type=int, default=1,
+                    help="b200.utility_every: K-mass runs on every N-th step")
     ap.add_argument("--prefill-budget", type=int, default=0,
                     help="b200.prefill_budget: cold prompt rows written per step (0 = all)")
     args = ap.parse_args()

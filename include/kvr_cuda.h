@@ -49,7 +49,8 @@ typedef struct kvr_geometry {
     uint64_t max_desc_bytes;/* capacity of one step descriptor */
     uint32_t max_scan_descs;/* K-scan capacity (descriptors / spans) */
     uint32_t max_trains;
-    uint32_t utility;       /* 1: K-mass measures attention-utility observations each step */
+    uint32_t utility;       /* N >= 1: K-mass measures attention-utility observations on
+                               steps with step % N == 0 (0: off) */
     uint32_t utility_layer; /* probe layer of K-mass */
 } kvr_geometry;
 

@@ -45,6 +45,7 @@ struct B200Config {
     std::string utility = "synthetic"; // placement observations: "synthetic" (the reference's,
                                        // scenario.cpp:526-529) | "attention" (K-mass, measured)
     int32_t utility_layer = -1;    // K-mass probe layer; < 0 = the last layer
+    uint32_t utility_every = 1;    // K-mass runs on steps with step % utility_every == 0
     uint32_t shard_rank = 0;       // requests shard by sequence across GPUs:
     uint32_t shard_world = 1;      //   this rank keeps request_id % world == rank
 };

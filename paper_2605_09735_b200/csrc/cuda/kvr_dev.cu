@@ -256,7 +256,7 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         if (g.utility) {
             if (!g.attention || g.utility_layer >= g.layers || c.group > mass_max_group())
                 throw std::runtime_error("utility: needs attention, utility_layer < layers and q-group <= 16");
-            c.utility = 1;
+            c.utility = g.utility; // measure on steps with step % utility == 0
             c.util_layer = g.utility_layer;
             c.mass_sc = static_cast<float *>(dalloc(d.get(), mass_scratch_floats(c) * 4, "mass scores"));
             c.mass_part = static_cast<float2 *>(dalloc(d.get(), mass_part_entries(c) * sizeof(float2), "mass parts"));
@@ -375,7 +375,7 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
         }
         ck(cudaMemcpyAsync(d->h_scan[k], c.scan, sizeof(ScanCounters), cudaMemcpyDeviceToHost, d->stream),
            "stats D2H");
-        if (c.utility) {
+        if (c.utility && h->step % c.utility == 0) {
             ck(cudaMemcpyAsync(d->h_mass_count[k], c.mass_count, uint64_t(c.n_slots) * 4, cudaMemcpyDeviceToHost,
                                d->stream),
                "mass count D2H");
@@ -527,6 +527,8 @@ int kvr_dev_utility(kvr_dev *d, uint32_t k, kvr_mass_run *out, uint32_t *counts)
         if (d->in_flight[k])
             throw std::runtime_error("the step of this ring slot has not been waited for");
         const DevCtx &c = d->base;
+        if (d->launched[k] % c.utility)
+            throw std::runtime_error("K-mass did not run on that step (geometry.utility)");
         std::memcpy(counts, d->h_mass_count[k], uint64_t(c.n_slots) * 4);
         for (uint32_t s = 0; s < c.n_slots; ++s)
             std::memcpy(out + uint64_t(s) * c.W, d->h_mass[k] + uint64_t(s) * c.W,

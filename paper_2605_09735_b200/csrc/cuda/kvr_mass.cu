@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(1024) k_mass_rows(DevCtx c) {
     const uint32_t n_split = (c.W + c.far_cap + kSplitRows - 1) / kSplitRows;
     const uint32_t split = blockIdx.x % n_split, slot = blockIdx.x / n_split;
     const kvr_slot_state st = slots[slot];
-    if (!st.live)
+    if (!st.live || h->step % c.utility) // (b200.utility_every: not measured this step)
         return;
     const uint64_t w = st.written, lo = w > c.W ? w - c.W : 0;
     const uint32_t n_far = st.far_count, n = n_far + uint32_t(w - lo);
@@ -160,6 +160,8 @@ __global__ void __launch_bounds__(kMassThreads) k_mass_runs(DevCtx c) {
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
     const uint32_t slot = blockIdx.x;
+    if (h->step % c.utility)
+        return;
     const kvr_slot_state st = slots[slot];
     kvr_mass_run *runs = c.mass_runs + uint64_t(slot) * c.W;
     const uint64_t w = st.written, lo = w > c.W ? w - c.W : 0;

@@ -735,10 +735,12 @@ std::vector<std::vector<kvr_mass_run>> DeviceStep::utility_runs(uint64_t step) {
     collect(step);
     const uint32_t k = uint32_t(step & 1);
     const uint32_t W = m.g.near_window;
+    std::vector<std::vector<kvr_mass_run>> out(m.g.n_slots);
+    if (!m.g.utility || step % m.g.utility)
+        return out; // K-mass did not run on this step
     std::vector<kvr_mass_run> runs(uint64_t(m.g.n_slots) * W);
     std::vector<uint32_t> counts(m.g.n_slots);
     ck(kvr_dev_utility(m.dev, k, runs.data(), counts.data()));
-    std::vector<std::vector<kvr_mass_run>> out(m.g.n_slots);
     const std::vector<kvr_slot_state> &slots = m.launched_slots[k];
     for (uint32_t s = 0; s < m.g.n_slots && s < slots.size(); ++s)
         if (slots[s].live)

@@ -372,7 +372,9 @@ struct ScenarioDriver::Impl {
         g.use_graph = b.graph;
         if (b.utility != "synthetic" && b.utility != "attention")
             raise(Errc::bad_config, "b200.utility must be synthetic or attention");
-        g.utility = b.utility == "attention";
+        if (b.utility_every == 0)
+            raise(Errc::bad_config, "b200.utility_every must be >= 1");
+        g.utility = b.utility == "attention" ? b.utility_every : 0;
         g.utility_layer = b.utility_layer < 0 ? g.layers - 1 : uint32_t(b.utility_layer);
         if (g.utility && (!b.attention || g.utility_layer >= g.layers))
             raise(Errc::bad_config, "b200.utility = attention needs the attention and utility_layer < layers");
@@ -718,9 +720,10 @@ struct ScenarioDriver::Impl {
         }
 
         prof.lap(2);
-        if (measured_utility && t >= 2 && dev->launched(t - 2)) {
+        if (measured_utility && t >= 2 && dev->launched(t - 2) && (t - 2) % cfg.b200.utility_every == 0) {
             // attention-utility observations measured by K-mass two steps back (the
-            // newest step the device has finished), for sessions still decoding
+            // newest step the device has finished), for sessions still decoding; steps
+            // K-mass skips (utility_every) bring no observations
             std::unordered_set<SessionId> decoding;
             for (const Req &r : live)
                 if (!r.eos)
@@ -1430,6 +1433,7 @@ static ScenarioConfig config_from_json(const ojson &j) {
         take(p, "prefill_budget", c.b200.prefill_budget);
         take(p, "utility", c.b200.utility);
         take(p, "utility_layer", c.b200.utility_layer);
+        take(p, "utility_every", c.b200.utility_every);
         take(p, "shard_rank", c.b200.shard_rank);
         take(p, "shard_world", c.b200.shard_world);
     }

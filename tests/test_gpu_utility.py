@@ -59,6 +59,20 @@ def test_utility_mass_with_far_summaries():
     assert ob.check_driver_utility(d) <= 1e-4
 
 
+def test_utility_every_n_steps():
+    """utility_every = 3: K-mass runs on steps divisible by 3 only; the other steps
+    report no observations, and the measured ones still match the oracle."""
+    cfg = json.loads(read("far_config.json"))
+    cfg["steps"] = 121  # the last step (120) is a measured one
+    cfg["b200"] = dict(kv_heads=1, head_dim=64, utility="attention", utility_every=3, check=True)
+    d = kv.Driver(cfg, device=0)
+    d.run()
+    checked, bad, first = d.device_check()
+    assert checked == cfg["steps"] and bad == 0, first
+    assert ob.check_driver_utility(d) <= 1e-4
+    assert all(not r for r in d.device().utility(119))
+
+
 def test_measured_utility_drives_placement():
     """With measured observations the placement loop still keeps every audit (one
     commit per live session, device K-scan == host reduce()), and its far-view
