@@ -67,7 +67,6 @@ __global__ void k_blob(DevCtx c) {
 // ---------------------------------------------------------------------------
 // K-write: one CTA per written token (grid-stride), 16 bytes per thread-step.
 
-
 __device__ inline uint16_t f2h_bits(float v) { return __half_as_ushort(__float2half_rn(v)); }
 __device__ inline uint16_t f2b_bits(float v) { return __bfloat16_as_ushort(__float2bfloat16_rn(v)); }
 
