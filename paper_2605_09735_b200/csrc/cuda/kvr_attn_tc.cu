@@ -3,19 +3,24 @@
 // far_view.cpp:113-155 per (layer, q-head), q-head j -> kv-head j / g), with both
 // contractions on the 5th-generation tensor cores.
 //
-// Work item = (slot, layer, kv head); persistent grid, one CTA per SM.
-//   warp 0  producer: 128-row K|V tiles of the window ring by 4-D TMA (32-row
-//           boxes, 128-byte swizzle; boxes without a live row are skipped), far
-//           summary rows by cp.async into the same swizzled layout;
-//   warp 1  TMEM owner + MMA issuer (one thread):
+// Work item = (slot, layer, kv head); persistent grid, one CTA per SM, 384 threads.
+//   warp 0  K producer, warp 2 V producer: each streams its half of the 128-row
+//           tiles through its own ring (3 x 32 KiB stages) — an interior tile half
+//           is ONE 5-D TMA op, window-edge / ring-wrap tiles go as 32-row 4-D
+//           boxes (only boxes with a live row), far summary rows by TMA gather4
+//           folded in front of the tail tile; 128-byte swizzle throughout;
+//   warp 1  TMEM owner + S issuer (one elected lane issues):
 //             S^T[128 rows x 16]  = K_tile[128 x 128] . Qs^T      (K-major A)
+//   warp 3  PV issuer (one elected lane issues):
 //             O^T[128 dims x 16] += V_tile^T[128 x 128] . Ps      (MN-major A)
 //           tcgen05.mma kind::f16, fp32 accumulators in TMEM (S and O double
-//           buffered, 64 columns), completion by tcgen05.commit -> mbarrier;
-//   warps 4-7 softmax/correction warpgroup: thread t owns TMEM lane t, i.e.
-//           token row t of S and head dim t of O. Online softmax in base 2 per
-//           q-head column (cross-warp tile max through shared memory), P written
-//           back as bf16/fp16 for the PV MMA, O folded into fp32 registers.
+//           buffered per warpgroup, 128 columns), completion by tcgen05.commit ->
+//           mbarrier; each issuer tests all barriers of an iteration at once;
+//   warps 4-7, 8-11  two softmax/correction warpgroups, items alternating between
+//           them: thread t owns TMEM lane t, i.e. token row t of S and head dim t
+//           of O. Online softmax in base 2 per q-head column (cross-warp tile max
+//           through shared memory), P written back as bf16/fp16 for the PV MMA, O
+//           folded into fp32 registers; the next item's Q is fetched ahead.
 // Precision: the MMA operands are 16-bit, so q and p are split hi + lo
 // (x = hi + lo, both in the element type) into columns [0, g) and [g, 2g) of
 // the N = 16 operand; S = S_hi + S_lo and O = O_hi + O_lo recover ~16 extra
