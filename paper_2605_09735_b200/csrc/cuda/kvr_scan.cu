@@ -79,15 +79,24 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
     uint32_t *run_of = order + cap;                           // head position -> run index
     uint32_t *run_start = run_of + cap;
     uint32_t *run_cnt = run_start + cap;                      // trains per run -> train base
+    uint64_t *sp_b = reinterpret_cast<uint64_t *>(run_cnt + cap); // span byte offset (staged once)
+    uint64_t *sp_l = sp_b + cap;                                  // span bytes (0: empty span)
 
     const uint32_t n_need = h->n_need;
     if (threadIdx.x == 0)
         s_status = (n_need > kMaxNeeds || h->n_span > cap) ? 4u : 0u;
     __syncthreads();
     const uint64_t tb = c.token_bytes, page = c.page_bytes;
-    auto span_begin = [&](const kvr_span_rec &sp) {
-        return uint64_t(sp.block) * page + uint64_t(sp.slot_begin) * tb;
-    };
+    // every span's byte range staged in shared memory by all threads at once: the
+    // per-need insertion sort below then compares in shared memory instead of
+    // chasing dependent global loads
+    if (!s_status)
+        for (uint32_t i = threadIdx.x; i < h->n_span; i += blockDim.x) {
+            const kvr_span_rec sp = spans[i];
+            sp_b[i] = uint64_t(sp.block) * page + uint64_t(sp.slot_begin) * tb;
+            sp_l[i] = uint64_t(sp.slot_count) * tb;
+        }
+    __syncthreads();
 
     // ---- 1. stage: per-need insertion sort by (offset, length) + fusion ----
     uint32_t n_desc = 0;
@@ -97,14 +106,12 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
             uint32_t *ord = sidx + nd.span_begin;
             uint32_t m = 0, dcount = 0;
             for (uint32_t k = 0; k < nd.span_count; ++k) {
-                const kvr_span_rec &sp = spans[nd.span_begin + k];
-                if (sp.slot_count == 0)
+                const uint64_t b = sp_b[nd.span_begin + k], len = sp_l[nd.span_begin + k];
+                if (len == 0)
                     continue;
-                const uint64_t b = span_begin(sp), len = uint64_t(sp.slot_count) * tb;
                 uint32_t at = m++;
                 while (at > 0) {
-                    const kvr_span_rec &o = spans[ord[at - 1]];
-                    const uint64_t ob = span_begin(o), ol = uint64_t(o.slot_count) * tb;
+                    const uint64_t ob = sp_b[ord[at - 1]], ol = sp_l[ord[at - 1]];
                     if (ob < b || (ob == b && ol <= len))
                         break;
                     ord[at] = ord[at - 1];
@@ -114,10 +121,9 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
             }
             uint64_t end = 0;
             for (uint32_t k = 0; k < m; ++k) {
-                const kvr_span_rec &sp = spans[ord[k]];
-                if (k == 0 || span_begin(sp) != end)
+                if (k == 0 || sp_b[ord[k]] != end)
                     ++dcount;
-                end = span_begin(sp) + uint64_t(sp.slot_count) * tb;
+                end = sp_b[ord[k]] + sp_l[ord[k]];
             }
             sm.need_m[i] = m;
             sm.need_d[i] = dcount;
@@ -142,8 +148,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
                 uint32_t d = sm.need_base[i] - 1;
                 uint64_t end = 0;
                 for (uint32_t k = 0; k < sm.need_m[i]; ++k) {
-                    const kvr_span_rec &sp = spans[sidx[first + k]];
-                    const uint64_t b = span_begin(sp), len = uint64_t(sp.slot_count) * tb;
+                    const uint64_t b = sp_b[sidx[first + k]], len = sp_l[sidx[first + k]];
                     if (k == 0 || b != end) {
                         ++d;
                         d_off[d] = b;
@@ -361,7 +366,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
 
 } // namespace
 
-size_t scan_dynamic_smem(uint32_t cap) { return size_t(cap) * (3 * 8 + 8 * 4); }
+size_t scan_dynamic_smem(uint32_t cap) { return size_t(cap) * (5 * 8 + 8 * 4); }
 
 void launch_scan(const DevCtx &c, cudaStream_t s) {
     k_scan<<<1, kScanThreads, scan_dynamic_smem(c.max_scan), s>>>(c);
