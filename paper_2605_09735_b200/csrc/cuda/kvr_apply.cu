@@ -387,14 +387,35 @@ template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c) {
 #pragma unroll
         for (int i = 0; i < 16 / E; ++i)
             acc[i] = 0.0;
+        // 2-byte lanes are multiples of 1/128 in [-1, 1) and a chunk has <= 512 rows, so
+        // every partial sum is exact in fp32: summing in fp32 and widening once gives
+        // the same double as the reference's double sum (far_view.cpp:36-46), without
+        // a conversion and an FP64 add per lane per row
+        float accf[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
         for (uint32_t r = op.run_begin; r < op.run_begin + op.run_count; ++r) {
             const kvr_presum_run run = runs[r];
             uint8_t *dst = c.arena + uint64_t(run.block) * c.page_bytes + uint64_t(run.slot) * c.token_bytes + 16 * col;
             for (uint32_t k = 0; k < run.count; ++k) {
                 const int4 v = payload16<kKind>(c, tab, op.session, run.token + k, 16 * col);
                 *reinterpret_cast<int4 *>(dst + uint64_t(k) * c.token_bytes) = v;
-                add_chunk<E>(c, v, acc);
+                if constexpr (kKind == kLanes16) {
+                    const uint32_t w[4] = {uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w)};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const float2 f = c.elem_kind == KVR_ELEM_BF16
+                                             ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w[i]))
+                                             : __half22float2(*reinterpret_cast<const __half2 *>(&w[i]));
+                        accf[2 * i] += f.x, accf[2 * i + 1] += f.y;
+                    }
+                } else {
+                    add_chunk<E>(c, v, acc);
+                }
             }
+        }
+        if constexpr (kKind == kLanes16) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+                acc[i] = double(accf[i]);
         }
         store_mean<E>(c, c.stash + (uint64_t(op.dev_slot) * c.max_chunks + op.chunk) * c.token_bytes + 16 * col,
                       acc);
