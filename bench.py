@@ -162,7 +162,7 @@ def peaks() -> dict:
 
 class Clocks:
     """SM clock and throttle reasons sampled DURING the timed region
-    (B200_PROFILING.md clocks line): NVML polled every ~1 ms on a thread, so even
+    (B200_PROFILING.md clocks line): NVML polled every 2 ms on a thread, so even
     a short timed region gets samples; nvidia-smi as the fallback."""
     NAMES = {"hw_slowdown": "nvmlClocksEventReasonHwSlowdown",
              "hw_thermal_slowdown": "nvmlClocksEventReasonHwThermalSlowdown",
@@ -187,7 +187,7 @@ class Clocks:
             self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
             self.reasons.update(k for k, m in masks.items() if r & m)
-            time.sleep(0.001)
+            time.sleep(0.002)
 
     def __enter__(self):
         try:
