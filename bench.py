@@ -178,24 +178,27 @@ class Clocks:
         self.stop = threading.Event()
         self.thread = None
 
-    def _poll(self):
-        import pynvml as nv
-        h = nv.nvmlDeviceGetHandleByIndex(self.device)
-        self.max_sm.append(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
-        masks = {k: getattr(nv, v) for k, v in self.NAMES.items() if hasattr(nv, v)}
+    def _poll(self, nv, h, masks):
         while not self.stop.is_set():
             self.sm.append(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM))
             r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
             self.reasons.update(k for k, m in masks.items() if r & m)
+            self.first.set()
             time.sleep(0.002)
 
     def __enter__(self):
+        # NVML set up here, before the timed region (its first calls can take tens of
+        # ms); the poll thread is running and has one sample when this returns
         try:
             import pynvml as nv
             nv.nvmlInit()
-            self.thread = threading.Thread(target=self._poll, daemon=True)
+            h = nv.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_sm.append(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+            masks = {k: getattr(nv, v) for k, v in self.NAMES.items() if hasattr(nv, v)}
+            self.first = threading.Event()
+            self.thread = threading.Thread(target=self._poll, args=(nv, h, masks), daemon=True)
             self.thread.start()
-            time.sleep(0.01)  # first sample before the timed region starts
+            self.first.wait(timeout=1.0)
         except Exception:
             self.thread = None
         return self
