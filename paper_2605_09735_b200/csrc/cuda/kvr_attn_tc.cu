@@ -833,7 +833,7 @@ bool attn_tc_maps(const DevCtx &c, TcMaps *maps) {
     auto enc = [&](CUtensorMap *m, uint32_t rank, void *base, const cuuint64_t *dims, const cuuint64_t *strides,
                    const cuuint32_t *box) {
         return encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, rank, base, dims, strides, box, estr,
-                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
     // 32-row boxes: (head_dim, 2*Hkv heads, R rows, L*n_slots)
