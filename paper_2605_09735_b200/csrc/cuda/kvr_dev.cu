@@ -173,6 +173,8 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
             g.max_trains = 2048;
         if (g.max_scan_descs & (g.max_scan_descs - 1))
             throw std::runtime_error("max_scan_descs must be a power of two");
+        if (scan_dynamic_smem(g.max_scan_descs) > (192u << 10)) // K-scan stages its arrays in shared memory
+            throw std::runtime_error("max_scan_descs too large for K-scan's shared memory (<= 2048)");
         d->g = g;
         ck(cudaSetDevice(g.device), "cudaSetDevice");
         cudaDeviceProp prop;
