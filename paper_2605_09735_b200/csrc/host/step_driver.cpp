@@ -385,6 +385,8 @@ struct ScenarioDriver::Impl {
     }
 
     void setup_paged() {
+        if (cfg.b200.utility_every == 0)
+            raise(Errc::bad_config, "b200.utility_every must be >= 1");
         PagerConfig pc = cfg.pager;
         pc.arena_pages = arena_pages();
         if (cfg.b200.device >= 0) {

@@ -74,3 +74,11 @@ def test_attention_weights_oracle_is_attend(n_far, n_near, layers, kvh, hd, kind
             for i in range(hd):
                 want = sum(w[s] * rows[s][v_off + i] for s in range(len(rows)))
                 assert abs(out[i] - want) <= 1e-6 * max(1.0, abs(want))
+
+
+def test_utility_every_must_be_positive():
+    cfg = far_cfg()
+    cfg["b200"] = {"utility": "attention", "utility_every": 0}
+    with pytest.raises(kv.KvrailError) as e:
+        kv.Driver(cfg)
+    assert e.value.code == "BadConfig" and "utility_every" in str(e.value)
