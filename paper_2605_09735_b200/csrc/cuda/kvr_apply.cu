@@ -224,10 +224,10 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
 // Decode queries for live slots: [slot][L][Hq][hd], exact in the KV element type
 // (kvo_fill_query in the oracle). One CTA per (slot, layer); one hash per 8 lanes.
 __global__ void __launch_bounds__(256) k_query(DevCtx c) {
-    __shared__ float val[256]; // (b - 128) / 128
-    for (uint32_t i = threadIdx.x; i < 256; i += blockDim.x)
-        val[i] = float(int(i) - 128) / 128.0f;
-    __syncthreads();
+    // byte k of x -> (b - 128) / 128, exactly: b placed in the mantissa of 2^23 + b
+    auto val = [](uint32_t x, uint32_t k) {
+        return fmaf(__uint_as_float(__byte_perm(x, 0x4B000000u, 0x7440 | k)), 0.0078125f, -65537.f);
+    };
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
     const uint32_t per_layer = c.Hq * c.hd;
@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
             const uint32_t head = (8 * i) >> hd_shift, d8 = i & ((c.hd >> 3) - 1);
             const uint64_t x = splitmix64(base ^ (uint64_t(head) << 8) ^ d8);
             const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
-            q[2 * i] = make_float4(val[lo & 0xffu], val[(lo >> 8) & 0xffu], val[(lo >> 16) & 0xffu], val[lo >> 24]);
-            q[2 * i + 1] = make_float4(val[hi & 0xffu], val[(hi >> 8) & 0xffu], val[(hi >> 16) & 0xffu], val[hi >> 24]);
+            q[2 * i] = make_float4(val(lo, 0), val(lo, 1), val(lo, 2), val(lo, 3));
+            q[2 * i + 1] = make_float4(val(hi, 0), val(hi, 1), val(hi, 2), val(hi, 3));
         }
     }
 }
