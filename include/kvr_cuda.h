@@ -20,8 +20,13 @@ extern "C" {
 
 enum { KVR_ELEM_F32 = 0, KVR_ELEM_F16 = 1, KVR_ELEM_BF16 = 2 };
 enum { KVR_PAYLOAD_BYTES = 0, KVR_PAYLOAD_LANES = 1 };
+/* decode queries: EXACT = byte fields (b - 128) / 128, exact in the KV type (the
+ * tensor-core kernel's lo half is 0); F32 = 24-bit random fp32 in [-1, 1), not
+ * representable in 16 bits (exercises the hi + lo query split) */
+enum { KVR_QUERY_EXACT = 0, KVR_QUERY_F32 = 1 };
 #define KVR_NO_SLOT 0xffffffffu
 #define KVR_SUMMARY_BASE (1ull << 40) /* summary slots' logical tokens, scenario.cpp:41 */
+#define KVR_MAX_SCAN_NEEDS 2048u      /* K-scan: stage needs per step */
 
 typedef struct kvr_geometry {
     int32_t device;
@@ -52,6 +57,9 @@ typedef struct kvr_geometry {
     uint32_t utility;       /* N >= 1: K-mass measures attention-utility observations on
                                steps with step % N == 0 (0: off) */
     uint32_t utility_layer; /* probe layer of K-mass */
+    uint32_t lane_shift;    /* 2-byte lanes payload: lane = (b - 128) / 2^lane_shift
+                               (0 = 7: [-1, 1); 3 = "wide" [-16, 16), peaked softmaxes) */
+    uint32_t query_mode;    /* KVR_QUERY_* */
 } kvr_geometry;
 
 /* K-mass output: one run of window rows mapped to one arena block, with the
@@ -131,6 +139,10 @@ typedef struct kvr_slot_state {
     uint32_t live;          /* attention runs for this slot this step */
     uint32_t far_begin;     /* index into the far-id array */
     uint32_t far_count;     /* selected far chunks (<= far_cap) */
+    /* tokens [stage_lo, stage_hi) of this slot are covered by this step's near-window
+       staged spans: K-gather is their only window writer this step (K-write and
+       K-prime leave those ring rows to it), so the window consumes the staged bytes */
+    uint64_t stage_lo, stage_hi;
 } kvr_slot_state;
 
 /* step results (written by the device, read back one step later) */
@@ -178,6 +190,21 @@ enum {
     KVR_BUF_SMAP = 9,    /* [slot][max_chunks] u32 summary-slot map */
 };
 int kvr_dev_read(kvr_dev *d, int buffer, uint64_t offset, uint64_t bytes, void *out);
+/* K-gather's DESTINATION bytes of the last step's staged tokens [tok_begin, tok_begin +
+ * count) in train order (the order of the trains' descriptors): each token
+ * as the reference lays it out (token_bytes, layer rows [K_l|V_l] concatenated), read
+ * back from the window ring (near spans) or the far rows (far spans). A row the window
+ * does not hold is read from the arena instead. `in_window` (count bytes, may be NULL):
+ * 1 delivered; 0 a near row behind the live window (older than written - W*, not part
+ * of the window by definition); 2 not held for another reason (never expected). */
+int kvr_dev_read_staged(kvr_dev *d, uint64_t tok_begin, uint64_t count, void *out, uint8_t *in_window);
+/* fault injection for the parity tests (never set by the product path):
+ * KVR_FAULT_DROP_SPAN: K-gather skips gather-list span `arg` (~0 = off,
+ *                      KVR_FAULT_ALL = every span);
+ * KVR_FAULT_SHIFT_ROWS: K-gather writes near rows `arg` ring rows too far (0 = off). */
+enum { KVR_FAULT_DROP_SPAN = 1, KVR_FAULT_SHIFT_ROWS = 2 };
+#define KVR_FAULT_ALL (~1ull)
+int kvr_dev_fault(kvr_dev *d, int what, uint64_t arg);
 int kvr_dev_buffer_bytes(kvr_dev *d, int buffer, uint64_t *out);
 /* time `iters` replays of the last launched step's attention kernel alone
  * (CUDA events on the launch stream); used by bench.py for the roofline */

@@ -69,7 +69,11 @@ public:
     void slot_state(uint32_t slot, SessionId sid, uint64_t written, bool live);
     void need(uint32_t slot, SessionId sid, TrainKind kind, std::span<const StagedSpan> spans,
               std::span<const uint64_t> first_tokens);
-    void prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end);
+    /// Window rows [tok_begin, tok_end) of `slot` copied from the arena through the
+    /// page table (an aliased prefix). `src`: the session owning those rows (the alias
+    /// source) — its pending rows are written before K-prime reads them.
+    static constexpr SessionId kNoPrimeSource = 0xffffffffu;
+    void prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end, SessionId src = kNoPrimeSource);
     void far_selection(uint32_t slot, std::span<const uint64_t> chunk_ids);
 
     /// Seal the step descriptor, publish it and launch the step (async).
@@ -108,6 +112,12 @@ public:
     std::vector<uint64_t> far_selection_of(uint32_t slot) const;
     /// Last K-scan result: trains (desc_begin/count index `descs`).
     void read_scan(std::vector<kvr_train> &trains, std::vector<kvr_descriptor> &descs);
+    /// K-gather's destination bytes of the last step's staged tokens [tok_begin, +count)
+    /// in train order, token-major (kvr_dev_read_staged); in_window[i] = 0 for a token
+    /// with a row the window does not hold (read from the arena instead).
+    void read_staged(uint64_t tok_begin, uint64_t count, void *out, uint8_t *in_window);
+    /// Test hook (kvr_dev_fault): KVR_FAULT_DROP_SPAN / KVR_FAULT_SHIFT_ROWS in K-gather.
+    void fault(int what, uint64_t arg);
 
     struct Impl; // public so the arena-backed PayloadStore can reach it
 

@@ -32,7 +32,9 @@ struct B200Config {
     uint32_t head_dim = 0;    // 0: kv_head_dim / kv_heads
     uint32_t q_heads = 0;     // 0: kv_heads (MHA); GQA group = q_heads / kv_heads
     std::string payload = "bytes"; // "bytes": reference fill_token_payload; "lanes": float
-                                   // lane pattern rounded to dtype (finite for attention)
+                                   // lane pattern rounded to dtype (finite for attention);
+                                   // "wide": the same bytes as lanes of [-16, 16) (peaked softmax)
+    std::string query = "exact";   // decode queries: "exact" in the KV type | "f32" (24-bit)
     std::string dtype = "auto";    // fp16 | bf16 | fp32 | auto (elem_bytes 4 -> fp32, 2 -> fp16)
     bool trace = false;            // record the per-step parity trace
     bool attention = true;         // run the window attention kernel each step
@@ -153,6 +155,12 @@ public:
     std::vector<LiveInfo> live() const;
     /// b200.check results: steps checked, mismatching steps, first mismatch.
     void device_check(uint64_t &checked, uint64_t &mismatches, std::string &first) const;
+    /// b200.trace on a device: staged tokens whose trace hash was read from K-gather's
+    /// destination (window ring / far rows), near rows behind the live window (read from
+    /// the arena: not part of the window), and rows missing from the window otherwise.
+    void staged_rows(uint64_t &delivered, uint64_t &behind, uint64_t &missing) const;
+    /// Test hook (kvr_dev_fault): corrupt K-gather on every later step.
+    void fault(int what, uint64_t arg);
 
 private:
     struct Impl;

@@ -324,6 +324,13 @@ int kvr_driver_workload_hash(kvr_driver *d, uint64_t *out);
  * mismatching steps and the first mismatch description. */
 int kvr_driver_device_check(kvr_driver *d, uint64_t *checked, uint64_t *mismatches, char *buf,
                             uint64_t cap);
+/* b200.trace on a device: staged tokens the trace hashed from K-gather's destination
+ * (window ring / far rows), near rows behind the live window (hashed from the arena:
+ * not part of the window) and rows missing from the window for any other reason. */
+int kvr_driver_staged_rows(kvr_driver *d, uint64_t *delivered, uint64_t *behind, uint64_t *missing);
+/* Test hook (fault injection, kvr_dev_fault): K-gather drops a span (KVR_FAULT_DROP_SPAN)
+ * or misplaces near rows (KVR_FAULT_SHIFT_ROWS) on every later step. */
+int kvr_driver_fault(kvr_driver *d, int what, uint64_t arg);
 
 /* ---- B200 device (kvrail::DeviceStep) ---------------------------------------
  * A device context: arena, page-table mirror, window ring and the step graph

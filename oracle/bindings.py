@@ -34,6 +34,10 @@ def oracle() -> C.CDLL:
                                              C.c_void_p]
         lib.kvo_fill_query.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
                                        C.c_uint32, C.c_int, f]
+        lib.kvo_fill_query_mode.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint32, C.c_uint32,
+                                            C.c_uint32, C.c_int, C.c_int, f]
+        lib.kvo_fill_token_lanes_shift.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, C.c_int,
+                                                   C.c_uint32, C.c_void_p]
         lib.kvo_summarize_chunk.argtypes = [f, C.c_uint32, C.c_uint64, f]
         lib.kvo_select_chunks.argtypes = [C.POINTER(C.c_double), C.c_uint64, C.c_uint32,
                                           C.POINTER(C.c_uint64)]
@@ -91,9 +95,9 @@ def ref_scenario(config: dict, trace: bool = False):
 
 
 # ---- helpers ---------------------------------------------------------------------
-def fill_query(seed, session, step, layer, head, head_dim, elem_kind):
+def fill_query(seed, session, step, layer, head, head_dim, elem_kind, mode=0):
     out = (C.c_float * head_dim)()
-    oracle().kvo_fill_query(seed, session, step, layer, head, head_dim, elem_kind, out)
+    oracle().kvo_fill_query_mode(seed, session, step, layer, head, head_dim, elem_kind, mode, out)
     return list(out)
 
 
@@ -147,7 +151,7 @@ def check_driver_utility(driver, layer=None) -> float:
             far_imgs += as_floats(dev.far_row(slot, chunk), g.elem_kind)
         rows = [0.0] * (written - lo)
         for qh in range(g.q_heads):
-            q = fill_query(g.seed, session, step, layer, qh, g.head_dim, g.elem_kind)
+            q = fill_query(g.seed, session, step, layer, qh, g.head_dim, g.elem_kind, g.query_mode)
             w = attention_weights(window, written - lo, g.layers, g.kv_heads, g.head_dim, g.elem_kind,
                                   layer, qh // group, q, far_imgs, len(far))
             for i in range(written - lo):
@@ -225,7 +229,7 @@ def check_driver_window_and_attention(driver, far_images_of=None, only_slots=Non
                 if heads is not None and (layer, qh) not in heads:
                     continue
                 base = (layer * g.q_heads + qh) * g.head_dim
-                q = fill_query(g.seed, session, step, layer, qh, g.head_dim, g.elem_kind)
+                q = fill_query(g.seed, session, step, layer, qh, g.head_dim, g.elem_kind, g.query_mode)
                 assert q == q_dev[base:base + g.head_dim], "device query differs from the oracle"
                 want = attend_window(window, written - lo, g.layers, g.kv_heads, g.head_dim,
                                      g.elem_kind, layer, qh // group, q, far_imgs, len(far))

@@ -124,21 +124,41 @@ static float load_lane(const void *in, uint64_t i, int elem_kind) {
     return kvo_bf16_to_float(((const uint16_t *)in)[i]);
 }
 
-void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint64_t lanes,
-                          int elem_kind, void *out) {
+void kvo_fill_token_lanes_shift(uint64_t seed, uint32_t session, uint64_t token, uint64_t lanes,
+                                int elem_kind, uint32_t shift, void *out) {
     if (elem_kind == 0) { /* fp32: the reference float pattern, scenario.cpp:198-201 */
         for (uint64_t l = 0; l < lanes; ++l)
             store_lane(out, l, lane_value(pattern(seed, session, token, l)), elem_kind);
         return;
     }
     /* 2-byte lanes: one splitmix64 per group of 8 lanes (16 bytes; tweaked by
-     * bit 62), lane j of the group takes byte j: (b - 128) / 128, exact in fp16
-     * and bf16 */
+     * bit 62), lane j of the group takes byte j: (b - 128) / 2^shift, exact in fp16
+     * and bf16 (shift 7: [-1, 1); shift 3, "wide": [-16, 16)) */
     for (uint64_t l = 0; l < lanes; ++l) {
         const uint64_t x = pattern(seed, session, token, (l >> 3) ^ 0x4000000000000000ull);
         const uint32_t b = (uint32_t)((x >> (8 * (l & 7))) & 0xffu);
-        store_lane(out, l, (float)((int)b - 128) / 128.0f, elem_kind);
+        store_lane(out, l, (float)((int)b - 128) / (float)(1u << shift), elem_kind);
     }
+}
+
+void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint64_t lanes,
+                          int elem_kind, void *out) {
+    kvo_fill_token_lanes_shift(seed, session, token, lanes, elem_kind, 7, out);
+}
+
+void kvo_fill_query_mode(uint64_t seed, uint32_t session, uint64_t step, uint32_t layer,
+                         uint32_t head, uint32_t head_dim, int elem_kind, int mode, float *out) {
+    if (mode == 1) { /* KVR_QUERY_F32: two 24-bit lanes per splitmix64, (u - 2^23) / 2^23 */
+        for (uint32_t d = 0; d < head_dim; ++d) {
+            uint64_t h = kvo_splitmix64(seed ^ (0x52ull << 56) ^ ((uint64_t)session << 32) ^
+                                        (step << 20) ^ ((uint64_t)layer << 12) ^
+                                        ((uint64_t)head << 8) ^ (d >> 1));
+            uint32_t u = (uint32_t)(h >> (32 * (d & 1)));
+            out[d] = (float)((int32_t)(u >> 8) - 8388608) * (1.0f / 8388608.0f);
+        }
+        return;
+    }
+    kvo_fill_query(seed, session, step, layer, head, head_dim, elem_kind, out);
 }
 
 void kvo_fill_query(uint64_t seed, uint32_t session, uint64_t step, uint32_t layer,

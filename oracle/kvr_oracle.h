@@ -35,6 +35,10 @@ void kvo_fill_token_payload(uint64_t seed, uint32_t session, uint64_t token, uin
  * = byte j: (b - 128) / 128, exact in both types. */
 void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint64_t lanes,
                           int elem_kind, void *out);
+/* The same with lane = (b - 128) / 2^shift (shift 7 = kvo_fill_token_lanes; shift 3 =
+ * the "wide" payload, [-16, 16): large logits, peaked softmaxes). */
+void kvo_fill_token_lanes_shift(uint64_t seed, uint32_t session, uint64_t token, uint64_t lanes,
+                                int elem_kind, uint32_t shift, void *out);
 
 /* Synthetic decode query for (seed, session, step, layer, q_head): hd floats,
  * lane d = (b - 128) / 128 with b the byte d & 7 of
@@ -43,6 +47,12 @@ void kvo_fill_token_lanes(uint64_t seed, uint32_t session, uint64_t token, uint6
  * element type. (A B200-side synthetic input: the reference has no query.) */
 void kvo_fill_query(uint64_t seed, uint32_t session, uint64_t step, uint32_t layer,
                     uint32_t head, uint32_t head_dim, int elem_kind, float *out);
+/* mode 0 = kvo_fill_query; mode 1 (KVR_QUERY_F32): lane d = (u - 2^23) / 2^23 with u the
+ * top 24 bits of 32-bit half d & 1 of h = splitmix64(seed ^ 0x52<<56 ^ session<<32 ^
+ * step<<20 ^ layer<<12 ^ head<<8 ^ (d >> 1)): random fp32 in [-1, 1), generally not
+ * representable in fp16 / bf16 (the tensor-core kernel's lo query half is non-zero). */
+void kvo_fill_query_mode(uint64_t seed, uint32_t session, uint64_t step, uint32_t layer,
+                         uint32_t head, uint32_t head_dim, int elem_kind, int mode, float *out);
 
 float kvo_half_to_float(uint16_t h);
 float kvo_bf16_to_float(uint16_t h);

@@ -50,16 +50,20 @@ __global__ void k_cow(DevCtx c) {
     }
 }
 
+// Host payload bytes (Pager::write_tokens): blob offsets and token_bytes are
+// multiples of 16, so every op moves int4s, spread over the whole grid.
 __global__ void k_blob(DevCtx c) {
     const kvr_step_header *h = hdr(c);
     const kvr_blob_op *ops = section<kvr_blob_op>(c, h->off_blob_ops);
     const uint8_t *blob = c.desc + h->off_blob;
-    for (uint32_t i = blockIdx.x; i < h->n_blob; i += gridDim.x) {
+    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, stride = uint64_t(gridDim.x) * blockDim.x;
+    for (uint32_t i = 0; i < h->n_blob; ++i) {
         const kvr_blob_op op = ops[i];
-        uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot) * c.token_bytes;
-        const uint8_t *src = blob + op.blob_offset;
-        const uint64_t n = uint64_t(op.count) * c.token_bytes;
-        for (uint64_t k = threadIdx.x; k < n; k += blockDim.x)
+        int4 *dst = reinterpret_cast<int4 *>(c.arena + uint64_t(op.block) * c.page_bytes +
+                                             uint64_t(op.slot) * c.token_bytes);
+        const int4 *src = reinterpret_cast<const int4 *>(blob + op.blob_offset);
+        const uint64_t n16 = uint64_t(op.count) * c.token_bytes / 16;
+        for (uint64_t k = tid; k < n16; k += stride)
             dst[k] = src[k];
     }
 }
@@ -102,17 +106,18 @@ __device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab,
             w[i] = tab(splitmix64(base ^ (lane0 + i)));
     } else if constexpr (kKind == kLanes16) {
         // 2-byte lanes (B200 extension, kvo_fill_token_lanes): one splitmix64 per
-        // 8 lanes (16 bytes), lane j = byte j: (b - 128) / 128, exact in fp16 / bf16
+        // 8 lanes (16 bytes), lane j = byte j: (b - 128) / 2^shift, exact in fp16 / bf16
         // (arithmetic, no table: byte_perm places byte b in the mantissa of 2^23 + b,
-        // one exact FFMA maps it to (b - 128) / 128, and a pack converts two lanes)
+        // one exact FFMA maps it to (b - 128) / 2^shift, and a pack converts two lanes)
         const uint64_t x = splitmix64(base ^ 0x4000000000000000ull ^ (b0 >> 4));
         const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
         const bool bf = c.elem_kind == KVR_ELEM_BF16;
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);
-            const float v0 = fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | k)), 0.0078125f, -65537.f);
-            const float v1 = fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | (k + 1))), 0.0078125f, -65537.f);
+            const float v0 = fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | k)), c.lane_scale, -c.lane_bias);
+            const float v1 =
+                fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | (k + 1))), c.lane_scale, -c.lane_bias);
             if (bf) {
                 const __nv_bfloat162 p = __floats2bfloat162_rn(v0, v1);
                 w[i] = *reinterpret_cast<const uint32_t *>(&p);
@@ -189,11 +194,9 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
             tok = op.token + k;
             dst = c.arena + uint64_t(op.block) * c.page_bytes + (op.slot + k) * c.token_bytes;
             ring = nullptr;
-            if (op.dev_slot != KVR_NO_SLOT) {
-                const uint64_t w = slots[op.dev_slot].written;
-                if (tok < w && tok + c.W >= w) // inside the live window after this step
-                    ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
-            }
+            // inside the live window after this step and not delivered by K-gather
+            if (op.dev_slot != KVR_NO_SLOT && ring_owned_by_writer(c, slots[op.dev_slot], tok))
+                ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
         }
         if (op.source == 0) {
             int4 v[kPer];
@@ -239,6 +242,17 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
                               (h->step << 20) ^ (uint64_t(l) << 12);
         float4 *q = reinterpret_cast<float4 *>(c.q + uint64_t(sl) * per_layer);
         const uint32_t hd_shift = __ffs(c.hd) - 1; // head_dim is a power of two (32/64/128)
+        if (c.query_mode == KVR_QUERY_F32) { // two 24-bit lanes per hash (kvo_fill_query_mode)
+            const uint64_t fbase = base ^ (0x52ull << 56) ^ (0x51ull << 56);
+            float2 *q2 = reinterpret_cast<float2 *>(q);
+            for (uint32_t i = threadIdx.x; i < per_layer / 2; i += blockDim.x) {
+                const uint32_t head = (2 * i) >> hd_shift, d2 = i & ((c.hd >> 1) - 1);
+                const uint64_t x = splitmix64(fbase ^ (uint64_t(head) << 8) ^ d2);
+                q2[i] = make_float2(float(int32_t(uint32_t(x) >> 8) - 8388608) * (1.0f / 8388608.0f),
+                                    float(int32_t(uint32_t(x >> 32) >> 8) - 8388608) * (1.0f / 8388608.0f));
+            }
+            continue;
+        }
         for (uint32_t i = threadIdx.x; i < per_layer / 8; i += blockDim.x) { // 8 lanes per hash
             const uint32_t head = (8 * i) >> hd_shift, d8 = i & ((c.hd >> 3) - 1);
             const uint64_t x = splitmix64(base ^ (uint64_t(head) << 8) ^ d8);
@@ -387,8 +401,9 @@ template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c) {
 #pragma unroll
         for (int i = 0; i < 16 / E; ++i)
             acc[i] = 0.0;
-        // 2-byte lanes are multiples of 1/128 in [-1, 1) and a chunk has <= 512 rows, so
-        // every partial sum is exact in fp32: summing in fp32 and widening once gives
+        // 2-byte lanes are multiples of 2^-shift in [-2^(7-shift), 2^(7-shift)) and a chunk
+        // has <= 512 rows, so every partial sum needs <= 7 + 9 + 1 bits and is exact in
+        // fp32: summing in fp32 and widening once gives
         // the same double as the reference's double sum (far_view.cpp:36-46), without
         // a conversion and an FP64 add per lane per row
         float accf[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -459,9 +474,9 @@ __global__ void k_prime(DevCtx c) {
     const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
     for (uint32_t i = 0; i < h->n_prime; ++i) {
         const kvr_prime_op op = ops[i];
-        const uint64_t w = slots[op.slot].written;
+        const kvr_slot_state st = slots[op.slot];
         for (uint64_t tok = op.tok_begin + blockIdx.x; tok < op.tok_end; tok += gridDim.x) {
-            if (!(tok < w && tok + c.W >= w) || tok >= c.max_tokens)
+            if (!ring_owned_by_writer(c, st, tok) || tok >= c.max_tokens)
                 continue;
             const uint32_t gs = c.tmap[uint64_t(op.slot) * c.max_tokens + tok];
             if (gs == kNoMap)
@@ -483,7 +498,7 @@ __global__ void k_prime(DevCtx c) {
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms) {
     k_zero<<<sms * 4, 256, 0, s>>>(c);
     k_cow<<<sms * 4, 256, 0, s>>>(c);
-    k_blob<<<sms, 256, 0, s>>>(c);
+    k_blob<<<sms * 2, 256, 0, s>>>(c);
 }
 
 void launch_presum(const DevCtx &c, cudaStream_t s, int sms) {

@@ -21,10 +21,15 @@
 //           of O. Online softmax in base 2 per q-head column (cross-warp tile max
 //           through shared memory), P written back as bf16/fp16 for the PV MMA, O
 //           folded into fp32 registers; the next item's Q is fetched ahead.
-// Precision: the MMA operands are 16-bit, so q and p are split hi + lo
-// (x = hi + lo, both in the element type) into columns [0, g) and [g, 2g) of
-// the N = 16 operand; S = S_hi + S_lo and O = O_hi + O_lo recover ~16 extra
-// mantissa bits, keeping the 1e-3 bound of the fp32 path.
+// Precision: the MMA operands are 16-bit, so q and p are split into 16-bit terms
+// (x = x_0 + x_1 [+ x_2], each the rounding of the remainder) in column blocks
+// [s*g, (s+1)*g) of the operand, and S / O are the sums of the column blocks. fp16
+// (11-bit significands) uses 2 terms: 22 bits. bf16 (8 bits) uses 3 terms for q
+// (24 bits: a 2-term q left ~2^-17 relative error in every logit, which broke 1e-3
+// with random fp32 queries over large-magnitude KV — measured 1.7e-3) and 3 terms
+// for p when 3g <= 16 (else 2: 16 bits, ~1e-4 of output error). With g = 8 the q
+// operand needs 24 columns: the S MMA then runs at N = 32 (its 4th column block
+// reads the next buffer — finite garbage in S columns nobody reads).
 #include <cstdio>
 #include <type_traits>
 #include <cudaTypedefs.h>
@@ -37,7 +42,7 @@ namespace {
 
 constexpr int kRows = 128;                 // tokens per tile (S: M, PV: K)
 constexpr int kHd = 128;                   // head dim (S: K, PV: M)
-constexpr int kN = 16;                     // MMA N: g hi columns + g lo columns
+constexpr int kN = 16;                     // PV MMA N (and S MMA N unless q needs 24 columns)
 constexpr int kSub = 32;                   // rows per TMA box
 constexpr uint32_t kHalfBytes = kRows * 128; // one 64-dim half of a K or V tile (16 KiB)
 constexpr uint32_t kSideBytes = 2 * kHalfBytes; // a K (or V) tile: two 64-dim halves, 32 KiB
@@ -52,7 +57,17 @@ constexpr uint32_t kSideBytes = 2 * kHalfBytes; // a K (or V) tile: two 64-dim h
 constexpr int kKStages = KVR_TC_KSTAGES, kVStages = KVR_TC_VSTAGES;
 static_assert(kVStages <= 4, "V stage index and phase are packed in 3 bits");
 static_assert(kKStages <= kVStages, "a K ring deeper than the V ring stalls the PV order (4 + 2 hung on B200)");
-constexpr uint32_t kOpBytes = kN * kHd * 2; // one Q or P operand buffer (4 KiB)
+constexpr uint32_t kOpBytes = kN * kHd * 2; // one P operand buffer (4 KiB): 2 column blocks of 8
+constexpr uint32_t kQBytes = 3 * 2048;       // the Q operand: up to 3 column blocks of 8 (24 columns)
+
+/// Split terms and MMA widths of a (T, g) variant.
+template <typename T, int G> struct Splits {
+    static constexpr bool kBf = std::is_same_v<T, __nv_bfloat16>;
+    static constexpr int QS = kBf ? 3 : 2;                    // q terms
+    static constexpr int PS = kBf && 3 * G <= kN ? 3 : 2;     // p terms
+    static constexpr int NQ = QS * G <= 16 ? 16 : 32;         // S MMA N
+    static_assert(QS * G <= 24 && PS * G <= kN, "split columns must fit the operand buffers");
+};
 #ifndef KVR_TC_TILE5D
 #define KVR_TC_TILE5D 1
 #endif
@@ -171,29 +186,37 @@ template <> struct Pack2<__half> {
     }
 };
 
-/// Row k of an N=16 MMA operand held MN-major, unswizzled (8x8 core matrices of
-/// 8 K-rows x 16 B; K-adjacent cores 128 B apart, N halves 2048 B apart): the
-/// thread owning k writes x split as hi (columns [0, G)) + lo (columns [G, 2G))
-/// with two 16-byte stores. Columns >= 2G stay zero.
-template <typename T, int G> __device__ inline void store_split(uint8_t *op, uint32_t k, const float (&x)[G]) {
-    uint32_t wd[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    if constexpr (G == 1) {
-        float2 back;
-        wd[0] = Pack2<T>::round(x[0], 0.f, back);
-        float2 b2;
-        wd[0] = (wd[0] & 0xffffu) | (Pack2<T>::round(x[0] - back.x, 0.f, b2) << 16);
-    } else {
+/// Row k of an MMA operand held MN-major, unswizzled (8x8 core matrices of 8 K-rows
+/// x 16 B; K-adjacent cores 128 B apart, blocks of 8 N-columns 2048 B apart): the
+/// thread owning k writes x split into S terms, term s in columns [s*G, (s+1)*G)
+/// (each term the element-type rounding of what the previous terms left), one
+/// 16-byte store per 8 columns. Columns >= S*G of the last written block stay zero.
+template <typename T, int G, int S> __device__ inline void store_split(uint8_t *op, uint32_t k, const float (&x)[G]) {
+    constexpr int NC = S * G, NB = (NC + 7) / 8; // used columns, 8-column blocks written
+    uint32_t wd[4 * NB];
 #pragma unroll
-        for (int g = 0; g < G; g += 2) {
-            float2 back, unused;
-            wd[g / 2] = Pack2<T>::round(x[g], x[g + 1], back);
-            wd[G / 2 + g / 2] = Pack2<T>::round(x[g] - back.x, x[g + 1] - back.y, unused);
+    for (int i = 0; i < 4 * NB; ++i)
+        wd[i] = 0;
+    float r[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g)
+        r[g] = x[g];
+#pragma unroll
+    for (int s = 0; s < S; ++s) {
+#pragma unroll
+        for (int g = 0; g < G; ++g) { // column s*G + g: the rounding of the remainder (exact subtraction)
+            float2 back;
+            const uint32_t bits = Pack2<T>::round(r[g], 0.f, back) & 0xffffu;
+            r[g] -= back.x;
+            const int col = s * G + g;
+            wd[col / 2] |= bits << (16 * (col & 1));
         }
     }
     uint8_t *row = op + (k >> 3) * 128u + (k & 7u) * 16u;
-    *reinterpret_cast<uint4 *>(row) = make_uint4(wd[0], wd[1], wd[2], wd[3]);
-    if constexpr (2 * G > 8)
-        *reinterpret_cast<uint4 *>(row + 2048) = make_uint4(wd[4], wd[5], wd[6], wd[7]);
+#pragma unroll
+    for (int bl = 0; bl < NB; ++bl)
+        *reinterpret_cast<uint4 *>(row + 2048 * bl) =
+            make_uint4(wd[4 * bl], wd[4 * bl + 1], wd[4 * bl + 2], wd[4 * bl + 3]);
 }
 
 /// Tiles of one work item, identical for every role. The near window [lo, w)
@@ -375,12 +398,12 @@ struct Stream { // (no arrays indexed by w: everything stays in registers)
 struct WgBars {
     uint64_t qfull, sfull[2], sempty[2], pfull[2], ofull[2], oempty[2];
 };
-constexpr uint32_t kWgBytes = 3 * kOpBytes; // Q + P[2]
+constexpr uint32_t kWgBytes = kQBytes + 2 * kOpBytes; // Q + P[2]
 
 template <typename T, int G>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(DevCtx c, const __grid_constant__ TcMaps maps) {
-    static_assert(2 * G <= kN, "hi/lo columns must fit N = 16");
+    using SP = Splits<T, G>;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *kbuf = smem;                                    // kKStages x 32 KiB
@@ -428,7 +451,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     fence_async_smem();
     if (warp == 1) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(smem_u32(tmem_slot)));
+        // per warpgroup 128 columns: S[b] at 32 b (N <= 32), O[b] at 64 + 16 b
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 256;" ::"r"(smem_u32(tmem_slot)));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     tc_fence_before();
@@ -512,7 +536,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         // The PVs are issued by warp 3: two issuing warps halve the per-tile event-loop
         // latency that bounded the kernel with one.
         constexpr uint32_t fmt = std::is_same_v<T, __nv_bfloat16> ? 1u : 0u;
-        constexpr uint32_t id_s = idesc(fmt, 0, 1, kRows, kN); // S^T = K . Q^T (Q MN-major)
+        constexpr uint32_t id_s = idesc(fmt, 0, 1, kRows, SP::NQ); // S^T = K . Q^T (Q MN-major)
         Stream S;
         S.init(c, slots, n_items);
         uint32_t s = 0, ph = 0, w = 0, k = 0;
@@ -534,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const uint64_t b0 = sdesc(wg0 + w * kWgBytes, 128, 2048, 0);
 #pragma unroll
                 for (uint32_t kk = 0; kk < kHd / 16; ++kk) // K: 32 B steps in a 128-B row, then next half
-                    mma_f16(tmem + 64 * w + 16 * b, a0 + (((kk >> 2) * kHalfBytes + (kk & 3u) * 32) >> 4),
+                    mma_f16(tmem + 128 * w + 32 * b, a0 + (((kk >> 2) * kHalfBytes + (kk & 3u) * 32) >> 4),
                             b0 + kk * (256 >> 4), id_s, kk > 0);
                 mma_commit(&wb[w].sfull[b]);
                 mma_commit(&kempty[s]); // the K half is free once S is computed
@@ -610,9 +634,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tc_fence_after();
                 if (elect_one()) {
                     const uint64_t a0 = sdesc(vbase + st * kSideBytes, kHalfBytes, 1024, 2);
-                    const uint64_t b0 = sdesc(wg0 + x * kWgBytes + (1 + b) * kOpBytes, 128, 2048, 0);
+                    const uint64_t b0 = sdesc(wg0 + x * kWgBytes + kQBytes + b * kOpBytes, 128, 2048, 0);
                     for (uint32_t kk = 0; kk < nk; ++kk) // +2048 B (V rows) / +256 B (P cores) per K step
-                        mma_f16(tmem + 64 * x + 32 + 16 * b, a0 + kk * (2048 >> 4), b0 + kk * (256 >> 4), id_o,
+                        mma_f16(tmem + 128 * x + 64 + 16 * b, a0 + kk * (2048 >> 4), b0 + kk * (256 >> 4), id_o,
                                 kk > 0);
                     mma_commit(&wb[x].ofull[b]);
                     mma_commit(&vempty[st]);
@@ -626,7 +650,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t w = uint32_t(warp - 4) >> 2;     // warpgroup 0: warps 4-7, 1: warps 8-11
         const uint32_t t = threadIdx.x - 128 - 128 * w; // TMEM lane: token row of S, head dim of O
         const uint32_t wq = uint32_t(warp) & 3u;
-        const uint32_t lane_base = ((32u * wq) << 16) + 64 * w;
+        const uint32_t lane_base = ((32u * wq) << 16) + 128 * w;
         const uint32_t bar_id = 1 + w;
         WgBars &B = wb[w];
         uint8_t *qb = wgbuf + w * kWgBytes;
@@ -662,7 +686,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         while (have) {
             float *o = c.out + ((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G) * kHd;
             // Q (hi | lo) of this kv head's q-heads; thread t owns head dim t
-            store_split<T, G>(qb, t, xq);
+            store_split<T, G, SP::QS>(qb, t, xq);
             fence_async_smem();
             __syncwarp();
             if (lane == 0)
@@ -680,14 +704,18 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&B.ofull[b], (nn >> 1) & 1u);
                 tc_fence_after();
                 float ov[16];
-                tmem_ld16(tmem + lane_base + 32 + 16 * b, ov);
+                tmem_ld16(tmem + lane_base + 64 + 16 * b, ov);
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0)
                     mbar_arrive(&B.oempty[b]);
 #pragma unroll
-                for (int g = 0; g < G; ++g)
-                    acc[g] = acc[g] * alpha[g] + (ov[g] + ov[G + g]);
+                for (int g = 0; g < G; ++g) {
+                    float o_small = ov[G + g];
+                    if constexpr (SP::PS == 3)
+                        o_small += ov[2 * G + g];
+                    acc[g] = acc[g] * alpha[g] + (ov[g] + o_small);
+                }
             };
             for (uint32_t k = 0; k < I.n_tiles; ++k, ++n) {
                 const uint32_t b = n & 1u;
@@ -697,8 +725,21 @@ __global__ void __launch_bounds__(kThreads, 1)
                                                       t < kSub * (tl.box_first + tl.n_boxes) && tok >= I.lo && tok < I.w);
                 mbar_wait(&B.sfull[b], (n >> 1) & 1u);
                 tc_fence_after();
-                float sv[16];
-                tmem_ld16(tmem + lane_base + 16 * b, sv);
+                float sv[SP::NQ];
+                if constexpr (SP::NQ == 32) {
+                    float hi16[16], lo16[16];
+                    tmem_ld16(tmem + lane_base + 32 * b, hi16);
+                    tmem_ld16(tmem + lane_base + 32 * b + 16, lo16);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        sv[i] = hi16[i], sv[16 + i] = lo16[i];
+                } else {
+                    float v16[16];
+                    tmem_ld16(tmem + lane_base + 32 * b, v16);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        sv[i] = v16[i];
+                }
                 tc_fence_before();
                 __syncwarp();
                 if (lane == 0)
@@ -706,7 +747,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float sc[G], mx[G];
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
-                    sc[g] = valid ? (sv[g] + sv[G + g]) * scale_log2 : -INFINITY;
+                    float s_small = sv[G + g];
+                    if constexpr (SP::QS == 3)
+                        s_small += sv[2 * G + g];
+                    sc[g] = valid ? (sv[g] + s_small) * scale_log2 : -INFINITY;
                     float v = sc[g];
 #pragma unroll
                     for (int off = 16; off; off >>= 1)
@@ -719,7 +763,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         rd[(b * 4 + wq) * 8 + g] = mx[g];
                 asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
                 float alpha[G], pv[G];
-                uint8_t *pb = qb + (1 + b) * kOpBytes;
+                uint8_t *pb = qb + kQBytes + b * kOpBytes;
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const float tm = fmaxf(fmaxf(rd[(b * 4 + 0) * 8 + g], rd[(b * 4 + 1) * 8 + g]),
@@ -731,7 +775,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     m[g] = mn;
                     pv[g] = p;
                 }
-                store_split<T, G>(pb, t, pv);
+                store_split<T, G, SP::PS>(pb, t, pv);
                 fence_async_smem();
                 __syncwarp();
                 if (lane == 0)
@@ -772,7 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem));
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
     }
 }
 

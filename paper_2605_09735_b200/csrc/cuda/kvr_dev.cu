@@ -24,8 +24,8 @@
 
 namespace kvr {
 size_t scan_dynamic_smem(uint32_t cap);
-void prepare_scan(uint32_t cap);
-void prepare_gather(const DevCtx &c);
+cudaError_t prepare_scan(uint32_t cap);
+cudaError_t prepare_gather(const DevCtx &c);
 } // namespace kvr
 
 using namespace kvr;
@@ -205,6 +205,16 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         c.esz = g.elem_bytes;
         c.elem_kind = uint32_t(g.elem_kind);
         c.payload_mode = g.payload_mode;
+        {
+            const uint32_t sh = g.lane_shift ? g.lane_shift : 7;
+            if (sh > 12)
+                throw std::runtime_error("lane_shift must be <= 12");
+            c.lane_scale = 1.0f / float(1u << sh);
+            c.lane_bias = 8388608.0f * c.lane_scale + 128.0f * c.lane_scale; // exact: 2^(23-sh) + 2^(7-sh)
+        }
+        if (g.query_mode > KVR_QUERY_F32)
+            throw std::runtime_error("unknown query_mode");
+        c.query_mode = g.query_mode;
         c.n_slots = g.n_slots;
         c.W = g.near_window;
         c.R = g.ring_rows;
@@ -245,6 +255,12 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         c.gspans = static_cast<GSpan *>(dalloc(d.get(), sizeof(GSpan) * c.max_scan, "gspans"));
         c.scan = static_cast<ScanCounters *>(dalloc(d.get(), sizeof(ScanCounters), "scan"));
         ck(cudaMemsetAsync(c.scan, 0, sizeof(ScanCounters), d->stream), "scan zero");
+        {
+            const uint64_t off[2] = {~0ull, 0};
+            auto *fault = static_cast<uint64_t *>(dalloc(d.get(), sizeof(off), "fault hooks"));
+            ck(cudaMemcpy(fault, off, sizeof(off), cudaMemcpyHostToDevice), "fault init");
+            c.fault = fault;
+        }
         for (int i = 0; i < 3; ++i) {
             d->d_desc[i] = static_cast<uint8_t *>(dalloc(d.get(), g.max_desc_bytes, "desc"));
             ck(cudaMallocHost(&d->h_desc[i], g.max_desc_bytes), "pinned desc");
@@ -276,8 +292,8 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
             if (!prepare_mass(c))
                 throw std::runtime_error("utility: head_dim must be 32, 64 or 128 and (W* + q_heads) * 8 bytes <= 200 KiB");
         }
-        prepare_scan(c.max_scan);
-        prepare_gather(c);
+        ck(prepare_scan(c.max_scan), "K-scan shared-memory attribute (max_scan_descs)");
+        ck(prepare_gather(c), "K-gather shared-memory attribute (row size)");
         if (g.attention) {
             d->attn = make_attn_plan(c, d->sms, g.device, int(g.attention));
             if (!d->attn)
@@ -486,6 +502,41 @@ int kvr_dev_read(kvr_dev *d, int buffer, uint64_t offset, uint64_t bytes, void *
         ck(cudaStreamSynchronize(d->stream), "read sync");
         ck(cudaMemcpy(out, static_cast<const uint8_t *>(base) + offset, bytes, cudaMemcpyDeviceToHost),
            "read D2H");
+    });
+}
+
+int kvr_dev_read_staged(kvr_dev *d, uint64_t tok_begin, uint64_t count, void *out, uint8_t *in_window) {
+    return guard([&] {
+        ck(cudaStreamSynchronize(d->stream), "read sync");
+        ScanCounters sc{};
+        ck(cudaMemcpy(&sc, d->base.scan, sizeof(sc), cudaMemcpyDeviceToHost), "scan counters");
+        if (tok_begin + count > sc.total_tokens)
+            throw std::runtime_error("read_staged: tokens past the last step's gather list");
+        if (!count)
+            return;
+        const int k = d->launched[1] > d->launched[0] ? 1 : 0; // the last launched step
+        const DevCtx c = ctx_for(d, k);
+        const uint64_t bytes = count * c.token_bytes;
+        uint8_t *buf = nullptr, *flags = nullptr;
+        ck(cudaMallocAsync(reinterpret_cast<void **>(&buf), bytes + count, d->stream), "read_staged scratch");
+        flags = buf + bytes;
+        launch_read_staged(c, d->stream, tok_begin, count, buf, flags);
+        ck(cudaGetLastError(), "read_staged launch");
+        ck(cudaMemcpyAsync(out, buf, bytes, cudaMemcpyDeviceToHost, d->stream), "read_staged D2H");
+        if (in_window)
+            ck(cudaMemcpyAsync(in_window, flags, count, cudaMemcpyDeviceToHost, d->stream), "read_staged D2H");
+        ck(cudaFreeAsync(buf, d->stream), "read_staged free");
+        ck(cudaStreamSynchronize(d->stream), "read_staged sync");
+    });
+}
+
+int kvr_dev_fault(kvr_dev *d, int what, uint64_t arg) {
+    return guard([&] {
+        if (what != KVR_FAULT_DROP_SPAN && what != KVR_FAULT_SHIFT_ROWS)
+            throw std::runtime_error("unknown fault");
+        ck(cudaStreamSynchronize(d->stream), "fault sync");
+        ck(cudaMemcpy(const_cast<uint64_t *>(d->base.fault) + (what - 1), &arg, sizeof(arg), cudaMemcpyHostToDevice),
+           "fault set");
     });
 }
 

@@ -65,6 +65,44 @@ struct Move {
     uint32_t bytes;
 };
 
+/// Source and destination of layer row `l` of gather-order token `tok_idx` inside span
+/// `sp` (dst == nullptr: the window does not hold that row). Near spans land in the
+/// slot's ring at row token mod R when the token is in [written - W*, + R); far spans
+/// (summary slots) in the slot's far row of their chunk.
+__device__ inline Move span_row(const DevCtx &c, const kvr_slot_state *slots, const GSpan &sp, uint64_t tok_idx,
+                                uint32_t l) {
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    const uint64_t k = tok_idx - sp.tok_prefix;
+    Move m{nullptr, nullptr, uint32_t(row_bytes)};
+    m.src = c.arena + uint64_t(sp.block) * c.page_bytes + (sp.slot_begin + k) * c.token_bytes + l * row_bytes;
+    if (sp.dev_slot >= c.n_slots)
+        return m;
+    const uint64_t tok = sp.first_token + k;
+    if (sp.kind == 0) {
+        const uint64_t w = slots[sp.dev_slot].written;
+        const uint64_t lo_tok = w > c.W ? w - c.W : 0; // rows of [lo_tok, lo_tok + R) are live
+        if (tok < lo_tok || tok >= lo_tok + c.R)
+            return m;
+        m.dst = c.ring + (ring_row(c, sp.dev_slot, l, uint32_t(tok % c.R)) * c.esz);
+    } else {
+        if (tok < KVR_SUMMARY_BASE)
+            return m;
+        const uint64_t chunk = tok - KVR_SUMMARY_BASE;
+        if (chunk >= c.max_chunks)
+            return m;
+        m.dst = c.far + ((uint64_t(sp.dev_slot) * c.L + l) * c.max_chunks + chunk) * c.row_elems * c.esz;
+    }
+    return m;
+}
+
+/// Test hook: the same position `shift` ring rows further (wrapping in the slot's layer ring).
+__device__ inline uint8_t *shifted_row(const DevCtx &c, uint8_t *dst, uint64_t shift) {
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    const uint64_t off = uint64_t(dst - c.ring), ring_bytes = uint64_t(c.R) * row_bytes;
+    const uint64_t base = off / ring_bytes * ring_bytes, within = off - base;
+    return c.ring + base + (within + (shift % c.R) * row_bytes) % ring_bytes;
+}
+
 /// Walks this CTA's contiguous range of units (token, layer, piece) with a
 /// forward-moving span cursor: no division or search per unit.
 struct Walker {
@@ -98,32 +136,13 @@ struct Walker {
     }
     __device__ Move resolve(const DevCtx &c, const kvr_slot_state *slots, uint32_t piece_bytes) const {
         const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
-        const GSpan sp = c.gspans[cur];
-        const uint64_t k = tok_idx - sp.tok_prefix;
-        Move m{nullptr, nullptr, 0};
-        if (sp.dev_slot >= c.n_slots)
-            return m;
         const uint64_t off0 = uint64_t(piece) * piece_bytes;
-        const uint32_t bytes = uint32_t(row_bytes - off0 < piece_bytes ? row_bytes - off0 : piece_bytes);
-        m.src = c.arena + uint64_t(sp.block) * c.page_bytes + (sp.slot_begin + k) * c.token_bytes +
-                l * row_bytes + off0;
-        const uint64_t tok = sp.first_token + k;
-        if (sp.kind == 0) {
-            const uint64_t w = slots[sp.dev_slot].written;
-            const uint64_t lo_tok = w > c.W ? w - c.W : 0; // rows of [lo_tok, lo_tok + R) are live
-            if (tok < lo_tok || tok >= lo_tok + c.R)
-                return m;
-            m.dst = c.ring + (ring_row(c, sp.dev_slot, l, uint32_t(tok % c.R)) * c.esz) + off0;
-        } else {
-            if (tok < KVR_SUMMARY_BASE)
-                return m;
-            const uint64_t chunk = tok - KVR_SUMMARY_BASE;
-            if (chunk >= c.max_chunks)
-                return m;
-            m.dst = c.far + ((uint64_t(sp.dev_slot) * c.L + l) * c.max_chunks + chunk) * c.row_elems * c.esz +
-                    off0;
+        Move m = span_row(c, slots, c.gspans[cur], tok_idx, l);
+        if (m.dst) {
+            m.src += off0;
+            m.dst += off0;
+            m.bytes = uint32_t(row_bytes - off0 < piece_bytes ? row_bytes - off0 : piece_bytes);
         }
-        m.bytes = bytes;
         return m;
     }
 };
@@ -152,15 +171,20 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     Walker wk;
     wk.init(c, n_spans, u0, pieces);
+    const uint64_t drop = c.fault[0], shift = c.fault[1]; // test hooks (off: ~0, 0)
     uint64_t next = u0;
     Move mv[kStages];
     uint32_t phase_bits = 0;
     auto issue = [&](int s) {
         while (next < u1) {
-            const Move m = wk.resolve(c, slots, piece_bytes);
+            Move m = wk.resolve(c, slots, piece_bytes);
+            if (drop != ~0ull && (wk.cur == drop || drop == KVR_FAULT_ALL))
+                m.dst = nullptr;
+            else if (shift && m.dst && c.gspans[wk.cur].kind == 0)
+                m.dst = shifted_row(c, m.dst, shift);
             ++next;
             wk.advance(c, n_spans, pieces);
-            if (m.bytes) {
+            if (m.dst) {
                 mv[s] = m;
                 mbar_expect_tx(&full[s], m.bytes);
                 bulk_g2s(stage + size_t(s) * piece_bytes, m.src, m.bytes, &full[s]);
@@ -186,16 +210,65 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
     bulk_wait_all();
 }
 
+// Parity read-back: one CTA per gather-order token; layer rows from the destination
+// (or the arena for rows the window does not hold), token-major like the reference.
+__global__ void __launch_bounds__(256) k_read_staged(DevCtx c, uint64_t tok_begin, uint64_t count, uint8_t *out,
+                                                     uint8_t *in_window) {
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, hdr(c)->off_slots);
+    const uint32_t n_spans = c.scan->spans;
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    for (uint64_t i = blockIdx.x; i < count; i += gridDim.x) {
+        const uint64_t tok_idx = tok_begin + i;
+        uint32_t lo = 0, hi = n_spans; // last span with tok_prefix <= tok_idx
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (c.gspans[mid].tok_prefix <= tok_idx)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        const GSpan sp = c.gspans[lo];
+        bool all = true;
+        for (uint32_t l = 0; l < c.L; ++l) {
+            const Move m = span_row(c, slots, sp, tok_idx, l);
+            all = all && m.dst != nullptr;
+            const int4 *src = reinterpret_cast<const int4 *>(m.dst ? m.dst : m.src);
+            int4 *dst = reinterpret_cast<int4 *>(out + i * c.token_bytes + l * row_bytes);
+            for (uint64_t q = threadIdx.x; q < row_bytes / 16; q += blockDim.x)
+                dst[q] = src[q];
+        }
+        if (threadIdx.x == 0 && in_window) {
+            // 1: delivered; 0: a near row older than written - W* (behind the live
+            // window: not part of the window by definition); 2: not held otherwise
+            uint8_t f = 1;
+            if (!all) {
+                f = 2;
+                if (sp.kind == 0 && sp.dev_slot < c.n_slots) {
+                    const uint64_t w = slots[sp.dev_slot].written;
+                    f = sp.first_token + (tok_idx - sp.tok_prefix) + c.W < w ? 0 : 2;
+                }
+            }
+            in_window[i] = f;
+        }
+    }
+}
+
 } // namespace
+
+void launch_read_staged(const DevCtx &c, cudaStream_t s, uint64_t tok_begin, uint64_t count, uint8_t *out,
+                        uint8_t *in_window) {
+    if (count)
+        k_read_staged<<<unsigned(count < 4096 ? count : 4096), 256, 0, s>>>(c, tok_begin, count, out, in_window);
+}
 
 uint32_t gather_piece_bytes(const DevCtx &c) {
     const uint64_t row = uint64_t(c.row_elems) * c.esz;
     return uint32_t(row <= kMaxPiece ? row : kMaxPiece);
 }
 
-void prepare_gather(const DevCtx &c) {
+cudaError_t prepare_gather(const DevCtx &c) {
     const int smem = int(kStages * gather_piece_bytes(c));
-    cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 void launch_gather(const DevCtx &c, cudaStream_t s, int sms) {

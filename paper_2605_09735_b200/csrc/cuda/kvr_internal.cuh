@@ -37,6 +37,8 @@ struct DevCtx {
     uint32_t tpp, arena_pages, L, Hkv, hd, Hq, group, d_kv, row_elems, esz;
     uint32_t elem_kind, payload_mode, n_slots, W, R, far_cap, chunk_tokens, max_chunks, smap_cap;
     uint32_t max_scan, max_trains;
+    float lane_scale, lane_bias; // 2-byte lanes: (2^23 + b) * scale - bias = (b - 128) * scale
+    uint32_t query_mode;         // KVR_QUERY_*
     uint8_t *arena;   // arena_pages * page_bytes
     uint8_t *ring;    // [slot][L][R][row_elems] elements
     uint32_t *tmap;   // [slot][max_tokens]
@@ -56,7 +58,15 @@ struct DevCtx {
     float2 *mass_part;       // [slot][Hq][row splits] (max, sum of exp)
     kvr_mass_run *mass_runs; // [slot][W]
     uint32_t *mass_count;    // [slot]
+    const uint64_t *fault;   // [0] KVR_FAULT_DROP_SPAN, [1] KVR_FAULT_SHIFT_ROWS arguments — test hooks only
 };
+
+/// Token `tok` of a slot is written into the ring by K-write / K-prime only when it
+/// lies in the live window after this step and K-gather does not deliver it (near
+/// staged range [stage_lo, stage_hi) of the slot this step).
+__device__ inline bool ring_owned_by_writer(const DevCtx &c, const kvr_slot_state &st, uint64_t tok) {
+    return tok < st.written && tok + c.W >= st.written && !(tok >= st.stage_lo && tok < st.stage_hi);
+}
 
 __host__ __device__ inline const kvr_step_header *hdr(const DevCtx &c) {
     return reinterpret_cast<const kvr_step_header *>(c.desc);
@@ -103,6 +113,9 @@ void launch_map(const DevCtx &c, cudaStream_t s, int sms);     // page-table edi
 void launch_prime(const DevCtx &c, cudaStream_t s, int sms);   // window priming
 void launch_scan(const DevCtx &c, cudaStream_t s);             // stage + reduce
 void launch_gather(const DevCtx &c, cudaStream_t s, int sms);  // trains -> window
+/// destination bytes of staged tokens [tok_begin, +count) into out (token-major)
+void launch_read_staged(const DevCtx &c, cudaStream_t s, uint64_t tok_begin, uint64_t count, uint8_t *out,
+                        uint8_t *in_window);
 struct AttnPlan;
 /// mode: 1 auto (tensor cores for GQA groups where supported), 2 CUDA-core
 /// kernel, 3 tensor-core kernel (null if unsupported). Builds the TMA descriptor.

@@ -19,7 +19,7 @@ namespace kvr {
 namespace {
 
 constexpr int kScanThreads = 1024;
-constexpr int kMaxNeeds = 2048;
+constexpr int kMaxNeeds = KVR_MAX_SCAN_NEEDS;
 
 // Exclusive block-wide scan of one value per thread; returns the block total.
 __device__ uint64_t block_exclusive_scan(uint64_t v, uint64_t &excl, uint64_t *warp_tot) {
@@ -372,8 +372,8 @@ void launch_scan(const DevCtx &c, cudaStream_t s) {
     k_scan<<<1, kScanThreads, scan_dynamic_smem(c.max_scan), s>>>(c);
 }
 
-void prepare_scan(uint32_t cap) {
-    cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, int(scan_dynamic_smem(cap)));
+cudaError_t prepare_scan(uint32_t cap) {
+    return cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, int(scan_dynamic_smem(cap)));
 }
 
 } // namespace kvr

@@ -482,6 +482,14 @@ int kvr_driver_device_check(kvr_driver *d, uint64_t *checked, uint64_t *mismatch
     });
 }
 
+int kvr_driver_staged_rows(kvr_driver *d, uint64_t *delivered, uint64_t *behind, uint64_t *missing) {
+    return call([&] { d->d->staged_rows(*delivered, *behind, *missing); });
+}
+
+int kvr_driver_fault(kvr_driver *d, int what, uint64_t arg) {
+    return call([&] { d->d->fault(what, arg); });
+}
+
 // ---- device ------------------------------------------------------------------
 
 #define DS reinterpret_cast<DeviceStep *>(d)

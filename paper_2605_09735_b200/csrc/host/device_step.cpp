@@ -53,8 +53,10 @@ struct DeviceStep::Impl {
     std::vector<kvr_need_rec> needs;
     std::vector<kvr_span_rec> spans;
     std::vector<kvr_prime_op> primes;
+    std::unordered_set<SessionId> prime_src; // sessions whose rows K-prime copies this step
     std::vector<uint32_t> far_ids;
     std::vector<kvr_slot_state> slots;
+    std::vector<uint64_t> staged_count; // per slot: near staged tokens this step
     std::vector<std::vector<uint64_t>> far_shown; // per slot, as of the last launch
     // K-presum: chunks summarised while their prompt rows were written (far view)
     std::vector<kvr_presum_op> presum_ops;
@@ -261,7 +263,7 @@ struct DeviceStep::Impl {
         // Rows read before the cold phase: staged blocks (K-gather) and chunks a
         // far job summarises (K-far), matched by session and token range.
         auto read_early = [&](const kvr_write_op &w) {
-            if (staged.count(w.block))
+            if (staged.count(w.block) || prime_src.count(w.session))
                 return true;
             for (const kvr_write_op &f : far_jobs)
                 if (f.session == w.session && w.token < f.aux + g.chunk_tokens && f.aux < w.token + w.count)
@@ -315,6 +317,8 @@ struct DeviceStep::Impl {
                 scan |= deferred.has_block(b);
             for (const kvr_write_op &f : far_jobs)
                 scan |= deferred.has_session(f.session);
+            for (SessionId s : prime_src)
+                scan |= deferred.has_session(s);
             if (scan)
                 deferred.extract(read_early, [&](const kvr_write_op &w) { hot.push_back(w); });
             // A queued row lies behind its session's window for good: it never
@@ -342,6 +346,16 @@ struct DeviceStep::Impl {
         std::vector<kvr_write_op> all_writes = hot;
         all_writes.insert(all_writes.end(), cold.begin(), cold.end());
         all_writes.insert(all_writes.end(), far_jobs.begin(), far_jobs.end());
+        if (with_step) {
+            // K-scan capacity (kvr_scan.cu): an overflow would skip the step's gather,
+            // so it is refused here instead (descriptors and trains <= non-empty spans)
+            if (needs.size() > KVR_MAX_SCAN_NEEDS)
+                throw std::runtime_error("step has " + std::to_string(needs.size()) + " stage needs > K-scan capacity " +
+                                         std::to_string(KVR_MAX_SCAN_NEEDS));
+            if (spans.size() > g.max_scan_descs)
+                throw std::runtime_error("step has " + std::to_string(spans.size()) +
+                                         " staged spans > geometry.max_scan_descs " + std::to_string(g.max_scan_descs));
+        }
         const auto &nd = with_step ? needs : std::vector<kvr_need_rec>{};
         const auto &sp = with_step ? spans : std::vector<kvr_span_rec>{};
         const auto &fi = with_step ? far_ids : std::vector<uint32_t>{};
@@ -407,6 +421,7 @@ struct DeviceStep::Impl {
         wave_slots.clear();
         wave_cow_dst.clear();
         primes.clear();
+        prime_src.clear();
     }
 
     void flush() {
@@ -587,8 +602,13 @@ DeviceStep::DeviceStep(const kvr_geometry &geometry) : impl_(std::make_unique<Im
     m.g = geometry;
     if (!m.g.max_desc_bytes)
         m.g.max_desc_bytes = 16ull << 20;
+    if (!m.g.max_scan_descs) // the defaults kvr_dev_open applies
+        m.g.max_scan_descs = 2048;
+    if (!m.g.max_trains)
+        m.g.max_trains = 2048;
     m.clean.assign(m.g.arena_pages, 1); // the arena starts zeroed
     m.slots.assign(m.g.n_slots, kvr_slot_state{});
+    m.staged_count.assign(m.g.n_slots, 0);
     m.store_ = std::make_shared<DeviceStore>(impl_.get());
 }
 
@@ -622,6 +642,8 @@ void DeviceStep::slot_state(uint32_t slot, SessionId sid, uint64_t written, bool
     s.live = live ? 1 : 0;
     s.far_begin = 0;
     s.far_count = 0;
+    s.stage_lo = s.stage_hi = 0;
+    impl_->staged_count[slot] = 0;
 }
 
 void DeviceStep::need(uint32_t slot, SessionId sid, TrainKind kind, std::span<const StagedSpan> spans,
@@ -636,10 +658,30 @@ void DeviceStep::need(uint32_t slot, SessionId sid, TrainKind kind, std::span<co
     m.needs.push_back(n);
     for (size_t i = 0; i < spans.size(); ++i)
         m.spans.push_back({first_tokens[i], spans[i].block, spans[i].slot_begin, spans[i].slot_count, 0});
+    // near spans: K-gather is the window writer of their tokens this step (the
+    // spans of one session's need are its current reservation span: contiguous)
+    if (kind == TrainKind::near_window && slot < m.g.n_slots) {
+        kvr_slot_state &st = m.slots[slot];
+        for (size_t i = 0; i < spans.size(); ++i) {
+            if (!spans[i].slot_count)
+                continue;
+            const uint64_t lo = first_tokens[i], hi = lo + spans[i].slot_count;
+            m.staged_count[slot] += spans[i].slot_count;
+            if (st.stage_lo == st.stage_hi) {
+                st.stage_lo = lo;
+                st.stage_hi = hi;
+            } else {
+                st.stage_lo = std::min(st.stage_lo, lo);
+                st.stage_hi = std::max(st.stage_hi, hi);
+            }
+        }
+    }
 }
 
-void DeviceStep::prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end) {
+void DeviceStep::prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end, SessionId src) {
     impl_->primes.push_back({tok_begin, tok_end, slot, 0});
+    if (src != kNoPrimeSource)
+        impl_->prime_src.insert(src); // its rows are read by K-prime: written hot, never deferred
 }
 
 void DeviceStep::far_selection(uint32_t slot, std::span<const uint64_t> chunk_ids) {
@@ -688,6 +730,11 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
     for (size_t s = 0; s < m.slots.size(); ++s)
         for (uint32_t i = 0; i < m.slots[s].far_count; ++i)
             m.far_shown[s].push_back(m.far_ids[m.slots[s].far_begin + i]);
+    // a slot whose near spans do not form one contiguous token range (never the
+    // Driver's; possible through the C-ABI) keeps K-write as its window writer
+    for (uint32_t s = 0; s < m.slots.size(); ++s)
+        if (m.slots[s].stage_hi - m.slots[s].stage_lo != m.staged_count[s])
+            m.slots[s].stage_lo = m.slots[s].stage_hi = 0;
     void *buf = nullptr;
     ck(kvr_dev_desc_buffer(m.dev, k, &buf));
     const uint64_t bytes = m.pack(buf, step, now, &tc, true);
@@ -701,10 +748,19 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
     m.needs.clear();
     m.spans.clear();
     m.far_ids.clear();
+    for (kvr_slot_state &s : m.slots)
+        s.stage_lo = s.stage_hi = 0;
+    std::fill(m.staged_count.begin(), m.staged_count.end(), 0);
 }
 
 DeviceStepStats DeviceStep::collect(uint64_t step) {
     Impl &m = *impl_;
+    auto overflow = [&](const DeviceStepStats &d) {
+        if (d.scan_status & 4u) // K-scan ran out of capacity: K-gather skipped the step
+            throw std::runtime_error("step " + std::to_string(d.step) +
+                                     ": K-scan capacity exceeded (trains > geometry.max_trains or descriptors > "
+                                     "max_scan_descs); the staged window of that step is invalid");
+    };
     const uint32_t k = uint32_t(step & 1);
     if (m.launched_step[k] != step)
         throw std::runtime_error("collect: step " + std::to_string(step) + " is not in flight");
@@ -727,6 +783,7 @@ DeviceStepStats DeviceStep::collect(uint64_t step) {
         d.end_ns = st.end_ns;
         m.have_done[k] = true;
     }
+    overflow(m.done[k]);
     return m.done[k];
 }
 
@@ -787,6 +844,12 @@ void DeviceStep::read_ring_token(uint32_t slot, uint64_t token, void *out) {
         ck(kvr_dev_read(impl_->dev, KVR_BUF_RING, off, row, static_cast<uint8_t *>(out) + l * row));
     }
 }
+
+void DeviceStep::read_staged(uint64_t tok_begin, uint64_t count, void *out, uint8_t *in_window) {
+    ck(kvr_dev_read_staged(impl_->dev, tok_begin, count, out, in_window));
+}
+
+void DeviceStep::fault(int what, uint64_t arg) { ck(kvr_dev_fault(impl_->dev, what, arg)); }
 
 void DeviceStep::read_page_table(uint32_t slot, uint64_t tok_begin, uint64_t count, uint32_t *out) {
     const kvr_geometry &g = impl_->g;

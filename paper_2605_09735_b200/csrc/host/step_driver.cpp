@@ -142,8 +142,10 @@ void ScenarioConfig::validate() const {
         raise(Errc::bad_config, "shared_prefix_tokens must be block aligned");
     if (eos_burst_fraction < 0.0 || eos_burst_fraction > 1.0)
         raise(Errc::bad_config, "eos_burst_fraction must be in [0,1]");
-    if (b200.payload != "bytes" && b200.payload != "lanes")
-        raise(Errc::bad_config, "b200.payload must be 'bytes' or 'lanes'");
+    if (b200.payload != "bytes" && b200.payload != "lanes" && b200.payload != "wide")
+        raise(Errc::bad_config, "b200.payload must be 'bytes', 'lanes' or 'wide'");
+    if (b200.query != "exact" && b200.query != "f32")
+        raise(Errc::bad_config, "b200.query must be 'exact' or 'f32'");
 }
 
 std::vector<TraceEvent> resolve_events(const ScenarioConfig &cfg) {
@@ -228,6 +230,7 @@ struct ScenarioDriver::Impl {
     uint32_t span_tokens = 0;
     int ekind = KVR_ELEM_F16;
     bool lanes_payload = false;
+    uint32_t lane_shift = 7; // 2-byte lanes: (b - 128) / 2^lane_shift
 
     std::unique_ptr<DeviceStep> dev;
     std::unique_ptr<Pager> pager;
@@ -250,6 +253,7 @@ struct ScenarioDriver::Impl {
     Step t = 0;
     std::vector<StepRecord> records;
     std::string trace;
+    uint64_t staged_rows_window = 0, staged_rows_behind = 0, staged_rows_missing = 0; // device trace coverage
     std::vector<StageNeed> traced_needs;
     std::vector<std::byte> buf;
 
@@ -259,7 +263,9 @@ struct ScenarioDriver::Impl {
         width = cfg.workload ? cfg.workload->concurrency : 64;
         span_tokens = cfg.span_blocks * tpp;
         ekind = elem_kind_of(cfg);
-        lanes_payload = cfg.b200.payload == "lanes";
+        lanes_payload = cfg.b200.payload == "lanes" || cfg.b200.payload == "wide";
+        lane_shift = cfg.b200.payload == "wide" ? 3 : 7;
+
         buf.resize(cfg.pager.token_bytes());
         if (cfg.pager_enabled)
             setup_paged();
@@ -285,7 +291,7 @@ struct ScenarioDriver::Impl {
                 } else { // 2-byte lanes: byte l % 8 of one splitmix per 8 lanes
                     const uint64_t x = pattern(id, tok, (l >> 3) ^ 0x4000000000000000ull);
                     const uint32_t r = uint32_t((x >> (8 * (l & 7))) & 0xffu);
-                    const float v = float(int(r) - 128) / 128.0f;
+                    const float v = float(int(r) - 128) / float(1u << lane_shift);
                     const uint16_t h = ekind == KVR_ELEM_BF16 ? to_bf16(v) : to_half(v);
                     std::memcpy(out + 2 * l, &h, 2);
                 }
@@ -323,6 +329,8 @@ struct ScenarioDriver::Impl {
         g.elem_kind = ekind;
         g.elem_bytes = cfg.pager.elem_bytes;
         g.payload_mode = lanes_payload ? KVR_PAYLOAD_LANES : KVR_PAYLOAD_BYTES;
+        g.lane_shift = lane_shift;
+        g.query_mode = cfg.b200.query == "f32" ? KVR_QUERY_F32 : KVR_QUERY_EXACT;
         g.page_bytes = cfg.pager.page_bytes;
         g.token_bytes = cfg.pager.token_bytes();
         g.arena_pages = pages;
@@ -900,7 +908,7 @@ struct ScenarioDriver::Impl {
                                         ? r.written - cfg.far_view.near_window
                                         : 0;
                 if (lo < r.write_begin)
-                    dev->prime(s, lo, r.write_begin);
+                    dev->prime(s, lo, r.write_begin, 0); // aliases the template session 0
             }
             if (cfg.far_view.enabled && cfg.far_view.cap > 0 && !r.chunk_scores.empty()) {
                 const std::vector<uint64_t> pick = select_chunks(r.chunk_scores, cfg.far_view.cap);
@@ -916,6 +924,8 @@ struct ScenarioDriver::Impl {
             std::vector<uint64_t> f = first[i];
             if (n.kind == TrainKind::far_view) {
                 // far spans carry their summary index as the logical token
+                if (it == slot_by_id.end())
+                    raise(Errc::unknown_session, "far-view need of a session without a live slot");
                 const Req &r = live[slot_of[it->second]];
                 for (size_t k = 0; k < n.spans.size(); ++k) {
                     const StagedSpan &sp = n.spans[k];
@@ -985,9 +995,29 @@ struct ScenarioDriver::Impl {
         traced_needs.clear();
         const uint64_t page = cfg.pager.page_bytes, tb = cfg.pager.token_bytes();
         std::vector<std::byte> tok(tb);
+        // Device mode: the staged bytes are hashed from K-gather's DESTINATION (the
+        // window ring / far rows), in train order, so the trace equals the reference's
+        // read_slots hash only if every train landed byte for byte.
+        std::vector<uint8_t> staged, in_window;
+        uint64_t staged_base = 0;
+        if (dev && pager) {
+            uint64_t total = 0;
+            for (const DmaTrain &tr : trains)
+                total += tr.total_bytes / tb;
+            staged.resize(total * tb);
+            in_window.resize(total);
+            dev->read_staged(0, total, staged.data(), in_window.data());
+            for (uint8_t w : in_window)
+                (w == 1 ? staged_rows_window : w == 0 ? staged_rows_behind : staged_rows_missing) += 1;
+        }
         for (const DmaTrain &tr : trains) {
             Fnv f;
-            if (pager)
+            if (pager && dev) {
+                const uint64_t n = tr.total_bytes;
+                for (uint64_t i = 0; i < n; ++i)
+                    f.byte(staged[staged_base + i]);
+                staged_base += n;
+            } else if (pager)
                 for (const Descriptor &d : tr.descriptors)
                     for (uint64_t off = d.phys_offset; off < d.phys_offset + d.length; off += tb) {
                         pager->read_slots(BlockId(off / page), uint32_t((off % page) / tb), 1,
@@ -1112,6 +1142,18 @@ void ScenarioDriver::device_check(uint64_t &checked, uint64_t &mismatches, std::
     checked = impl_->checked_steps;
     mismatches = impl_->scan_mismatches;
     first = impl_->first_mismatch;
+}
+
+void ScenarioDriver::staged_rows(uint64_t &delivered, uint64_t &behind, uint64_t &missing) const {
+    delivered = impl_->staged_rows_window;
+    behind = impl_->staged_rows_behind;
+    missing = impl_->staged_rows_missing;
+}
+
+void ScenarioDriver::fault(int what, uint64_t arg) {
+    if (!impl_->dev)
+        throw std::runtime_error("fault: host-only driver");
+    impl_->dev->fault(what, arg);
 }
 
 RunResult ScenarioDriver::result() const {
@@ -1424,6 +1466,7 @@ static ScenarioConfig config_from_json(const ojson &j) {
         take(p, "head_dim", c.b200.head_dim);
         take(p, "q_heads", c.b200.q_heads);
         take(p, "payload", c.b200.payload);
+        take(p, "query", c.b200.query);
         take(p, "dtype", c.b200.dtype);
         take(p, "trace", c.b200.trace);
         take(p, "attention", c.b200.attention);

@@ -163,7 +163,8 @@ class Geometry(C.Structure):
                 ("max_tokens", C.c_uint64), ("seed", C.c_uint64), ("attention", C.c_uint32),
                 ("use_graph", C.c_uint32), ("max_desc_bytes", C.c_uint64),
                 ("max_scan_descs", C.c_uint32), ("max_trains", C.c_uint32),
-                ("utility", C.c_uint32), ("utility_layer", C.c_uint32)]
+                ("utility", C.c_uint32), ("utility_layer", C.c_uint32),
+                ("lane_shift", C.c_uint32), ("query_mode", C.c_uint32)]
 
 
 class MassRun(C.Structure):
@@ -281,6 +282,8 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_driver_workload_hash": [vp, U64P],
         "kvr_driver_device": [vp, C.POINTER(vp)],
         "kvr_driver_device_check": [vp, U64P, U64P, C.c_char_p, C.c_uint64],
+        "kvr_driver_staged_rows": [vp, U64P, U64P, U64P],
+        "kvr_driver_fault": [vp, C.c_int, C.c_uint64],
         "kvr_device_open": [C.POINTER(Geometry), C.POINTER(vp)],
         "kvr_device_close": [vp],
         "kvr_device_flush": [vp],
@@ -300,6 +303,8 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_dev_time_attention": [vp, C.c_uint32, C.POINTER(C.c_double)],
         "kvr_dev_time_gather": [vp, C.c_uint32, C.POINTER(C.c_double)],
         "kvr_dev_read": [vp, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p],
+        "kvr_dev_read_staged": [vp, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p],
+        "kvr_dev_fault": [vp, C.c_int, C.c_uint64],
     }
     for name, args in sig.items():
         fn = getattr(lib, name)
@@ -747,3 +752,17 @@ class Driver:
         buf = C.create_string_buffer(512)
         check(native_lib().kvr_driver_device_check(self.h, C.byref(a), C.byref(b), buf, 512))
         return a.value, b.value, buf.value.decode()
+
+    def staged_rows(self) -> tuple[int, int, int]:
+        """Staged tokens of the device trace: (delivered by K-gather into the window,
+        behind the live window, missing from the window otherwise)."""
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        check(native_lib().kvr_driver_staged_rows(self.h, C.byref(a), C.byref(b), C.byref(c)))
+        return a.value, b.value, c.value
+
+    FAULT_DROP_SPAN, FAULT_SHIFT_ROWS, FAULT_ALL = 1, 2, 0xFFFFFFFFFFFFFFFE
+
+    def fault(self, what: int, arg: int) -> None:
+        """Test hook (kvr_dev_fault): KVR_FAULT_DROP_SPAN (span index, FAULT_ALL, -1 off)
+        or KVR_FAULT_SHIFT_ROWS (ring rows, 0 off) in K-gather on every later step."""
+        check(native_lib().kvr_driver_fault(self.h, what, arg & 0xFFFFFFFFFFFFFFFF))

@@ -2,8 +2,12 @@
 
 * Reference-byte payload ("bytes", scenario.cpp:193-206) generated on the GPU:
   the per-step trace — which hashes the bytes of every staged train read back
-  from the DEVICE arena, and digests the whole pager — must equal the trace the
-  reference recorded (tests/golden), step for step.
+  from K-gather's DESTINATION (the window ring / far rows), and digests the whole
+  pager — must equal the trace the reference recorded (tests/golden), step for
+  step (staged bytes = read_slots over each train's range).
+* K-gather is load-bearing: K-write and K-prime leave the ring rows of staged
+  tokens to it, so a K-gather that drops a span breaks both the trace and the
+  window (fault-injection test).
 * b200.check: the device K-scan (stage + reduce on the GPU) must equal the host
   reduce() on every step.
 * The window ring must hold exactly the arena bytes of every live slot's last
@@ -48,9 +52,18 @@ def c1():
     return cfg
 
 
+def assert_all_staged_rows_delivered(d, behind_ok=False):
+    """Every staged token the trace hashed came from K-gather's destination, except
+    (far-view configs, W* shorter than a reservation span) near rows older than
+    written - W*, which are not part of the window."""
+    win, behind, missing = d.staged_rows()
+    assert win > 0 and missing == 0 and (behind_ok or behind == 0), (win, behind, missing)
+
+
 def test_c1_reference_bytes_on_device():
     d = run(c1(), kv_heads=4, head_dim=64, payload="bytes", attention=False)
     assert d.trace() == read("c1_trace.txt")
+    assert_all_staged_rows_delivered(d)
     assert d.steps_csv() == read("c1_steps.csv")
     assert_scan_exact(d, 64)
     # fixed shape: the two step graphs (one per descriptor ring slot) are never recaptured
@@ -75,6 +88,45 @@ def test_golden_scenarios_on_device(name):
     d = run(cfg, payload="bytes", attention=False)
     assert d.trace() == read(f"{name}_trace.txt")
     assert_scan_exact(d, cfg["steps"])
+    assert_all_staged_rows_delivered(d)
+
+
+DROP_ALL = (kv.Driver.FAULT_DROP_SPAN, kv.Driver.FAULT_ALL)
+SHIFT_ONE = (kv.Driver.FAULT_SHIFT_ROWS, 1)
+
+
+def faulty_run(cfg, fault, **b200):
+    c = copy.deepcopy(cfg)
+    c.setdefault("b200", {}).update(dict(trace=True, check=True), **b200)
+    d = kv.Driver(c, device=0)
+    d.fault(*fault)
+    d.run()
+    return d
+
+
+@pytest.mark.parametrize("fault", [DROP_ALL, SHIFT_ONE], ids=["drop", "misplace"])
+def test_faulty_gather_breaks_the_trace(fault):
+    """K-gather drops its spans / lands near rows one ring row off: the
+    destination-hashed trace no longer equals the reference's (the source arena
+    is untouched, so a source-side hash would not notice)."""
+    d = faulty_run(c1(), fault, kv_heads=4, head_dim=64, payload="bytes", attention=False)
+    assert d.trace() != read("c1_trace.txt")
+    assert d.steps_csv() == read("c1_steps.csv")  # the control plane is unaffected
+    assert_scan_exact(d, 64)
+
+
+@pytest.mark.parametrize("fault", [DROP_ALL, SHIFT_ONE], ids=["drop", "misplace"])
+def test_faulty_gather_breaks_the_window(fault):
+    """With the near rows of staged tokens left to K-gather, a dropped or misplaced
+    span leaves wrong ring rows the attention reads: the window check must fail."""
+    cfg = c1()
+    cfg["steps"] = 40
+    kw = dict(kv_heads=4, head_dim=64, q_heads=4, payload="lanes", dtype="fp16")
+    good = run(cfg, **kw)
+    assert ob.check_driver_window_and_attention(good) <= 1e-3
+    bad = faulty_run(cfg, fault, **kw)
+    with pytest.raises(AssertionError, match="window ring mismatch"):
+        ob.check_driver_window_and_attention(bad)
 
 
 @pytest.mark.parametrize("name,budget", [("c1", 8), ("adv_burst", 64), ("far", 4)])
@@ -100,6 +152,7 @@ def test_far_view_fp32_on_device():
     d = run(cfg, kv_heads=1, head_dim=64)
     assert d.trace() == read("far_trace.txt")
     assert_scan_exact(d, cfg["steps"])
+    assert_all_staged_rows_delivered(d, behind_ok=True)
     worst = ob.check_driver_window_and_attention(d)
     assert worst <= 1e-3
 
@@ -142,6 +195,56 @@ def test_tcgen05_gqa_attention(dtype, kvh, qh, w_star):
             attention_kernel="tcgen05")
     assert "tc" in d.device().attention_variant()
     assert_scan_exact(d, 40)
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
+def not_16bit_exact(qs, elem_kind):
+    """Fraction of query lanes that a 16-bit type cannot hold (the tensor-core
+    kernel's lo half is non-zero for those)."""
+    import numpy as np
+    q = np.asarray(qs, np.float32)
+    if elem_kind == 1:
+        back = q.astype(np.float16).astype(np.float32)
+    else:
+        back = (((q.view(np.uint32) + 0x7FFF + ((q.view(np.uint32) >> 16) & 1)) >> 16) << 16).view(np.float32)
+    return float(np.mean(back != q))
+
+
+@pytest.mark.parametrize("kernel,dtype,kvh,hd,qh", [
+    ("cuda_core", "fp16", 4, 64, 4), ("cuda_core", "bf16", 2, 128, 2), ("cuda_core", "bf16", 2, 128, 8),
+    ("tcgen05", "bf16", 2, 128, 8), ("tcgen05", "fp16", 2, 128, 8), ("tcgen05", "bf16", 1, 128, 8),
+    ("tcgen05", "bf16", 2, 128, 4), ("tcgen05", "fp16", 2, 128, 16)])
+def test_attention_f32_queries_wide_kv(kernel, dtype, kvh, hd, qh):
+    """Random 24-bit fp32 queries (not representable in the KV type: q = q_hi + q_lo
+    with q_lo != 0 in the tensor-core kernel) over KV lanes of [-16, 16) — logits of
+    std ~5, peaked softmaxes — against the double-precision oracle at 1e-3."""
+    cfg = c1()
+    cfg["steps"] = 40
+    cfg["pager"]["kv_head_dim"] = kvh * hd
+    cfg["pager"]["page_bytes"] = 16 * 2 * 2 * kvh * hd * 2
+    cfg["transport"]["tau_bytes"] = 8 * cfg["pager"]["page_bytes"]
+    cfg["far_view"]["w_star"] = 512
+    d = run(cfg, kv_heads=kvh, head_dim=hd, q_heads=qh, payload="wide", query="f32", dtype=dtype,
+            attention_kernel=kernel)
+    assert ("tc" in d.device().attention_variant()) == (kernel == "tcgen05")
+    assert_scan_exact(d, 40)
+    g = d.device().geometry
+    assert g.query_mode == 1 and g.lane_shift == 3
+    slot, session, _ = d.live()[0]
+    q = ob.fill_query(g.seed, session, 39, 0, 0, hd, g.elem_kind, 1)
+    assert q == d.device().query(slot)[:hd]
+    assert not_16bit_exact(q, g.elem_kind) > 0.9
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
+def test_attention_f32_queries_wide_kv_far_view():
+    """The same inputs with far summary rows in the view (tensor-core kernel, gather4 rows)."""
+    cfg = json.loads(read("far_config.json"))
+    cfg["steps"] = 250
+    cfg["pager"].update({"elem_bytes": 2, "kv_head_dim": 256})
+    d = run(cfg, kv_heads=2, head_dim=128, q_heads=8, payload="wide", query="f32", dtype="bf16",
+            attention_kernel="tcgen05")
+    assert_scan_exact(d, 250)
     assert ob.check_driver_window_and_attention(d) <= 1e-3
 
 

@@ -24,6 +24,21 @@ def test_full_scale_control_plane_matches_reference(name, steps):
     assert f"{steps} steps identical" in out.stdout
 
 
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_headline_geometry_window_and_attention(name):
+    """The bench's own configurations at full width and geometry (C2: the headline
+    k_attn<f16,hd128,g1> G=4 variant, 64 slots x 32 layers; C3: the tcgen05 GQA
+    kernel, 128 slots): after the batch fills, sampled slots' window rings equal the
+    arena through the pager's views and sampled (layer, q-head) attention outputs are
+    within 1e-3 of the double-precision oracle."""
+    out = subprocess.run([sys.executable, "scripts/scale_parity.py", name], cwd=ROOT,
+                         capture_output=True, text=True, timeout=1200)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "window exact" in out.stdout
+    variant = "k_attn<f16,hd128,g1>" if name == "c2" else "tc"
+    assert variant in out.stdout
+
+
 def test_c5_geometry_attention_with_many_items_per_cta():
     """C5 geometry (80 layers, g = 8, far rows + 512-token windows) with 4 slots:
     ~17 items per CTA, so the two softmax warpgroups hand over items while the
