@@ -16,8 +16,13 @@ session, stage needs) + one committed descriptor + one replay of the step graph
   e2e    = emitted tokens / wall time of the same steps driven through the C-ABI
            (host control plane, pinned H2D of each step's descriptor, D2H of the
            step counters), synchronised at both ends.
-Multi-GPU (torchrun): requests shard by sequence (request_id % world); every rank
-runs its own pager + graph; the max over ranks of the timed region is used.
+Multi-GPU (one process per GPU; `--gpus N` without a torchrun environment re-launches
+itself under torch.distributed.run): requests shard by sequence (request_id % world);
+every rank runs its own pager + graph; the per-step counts (live, emitted, commits,
+EOS) are all-reduced by ONE ncclAllReduce captured at the end of every step graph
+(kvr_comm_init, NVLink/NVSwitch) — the KV data path never leaves its GPU; the max
+over ranks of the timed region is used. `--backend gloo` (tests, several ranks on
+one GPU via KVR_BENCH_DEVICE) does the per-step all-reduce in torch.distributed.
 
 --impl reference: the reference's own CPU path (oracle/_ref: run_scenario control
 plane + memcpy gather + build_view/attend), rank 0 only.
@@ -273,6 +278,18 @@ def reduce_sum(vals: list[float], world: int) -> list[float]:
     return t.tolist()
 
 
+def all_filled(filled: bool, world: int) -> bool:
+    """Every rank's batch is full (ranks run the same number of steps: each step graph
+    holds a collective)."""
+    if world == 1:
+        return filled
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([int(filled)], dtype=torch.int64, device=COLL_DEVICE)
+    dist.all_reduce(t, op=dist.ReduceOp.MIN)
+    return bool(t.item())
+
+
 def run_b200(args, rank, local, world) -> dict | None:
     import paper_2605_09735_b200 as pkg
 
@@ -287,13 +304,19 @@ def run_b200(args, rank, local, world) -> dict | None:
         cfg["b200"]["utility"] = args.utility
         cfg["b200"]["utility_every"] = args.utility_every
     d = pkg.Driver(cfg, device=local)
+    in_graph = world > 1 and args.backend == "nccl"
+    if in_graph:  # the per-step counts all-reduce, captured in every step graph
+        import torch.distributed as dist
+        uid = [pkg.kvrail.comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        d.comm_init(uid[0], rank, world)
     width = cfg["workload"]["concurrency"]
     # fill the fixed-width batch (admissions write whole prompts), then warm up
     fill = 0
     while fill < fill_cap:
         r = d.step()
         fill += 1
-        if r.live_sessions >= width:
+        if all_filled(r.live_sessions >= width, world):
             break
     for _ in range(args.warmup):
         d.step()
@@ -301,7 +324,7 @@ def run_b200(args, rank, local, world) -> dict | None:
     first = d.progress()[0]
     barrier(world)
     counts = None
-    if world > 1:  # per-step completion / EOS counts: the only cross-GPU traffic
+    if world > 1 and not in_graph:  # gloo: per-step counts all-reduced on the host
         import torch
         import torch.distributed as dist
         counts = torch.zeros(4, dtype=torch.int64, device=COLL_DEVICE)
@@ -330,6 +353,8 @@ def run_b200(args, rank, local, world) -> dict | None:
             raise RuntimeError(f"global single-commit audit failed: {commits_all} commit "
                                f"frames for {ranks_live} ranks with live sessions")
     recs = [d.record(s) for s in range(first, first + args.steps)]
+    # in-graph counts (the job-wide single-commit audit ran in the driver per step)
+    global_tokens = sum(r.global_emitted for r in recs)
     # inter-token latency: successive step-end %globaltimer stamps (pipelined steps)
     itl_ms = [(recs[i].end_ns - recs[i - 1].end_ns) / 1e6 for i in range(1, len(recs))]
     if args.dump_steps and rank == 0:  # per-step records for latency analysis
@@ -356,9 +381,14 @@ def run_b200(args, rank, local, world) -> dict | None:
     dev_s_max, wall_s_max = reduce_max([dev_s, wall_s], world)
     tokens_all, gather_bytes_all, attn_bytes_all = reduce_sum(
         [float(tokens), float(gather_bytes), float(attn_bytes)], world)
+    if in_graph and int(tokens_all) != global_tokens:
+        raise RuntimeError(f"in-graph counts ({global_tokens} tokens) differ from the host sum "
+                           f"({int(tokens_all)})")
     out = {
         "rank": rank, "cfg": cfg, "recs": recs, "dev_s": dev_s_max, "wall_s": wall_s_max,
         "tokens": tokens_all, "attn_bytes": attn_bytes, "attn_s": attn_s,
+        "counts_collective": ("ncclAllReduce in the step graph (kvr_comm_init)" if in_graph else
+                              "torch.distributed all_reduce per step (gloo)" if world > 1 else "none"),
         "attn_bytes_all": attn_bytes_all,
         "gather_bytes": gather_bytes, "gather_s": gather_s, "gather_bytes_all": gather_bytes_all,
         "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "captures": captures,
@@ -464,6 +494,10 @@ def main():
                     help="b200.prefill_budget: cold prompt rows written per step (0 = all)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args.gpus)  # one process per GPU (does not return)
+    if "KVR_BENCH_DEVICE" in os.environ:  # several ranks on one GPU: NCCL refuses that
+        args.backend = "gloo"
     if args.impl == "reference":  # CPU only: rank 0 runs it, no process group, no GPU
         if int(os.environ.get("RANK", "0")) == 0:
             print(json.dumps(reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")))), flush=True)
@@ -521,7 +555,10 @@ def main():
                             "max_step": res["max_step"]},
         "step_phases_ms_mean": res["phases"],
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],
-                "d2h_bytes_per_step": 40},  # step counters (ScanCounters) read back
+                # step counters (ScanCounters, 40 B) + the all-reduced counts (4 x int64)
+                "d2h_bytes_per_step": 40 + (32 if res["counts_collective"].startswith("nccl") else 0)},
+        "multi_gpu": {"n_gpus": world, "shard": "request_id % n_gpus",
+                      "counts_collective": res["counts_collective"]},
         "gpu_launches": res["step_kernels"] * args.steps,
         "graph": {"kernels_per_step": res["step_kernels"], "captures": res["captures"],
                   "note": "one CUDA graph per descriptor ring slot, captured once, replayed every step"},
@@ -540,6 +577,23 @@ def main():
         except Exception as e:  # the oracle is absent: report, do not fake
             line["cpu_baseline"] = {"value": None, "unavailable": str(e)}
     print(json.dumps(line), flush=True)
+
+
+def spawn_ranks(n: int) -> None:
+    """Re-run this command as n ranks, one per GPU (torch.distributed.run, 127.0.0.1)."""
+    import socket
+    if "KVR_BENCH_DEVICE" not in os.environ and "--impl" not in sys.argv:
+        import torch
+        have = torch.cuda.device_count()
+        if have < n:
+            raise SystemExit(f"bench.py --gpus {n}: only {have} GPU(s) visible")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    os.execv(sys.executable, cmd)
 
 
 def reference_arm(args, world) -> dict:

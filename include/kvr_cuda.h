@@ -27,6 +27,10 @@ enum { KVR_QUERY_EXACT = 0, KVR_QUERY_F32 = 1 };
 #define KVR_NO_SLOT 0xffffffffu
 #define KVR_SUMMARY_BASE (1ull << 40) /* summary slots' logical tokens, scenario.cpp:41 */
 #define KVR_MAX_SCAN_NEEDS 2048u      /* K-scan: stage needs per step */
+/* per-step counts all-reduced across GPUs: live sessions, emitted
+ * tokens, commit frames (commits_observed, sim_engine.cpp:41-44), EOS this step */
+#define KVR_COUNTS 4
+enum { KVR_COUNT_LIVE = 0, KVR_COUNT_EMITTED = 1, KVR_COUNT_COMMITS = 2, KVR_COUNT_EOS = 3 };
 
 typedef struct kvr_geometry {
     int32_t device;
@@ -86,6 +90,8 @@ typedef struct kvr_step_header {
     uint64_t off_presum, off_presum_runs;
     uint32_t n_presum_runs, pad_h;
     uint64_t total_bytes;
+    int64_t counts[KVR_COUNTS]; /* this GPU's per-step counts (KVR_COUNT_*): the input of
+                                   the in-graph NCCL all-reduce when a communicator is set */
 } kvr_step_header;
 
 typedef struct kvr_zero_op { uint32_t block, slot_begin, slot_count, pad; } kvr_zero_op;
@@ -159,6 +165,8 @@ typedef struct kvr_step_stats {
     uint64_t writeback_tokens;
     uint64_t attn_bytes;
     uint64_t end_ns;          /* device %globaltimer at the end of the step */
+    int64_t global_counts[KVR_COUNTS]; /* the step's counts summed over all ranks of the
+                                          communicator (this GPU's own without one) */
 } kvr_step_stats;
 
 typedef struct kvr_dev kvr_dev;
@@ -216,6 +224,18 @@ const char *kvr_dev_attention_variant(kvr_dev *d);
  * kvr_dev_wait for it; valid until that ring slot is launched again): runs
  * [slot * near_window, + counts[slot]) of `out` (n_slots * near_window entries) */
 int kvr_dev_utility(kvr_dev *d, uint32_t ring_slot, kvr_mass_run *out, uint32_t *counts);
+/* ---- multi-GPU: per-step counts over NCCL (NVLink / NVSwitch) -------------------
+ * Requests shard by sequence; the KV data path never leaves its GPU. With a
+ * communicator, every step graph ends with ONE ncclAllReduce (sum, int64) of the
+ * descriptor's counts[KVR_COUNTS] into a device buffer, read back with the step
+ * stats: job-wide tok/s, termination and the job-wide single-commit audit. NCCL is
+ * loaded at run time (dlopen "libnccl.so.2", the copy already in the process when
+ * there is one). Call kvr_comm_init before the first kvr_dev_launch (the graphs are
+ * captured with the collective in them); every rank must launch the same number of
+ * steps. */
+int kvr_comm_unique_id(uint8_t id[128]); /* on one rank; the caller distributes it */
+int kvr_comm_init(kvr_dev *d, const uint8_t id[128], int rank, int world);
+int kvr_comm_world(kvr_dev *d, int *rank, int *world); /* (0, 1) without a communicator */
 /* kernel nodes in the captured step graph (0 before the first graph launch) */
 int kvr_dev_step_kernels(kvr_dev *d, uint32_t *out);
 /* step graphs captured so far: 2 (one per descriptor ring slot) after the first two

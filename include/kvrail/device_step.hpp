@@ -29,6 +29,7 @@
 
 #include "kvrail/payload_store.hpp"
 #include "kvrail/transport.hpp"
+#include "kvr_cuda.h"
 #include "kvrail_c.h"
 
 namespace kvrail {
@@ -47,6 +48,7 @@ struct DeviceStepStats {
     uint64_t h2d_bytes = 0;     // committed descriptor bytes published this step
     uint32_t scan_status = 0;   // 0 ok; else capacity overflow flags
     uint64_t end_ns = 0;        // device %globaltimer at the end of the step
+    int64_t global_counts[KVR_COUNTS] = {}; // KVR_COUNT_* summed over the communicator
 };
 
 class DeviceStep {
@@ -76,6 +78,11 @@ public:
     void prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end, SessionId src = kNoPrimeSource);
     void far_selection(uint32_t slot, std::span<const uint64_t> chunk_ids);
 
+    /// This GPU's per-step counts (KVR_COUNT_*), carried in the next launched descriptor
+    /// and all-reduced inside its graph when a communicator is set.
+    void counts(const int64_t c[KVR_COUNTS]);
+    /// Join the per-step counts all-reduce (kvr_comm_init) before the first launch.
+    void comm_init(const uint8_t id[128], int rank, int world);
     /// Seal the step descriptor, publish it and launch the step (async).
     void launch(uint64_t step, double now, const TransportConfig &tc);
     /// Stats of `step` (blocks until that step has finished on the device).

@@ -159,6 +159,9 @@ public:
     /// destination (window ring / far rows), near rows behind the live window (read from
     /// the arena: not part of the window), and rows missing from the window otherwise.
     void staged_rows(uint64_t &delivered, uint64_t &behind, uint64_t &missing) const;
+    /// Join the per-step counts all-reduce over NCCL (kvr_comm_init) before the first
+    /// step; records then carry job-wide counts and the single-commit audit is job-wide.
+    void comm_init(const uint8_t id[128], int rank, int world);
     /// Test hook (kvr_dev_fault): corrupt K-gather on every later step.
     void fault(int what, uint64_t arg);
 

@@ -205,6 +205,9 @@ typedef struct kvr_step_record { /* StepRecord, sim_engine.hpp:47-63 + measured 
     uint64_t h2d_bytes;        /* committed step descriptor bytes copied host -> device */
     uint64_t end_ns;           /* device %globaltimer at the end of the step: successive
                                   differences are the inter-token latency */
+    /* job-wide counts of this step: the in-graph NCCL all-reduce over every GPU of
+       the communicator (kvr_driver_comm_init); this GPU's own without one */
+    uint64_t global_live, global_emitted, global_commits, global_eos;
 } kvr_step_record;
 
 /* ---- Pager (pager.hpp:121-183) ------------------------------------------ */
@@ -328,6 +331,9 @@ int kvr_driver_device_check(kvr_driver *d, uint64_t *checked, uint64_t *mismatch
  * (window ring / far rows), near rows behind the live window (hashed from the arena:
  * not part of the window) and rows missing from the window for any other reason. */
 int kvr_driver_staged_rows(kvr_driver *d, uint64_t *delivered, uint64_t *behind, uint64_t *missing);
+/* Join the per-step counts all-reduce over NCCL (kvr_comm_init, kvr_cuda.h) before
+ * the first step: `id` from kvr_comm_unique_id on one rank, distributed by the caller. */
+int kvr_driver_comm_init(kvr_driver *d, const uint8_t id[128], int rank, int world);
 /* Test hook (fault injection, kvr_dev_fault): K-gather drops a span (KVR_FAULT_DROP_SPAN)
  * or misplaces near rows (KVR_FAULT_SHIFT_ROWS) on every later step. */
 int kvr_driver_fault(kvr_driver *d, int what, uint64_t arg);

@@ -11,8 +11,11 @@
 //   far    [slot][layer][max_chunks][2*d_kv] far-view summary rows
 //   q/out  [slot][layer][q_head][head_dim] f32
 //   desc   3 x max_desc_bytes               step descriptors (2 ring slots + apply-only)
+#include <cstddef>
 #include <cstdio>
 #include <algorithm>
+#include <dlfcn.h>
+#include <nccl.h>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -50,6 +53,12 @@ struct kvr_dev {
     bool in_flight[2] = {false, false};
     uint64_t pending_write_tokens[2] = {0, 0};
     std::vector<void *> allocs;
+    // per-step counts collective (kvr_comm_init)
+    ncclComm_t comm = nullptr;
+    int rank = 0, world = 1;
+    uint64_t n_launches = 0;
+    int64_t *d_counts = nullptr;                  // all-reduce result (device)
+    int64_t *h_counts[2] = {nullptr, nullptr};    // its D2H copy per ring slot (pinned)
 };
 
 namespace {
@@ -65,6 +74,39 @@ void ck(cudaError_t e, const char *what) {
         throw CudaFail(std::string("CUDA error in ") + what + ": " + cudaGetErrorString(e));
 }
 
+/// NCCL entry points, resolved at run time: the library already in the process
+/// (torch's) when there is one, else the system's.
+struct Nccl {
+    ncclResult_t (*get_unique_id)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*comm_init_rank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*all_reduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                               cudaStream_t) = nullptr;
+    ncclResult_t (*comm_destroy)(ncclComm_t) = nullptr;
+    const char *(*error_string)(ncclResult_t) = nullptr;
+};
+
+const Nccl &nccl() {
+    static Nccl api = [] {
+        Nccl a;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h)
+            h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h)
+            return a;
+        a.get_unique_id = reinterpret_cast<decltype(a.get_unique_id)>(dlsym(h, "ncclGetUniqueId"));
+        a.comm_init_rank = reinterpret_cast<decltype(a.comm_init_rank)>(dlsym(h, "ncclCommInitRank"));
+        a.all_reduce = reinterpret_cast<decltype(a.all_reduce)>(dlsym(h, "ncclAllReduce"));
+        a.comm_destroy = reinterpret_cast<decltype(a.comm_destroy)>(dlsym(h, "ncclCommDestroy"));
+        a.error_string = reinterpret_cast<decltype(a.error_string)>(dlsym(h, "ncclGetErrorString"));
+        return a;
+    }();
+    if (!api.get_unique_id || !api.comm_init_rank || !api.all_reduce || !api.comm_destroy)
+        throw std::runtime_error("NCCL (libnccl.so.2) is not loadable");
+    return api;
+}
+
+void nck(ncclResult_t r, const char *what);
+
 template <typename Fn> int guard(Fn &&fn) {
     try {
         fn();
@@ -76,6 +118,12 @@ template <typename Fn> int guard(Fn &&fn) {
         g_err = e.what();
         return KVR_E_BAD_CONFIG;
     }
+}
+
+void nck(ncclResult_t r, const char *what) {
+    if (r != ncclSuccess)
+        throw CudaFail(std::string("NCCL error in ") + what + ": " +
+                       (nccl().error_string ? nccl().error_string(r) : std::to_string(int(r))));
 }
 
 void *dalloc(kvr_dev *d, size_t bytes, const char *what) {
@@ -134,6 +182,11 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     // overlap saved, so the step runs them after it with the whole GPU.
     launch_write(c, s, d->sms, 1);
     launch_presum(c, s, d->sms);
+    // the step's counts summed over every rank (the only cross-GPU traffic)
+    if (d->comm)
+        nck(nccl().all_reduce(c.desc + offsetof(kvr_step_header, counts), d->d_counts, KVR_COUNTS, ncclInt64,
+                              ncclSum, d->comm, s),
+            "per-step counts all-reduce");
     launch_stamp(c, s);
     mark(7);
 }
@@ -270,7 +323,11 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
             void *p;
             ck(cudaMallocHost(&p, sizeof(ScanCounters)), "pinned stats");
             d->h_scan[i] = static_cast<ScanCounters *>(p);
+            ck(cudaMallocHost(&p, KVR_COUNTS * sizeof(int64_t)), "pinned counts");
+            d->h_counts[i] = static_cast<int64_t *>(p);
+            std::memset(p, 0, KVR_COUNTS * sizeof(int64_t));
         }
+        d->d_counts = static_cast<int64_t *>(dalloc(d.get(), KVR_COUNTS * sizeof(int64_t), "counts"));
         if (g.utility) {
             if (!g.attention || g.utility_layer >= g.layers || c.group > mass_max_group())
                 throw std::runtime_error("utility: needs attention, utility_layer < layers and q-group <= 16");
@@ -328,6 +385,8 @@ int kvr_dev_close(kvr_dev *d) {
                 cudaEventDestroy(d->ev_phase[i][j]);
         if (d->h_scan[i])
             cudaFreeHost(d->h_scan[i]);
+        if (d->h_counts[i])
+            cudaFreeHost(d->h_counts[i]);
         if (d->h_mass[i])
             cudaFreeHost(d->h_mass[i]);
         if (d->h_mass_count[i])
@@ -336,6 +395,8 @@ int kvr_dev_close(kvr_dev *d) {
     for (int i = 0; i < 3; ++i)
         if (d->h_desc[i])
             cudaFreeHost(d->h_desc[i]);
+    if (d->comm)
+        nccl().comm_destroy(d->comm);
     for (void *p : d->allocs)
         cudaFree(p);
     if (d->attn)
@@ -393,6 +454,12 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
         }
         ck(cudaMemcpyAsync(d->h_scan[k], c.scan, sizeof(ScanCounters), cudaMemcpyDeviceToHost, d->stream),
            "stats D2H");
+        if (d->comm)
+            ck(cudaMemcpyAsync(d->h_counts[k], d->d_counts, KVR_COUNTS * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                               d->stream),
+               "counts D2H");
+        else
+            std::memcpy(d->h_counts[k], h->counts, KVR_COUNTS * sizeof(int64_t));
         if (c.utility && h->step % c.utility == 0) {
             ck(cudaMemcpyAsync(d->h_mass_count[k], c.mass_count, uint64_t(c.n_slots) * 4, cudaMemcpyDeviceToHost,
                                d->stream),
@@ -404,6 +471,7 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
         ck(cudaEventRecord(d->ev_stop[k], d->stream), "event");
         d->launched[k] = h->step;
         d->in_flight[k] = true;
+        ++d->n_launches;
         d->pending_write_tokens[k] = h->write_tokens + h->write_tokens_cold + uint64_t(h->n_presum) * c.chunk_tokens;
     });
 }
@@ -451,6 +519,7 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
         out->end_ns = sc.end_ns;
         out->staged_tokens = sc.total_tokens;
         out->writeback_tokens = d->pending_write_tokens[k];
+        std::memcpy(out->global_counts, d->h_counts[k], sizeof(out->global_counts));
         d->in_flight[k] = false;
     });
 }
@@ -586,6 +655,39 @@ int kvr_dev_utility(kvr_dev *d, uint32_t k, kvr_mass_run *out, uint32_t *counts)
         for (uint32_t s = 0; s < c.n_slots; ++s)
             std::memcpy(out + uint64_t(s) * c.W, d->h_mass[k] + uint64_t(s) * c.W,
                         std::min<uint32_t>(counts[s], c.W) * sizeof(kvr_mass_run));
+    });
+}
+
+int kvr_comm_unique_id(uint8_t id[128]) {
+    return guard([&] {
+        ncclUniqueId u;
+        nck(nccl().get_unique_id(&u), "ncclGetUniqueId");
+        static_assert(sizeof(u) == 128, "ncclUniqueId is 128 bytes");
+        std::memcpy(id, &u, sizeof(u));
+    });
+}
+
+int kvr_comm_init(kvr_dev *d, const uint8_t id[128], int rank, int world) {
+    return guard([&] {
+        if (d->comm)
+            throw std::runtime_error("kvr_comm_init: communicator already set");
+        if (d->n_launches)
+            throw std::runtime_error("kvr_comm_init must precede the first step launch (graph capture)");
+        if (world < 1 || rank < 0 || rank >= world)
+            throw std::runtime_error("kvr_comm_init: bad rank / world");
+        ck(cudaSetDevice(d->g.device), "cudaSetDevice");
+        ncclUniqueId u;
+        std::memcpy(&u, id, sizeof(u));
+        nck(nccl().comm_init_rank(&d->comm, world, u, rank), "ncclCommInitRank");
+        d->rank = rank;
+        d->world = world;
+    });
+}
+
+int kvr_comm_world(kvr_dev *d, int *rank, int *world) {
+    return guard([&] {
+        *rank = d->rank;
+        *world = d->world;
     });
 }
 

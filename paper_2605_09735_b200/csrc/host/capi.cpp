@@ -379,6 +379,10 @@ static void fill_record(const StepRecord &r, kvr_step_record *o) {
         o->attn_bytes = r.attn_bytes;
         o->h2d_bytes = r.h2d_bytes;
         o->end_ns = r.end_ns;
+        o->global_live = r.global_live;
+        o->global_emitted = r.global_emitted;
+        o->global_commits = r.global_commits;
+        o->global_eos = r.global_eos;
 }
 
 int kvr_driver_step(kvr_driver *d, kvr_step_record *o) {
@@ -484,6 +488,10 @@ int kvr_driver_device_check(kvr_driver *d, uint64_t *checked, uint64_t *mismatch
 
 int kvr_driver_staged_rows(kvr_driver *d, uint64_t *delivered, uint64_t *behind, uint64_t *missing) {
     return call([&] { d->d->staged_rows(*delivered, *behind, *missing); });
+}
+
+int kvr_driver_comm_init(kvr_driver *d, const uint8_t id[128], int rank, int world) {
+    return call([&] { d->d->comm_init(id, rank, world); });
 }
 
 int kvr_driver_fault(kvr_driver *d, int what, uint64_t arg) {

@@ -210,6 +210,7 @@ struct DeviceStep::Impl {
     uint64_t launched_step[2] = {~0ull, ~0ull};
     std::vector<kvr_slot_state> launched_slots[2]; // slot states of the step in each ring slot
     uint64_t attn_bytes_pending[2] = {0, 0};
+    int64_t step_counts[KVR_COUNTS] = {};
     uint64_t desc_bytes_pending[2] = {0, 0};
 
     bool pending() const {
@@ -385,6 +386,7 @@ struct DeviceStep::Impl {
         h.n_presum_runs = uint32_t(presum_runs.size());
         h.off_presum_runs = place(presum_runs.size() * sizeof(kvr_presum_run));
         h.total_bytes = off;
+        std::memcpy(h.counts, step_counts, sizeof(h.counts));
         if (off > g.max_desc_bytes)
             throw std::runtime_error("step descriptor exceeds max_desc_bytes");
         auto *base = static_cast<uint8_t *>(dst);
@@ -717,6 +719,7 @@ void DeviceStep::launch(uint64_t step, double now, const TransportConfig &tc) {
         d.attn_bytes = m.attn_bytes_pending[k];
         d.h2d_bytes = m.desc_bytes_pending[k];
         d.end_ns = st.end_ns;
+        std::copy(st.global_counts, st.global_counts + KVR_COUNTS, d.global_counts);
         m.have_done[k] = true;
     }
     uint64_t attn = 0;
@@ -781,6 +784,7 @@ DeviceStepStats DeviceStep::collect(uint64_t step) {
         d.attn_bytes = m.attn_bytes_pending[k];
         d.h2d_bytes = m.desc_bytes_pending[k];
         d.end_ns = st.end_ns;
+        std::copy(st.global_counts, st.global_counts + KVR_COUNTS, d.global_counts);
         m.have_done[k] = true;
     }
     overflow(m.done[k]);
@@ -815,6 +819,12 @@ std::vector<std::pair<BlockId, double>> DeviceStep::utility(uint64_t step,
             for (const kvr_mass_run &r : runs[s])
                 obs.emplace_back(r.block, double(r.mass));
     return obs;
+}
+
+void DeviceStep::counts(const int64_t c[KVR_COUNTS]) { std::copy(c, c + KVR_COUNTS, impl_->step_counts); }
+
+void DeviceStep::comm_init(const uint8_t id[128], int rank, int world) {
+    ck(kvr_comm_init(impl_->dev, id, rank, world));
 }
 
 void DeviceStep::sync() { ck(kvr_dev_sync(impl_->dev)); }

@@ -54,6 +54,16 @@ void fill_device(StepRecord &r, const DeviceStepStats &ds) {
     r.attn_bytes = ds.attn_bytes;
     r.h2d_bytes = ds.h2d_bytes;
     r.end_ns = ds.end_ns;
+    r.global_live = uint64_t(ds.global_counts[KVR_COUNT_LIVE]);
+    r.global_emitted = uint64_t(ds.global_counts[KVR_COUNT_EMITTED]);
+    r.global_commits = uint64_t(ds.global_counts[KVR_COUNT_COMMITS]);
+    r.global_eos = uint64_t(ds.global_counts[KVR_COUNT_EOS]);
+    // the single-commit audit over every GPU of the job (sim_engine.cpp:41-44): the
+    // commit frames of all ranks equal their live sessions
+    if (r.global_commits != r.global_live)
+        raise(Errc::multi_commit, "step " + std::to_string(r.step) + " saw " + std::to_string(r.global_commits) +
+                                      " commits for " + std::to_string(r.global_live) +
+                                      " live sessions across the job");
 }
 constexpr SessionId kHolder = 0x7fffffff;
 
@@ -686,7 +696,7 @@ struct ScenarioDriver::Impl {
 
         std::vector<StageNeed> far_needs;
         std::vector<std::pair<BlockId, double>> obs;
-        uint64_t emitted = 0;
+        uint64_t emitted = 0, eos_now = 0;
         std::vector<size_t> order;
         for (uint32_t s = 0; s < width; ++s)
             if (slot_of[s] >= 0)
@@ -722,6 +732,7 @@ struct ScenarioDriver::Impl {
                 if (cfg.pager_enabled)
                     pager->trim_eos(r.id);
                 r.eos = true;
+                ++eos_now;
             } else if (cfg.pager_enabled) {
                 summarize(r, far_needs);
                 if (r.reserved_end - r.written <= 1 && r.next_span.empty())
@@ -878,6 +889,9 @@ struct ScenarioDriver::Impl {
         }
         prof.lap(5);
         if (dev) { // publish first: the trace then reads the bytes this step produced
+            const int64_t counts[KVR_COUNTS] = {int64_t(order.size()), int64_t(emitted), int64_t(commits),
+                                                int64_t(eos_now)};
+            dev->counts(counts);
             device_step(needs, need_first, now);
             if (cfg.b200.check)
                 check_device_scan(trains);
@@ -1148,6 +1162,14 @@ void ScenarioDriver::staged_rows(uint64_t &delivered, uint64_t &behind, uint64_t
     delivered = impl_->staged_rows_window;
     behind = impl_->staged_rows_behind;
     missing = impl_->staged_rows_missing;
+}
+
+void ScenarioDriver::comm_init(const uint8_t id[128], int rank, int world) {
+    if (!impl_->dev)
+        throw std::runtime_error("comm_init: host-only driver");
+    if (impl_->t != 0)
+        throw std::runtime_error("comm_init must precede the first step");
+    impl_->dev->comm_init(id, rank, world);
 }
 
 void ScenarioDriver::fault(int what, uint64_t arg) {

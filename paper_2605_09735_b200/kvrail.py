@@ -148,7 +148,9 @@ class StepRecord(C.Structure):
                 ("emitted_tokens", C.c_uint64), ("device_ms", C.c_double),
                 ("gather_ms", C.c_double), ("attn_ms", C.c_double), ("phase_ms", C.c_double * 8),
                 ("writeback_tokens", C.c_uint64), ("gather_bytes", C.c_uint64),
-                ("attn_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64), ("end_ns", C.c_uint64)]
+                ("attn_bytes", C.c_uint64), ("h2d_bytes", C.c_uint64), ("end_ns", C.c_uint64),
+                ("global_live", C.c_uint64), ("global_emitted", C.c_uint64),
+                ("global_commits", C.c_uint64), ("global_eos", C.c_uint64)]
 
 
 class Geometry(C.Structure):
@@ -284,6 +286,8 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_driver_device_check": [vp, U64P, U64P, C.c_char_p, C.c_uint64],
         "kvr_driver_staged_rows": [vp, U64P, U64P, U64P],
         "kvr_driver_fault": [vp, C.c_int, C.c_uint64],
+        "kvr_driver_comm_init": [vp, C.c_char_p, C.c_int, C.c_int],
+        "kvr_comm_unique_id": [C.c_char_p],
         "kvr_device_open": [C.POINTER(Geometry), C.POINTER(vp)],
         "kvr_device_close": [vp],
         "kvr_device_flush": [vp],
@@ -510,6 +514,15 @@ def reduce(descs: Sequence[tuple], tau: int, max_hold: float, merge: bool, now: 
 
 
 # ---- device -------------------------------------------------------------------
+def comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (128 bytes) for kvr_driver_comm_init; create it on one
+    rank and hand it to the others (e.g. with a torch.distributed broadcast)."""
+    api()
+    buf = C.create_string_buffer(128)
+    check(native_lib().kvr_comm_unique_id(buf))
+    return buf.raw
+
+
 def device_count() -> int:
     n = C.c_int(0)
     api()
@@ -759,6 +772,11 @@ class Driver:
         a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
         check(native_lib().kvr_driver_staged_rows(self.h, C.byref(a), C.byref(b), C.byref(c)))
         return a.value, b.value, c.value
+
+    def comm_init(self, unique_id: bytes, rank: int, world: int) -> None:
+        """Join the in-graph per-step counts all-reduce over NCCL (before the first step)."""
+        assert len(unique_id) == 128
+        check(native_lib().kvr_driver_comm_init(self.h, unique_id, rank, world))
 
     FAULT_DROP_SPAN, FAULT_SHIFT_ROWS, FAULT_ALL = 1, 2, 0xFFFFFFFFFFFFFFFE
 
