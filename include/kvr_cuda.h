@@ -26,7 +26,7 @@ enum { KVR_PAYLOAD_BYTES = 0, KVR_PAYLOAD_LANES = 1 };
 enum { KVR_QUERY_EXACT = 0, KVR_QUERY_F32 = 1 };
 #define KVR_NO_SLOT 0xffffffffu
 #define KVR_SUMMARY_BASE (1ull << 40) /* summary slots' logical tokens, scenario.cpp:41 */
-#define KVR_MAX_SCAN_NEEDS 2048u      /* K-scan: stage needs per step */
+#define KVR_MAX_SCAN_NEEDS 1024u      /* K-scan: stage needs per step */
 /* per-step counts all-reduced across GPUs: live sessions, emitted
  * tokens, commit frames (commits_observed, sim_engine.cpp:41-44), EOS this step */
 #define KVR_COUNTS 4

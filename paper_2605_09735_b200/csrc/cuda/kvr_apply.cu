@@ -20,45 +20,35 @@ namespace {
 __device__ inline void zero16(uint8_t *p) { *reinterpret_cast<int4 *>(p) = make_int4(0, 0, 0, 0); }
 
 // ---------------------------------------------------------------------------
-// K-apply: zero ops, then COW copies, then host blobs (three launches: a
-// recycled page may be a COW source in the same step).
-
-// Every op is spread over the whole grid (a zero run or a page copy can be
-// megabytes: one CTA per op left most SMs idle on span reservations).
-__global__ void k_zero(DevCtx c) {
+// K-apply: zero ops (recycled page slots), COW page copies and host blobs in ONE
+// kernel. The host keeps the three independent within a descriptor (a copy whose
+// source has a pending zero or write, or a blob into a copy's destination, splits
+// the wave: device_step.cpp), so they need no ordering here. Every op is spread
+// over the whole grid (a zero run or a page copy can be megabytes).
+__global__ void k_apply(DevCtx c) {
     const kvr_step_header *h = hdr(c);
-    const kvr_zero_op *ops = section<kvr_zero_op>(c, h->off_zero);
     const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, stride = uint64_t(gridDim.x) * blockDim.x;
+    const kvr_zero_op *zops = section<kvr_zero_op>(c, h->off_zero);
     for (uint32_t i = 0; i < h->n_zero; ++i) {
-        const kvr_zero_op op = ops[i];
+        const kvr_zero_op op = zops[i];
         uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot_begin) * c.token_bytes;
         const uint64_t n16 = uint64_t(op.slot_count) * c.token_bytes / 16;
         for (uint64_t k = tid; k < n16; k += stride)
             zero16(dst + 16 * k);
     }
-}
-
-__global__ void k_cow(DevCtx c) {
-    const kvr_step_header *h = hdr(c);
-    const kvr_cow_op *ops = section<kvr_cow_op>(c, h->off_cow);
-    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, stride = uint64_t(gridDim.x) * blockDim.x;
+    const kvr_cow_op *cops = section<kvr_cow_op>(c, h->off_cow);
     for (uint32_t i = 0; i < h->n_cow; ++i) {
-        const int4 *src = reinterpret_cast<const int4 *>(c.arena + uint64_t(ops[i].src) * c.page_bytes);
-        int4 *dst = reinterpret_cast<int4 *>(c.arena + uint64_t(ops[i].dst) * c.page_bytes);
+        const int4 *src = reinterpret_cast<const int4 *>(c.arena + uint64_t(cops[i].src) * c.page_bytes);
+        int4 *dst = reinterpret_cast<int4 *>(c.arena + uint64_t(cops[i].dst) * c.page_bytes);
         for (uint64_t k = tid; k < c.page_bytes / 16; k += stride)
             dst[k] = src[k];
     }
-}
-
-// Host payload bytes (Pager::write_tokens): blob offsets and token_bytes are
-// multiples of 16, so every op moves int4s, spread over the whole grid.
-__global__ void k_blob(DevCtx c) {
-    const kvr_step_header *h = hdr(c);
-    const kvr_blob_op *ops = section<kvr_blob_op>(c, h->off_blob_ops);
+    // host payload bytes (Pager::write_tokens): blob offsets and token_bytes are
+    // multiples of 16, so every op moves int4s
+    const kvr_blob_op *bops = section<kvr_blob_op>(c, h->off_blob_ops);
     const uint8_t *blob = c.desc + h->off_blob;
-    const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, stride = uint64_t(gridDim.x) * blockDim.x;
     for (uint32_t i = 0; i < h->n_blob; ++i) {
-        const kvr_blob_op op = ops[i];
+        const kvr_blob_op op = bops[i];
         int4 *dst = reinterpret_cast<int4 *>(c.arena + uint64_t(op.block) * c.page_bytes +
                                              uint64_t(op.slot) * c.token_bytes);
         const int4 *src = reinterpret_cast<const int4 *>(blob + op.blob_offset);
@@ -495,11 +485,7 @@ __global__ void k_prime(DevCtx c) {
 
 } // namespace
 
-void launch_apply(const DevCtx &c, cudaStream_t s, int sms) {
-    k_zero<<<sms * 4, 256, 0, s>>>(c);
-    k_cow<<<sms * 4, 256, 0, s>>>(c);
-    k_blob<<<sms * 2, 256, 0, s>>>(c);
-}
+void launch_apply(const DevCtx &c, cudaStream_t s, int sms) { k_apply<<<sms * 4, 256, 0, s>>>(c); }
 
 void launch_presum(const DevCtx &c, cudaStream_t s, int sms) {
     if (!c.stash)

@@ -12,6 +12,7 @@
 //   q/out  [slot][layer][q_head][head_dim] f32
 //   desc   3 x max_desc_bytes               step descriptors (2 ring slots + apply-only)
 #include <cstddef>
+#include <cstdlib>
 #include <cstdio>
 #include <algorithm>
 #include <dlfcn.h>
@@ -37,6 +38,8 @@ struct kvr_dev {
     kvr_geometry g{};
     int sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;                   // the step graph's forked branch (queries, K-scan)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     DevCtx base{};
     uint8_t *d_desc[3] = {nullptr, nullptr, nullptr};
     void *h_desc[3] = {nullptr, nullptr, nullptr};
@@ -57,6 +60,7 @@ struct kvr_dev {
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
     uint64_t n_launches = 0;
+    bool phase_events = true; // event nodes at every phase boundary (KVR_PHASE_EVENTS=0: K-attn only)
     int64_t *d_counts = nullptr;                  // all-reduce result (device)
     int64_t *h_counts[2] = {nullptr, nullptr};    // its D2H copy per ring slot (pinned)
 };
@@ -144,7 +148,7 @@ DevCtx ctx_for(const kvr_dev *d, int slot) {
 void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, bool capturing = false) {
     cudaStream_t s = d->stream;
     auto mark = [&](int i) {
-        if (k >= 0)
+        if (k >= 0 && (d->phase_events || i == 5 || i == 6)) // K-attn's pair is always kept
             ck(capturing ? cudaEventRecordWithFlags(d->ev_phase[k][i], s, cudaEventRecordExternal)
                          : cudaEventRecord(d->ev_phase[k][i], s),
                "phase event");
@@ -159,15 +163,23 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
         launch_prime(c, s, d->sms);
         return;
     }
+    // Side branch: the decode queries and K-scan depend only on the descriptor, so
+    // they run beside the byte kernels (one SM for K-scan's single CTA) and join
+    // before K-gather, off the step's critical path.
+    cudaStream_t side = d->side;
+    ck(cudaEventRecord(d->ev_fork, s), "fork"); // (under capture: a dependency, not a node)
+    ck(cudaStreamWaitEvent(side, d->ev_fork, 0), "fork wait");
+    launch_query(c, side, d->sms);
+    launch_scan(c, side);
+    ck(cudaEventRecord(d->ev_join, side), "join");
     mark(1);
     launch_write(c, s, d->sms, 0);
-    launch_query(c, s, d->sms);
     mark(2);
     launch_far(c, s, d->sms);
     launch_map(c, s, d->sms);
     launch_prime(c, s, d->sms);
     mark(3);
-    launch_scan(c, s);
+    ck(cudaStreamWaitEvent(s, d->ev_join, 0), "join wait");
     mark(4);
     launch_gather(c, s, d->sms);
     mark(5);
@@ -229,11 +241,16 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         if (scan_dynamic_smem(g.max_scan_descs) > (192u << 10)) // K-scan stages its arrays in shared memory
             throw std::runtime_error("max_scan_descs too large for K-scan's shared memory (<= 2048)");
         d->g = g;
+        if (const char *pe = getenv("KVR_PHASE_EVENTS"))
+            d->phase_events = std::string(pe) != "0";
         ck(cudaSetDevice(g.device), "cudaSetDevice");
         cudaDeviceProp prop;
         ck(cudaGetDeviceProperties(&prop, g.device), "cudaGetDeviceProperties");
         d->sms = prop.multiProcessorCount;
         ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
+        ck(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking), "side stream");
+        ck(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming), "fork event");
+        ck(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming), "join event");
         for (int i = 0; i < 2; ++i) {
             ck(cudaEventCreate(&d->ev_start[i]), "event");
             ck(cudaEventCreate(&d->ev_stop[i]), "event");
@@ -401,6 +418,12 @@ int kvr_dev_close(kvr_dev *d) {
         cudaFree(p);
     if (d->attn)
         free_attn_plan(d->attn);
+    if (d->ev_fork)
+        cudaEventDestroy(d->ev_fork);
+    if (d->ev_join)
+        cudaEventDestroy(d->ev_join);
+    if (d->side)
+        cudaStreamDestroy(d->side);
     if (d->stream)
         cudaStreamDestroy(d->stream);
     delete d;
@@ -506,7 +529,8 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
         out->device_ms = ms;
         for (int j = 0; j < 7; ++j) {
             float t = 0.f;
-            ck(cudaEventElapsedTime(&t, d->ev_phase[k][j], d->ev_phase[k][j + 1]), "elapsed");
+            if (d->phase_events || j == 5)
+                ck(cudaEventElapsedTime(&t, d->ev_phase[k][j], d->ev_phase[k][j + 1]), "elapsed");
             out->phase_ms[j] = t;
         }
         out->gather_ms = out->phase_ms[4];

@@ -10,6 +10,8 @@
 // shared->global to the destination, recycling a buffer once its store has
 // finished reading it (bulk_group read wait). Pure HBM-bound byte movement.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 #include "kvr_internal.cuh"
 
@@ -17,9 +19,9 @@ namespace kvr {
 
 namespace {
 
-constexpr int kStages = 8;  // stage buffers per CTA
-constexpr int kAhead = 6;   // loads in flight ahead of the stores
-constexpr uint32_t kMaxPiece = 8192; // rows larger than this move in pieces (3 CTAs per SM)
+constexpr int kStages = 6;              // stage buffers per CTA (one CTA per SM)
+constexpr int kAhead = 4;               // loads in flight ahead of the stores
+constexpr uint32_t kMaxPiece = 32768;   // stage bytes: one load of consecutive layer rows
 
 __device__ inline uint32_t smem_u32(const void *p) {
     return uint32_t(__cvta_generic_to_shared(p));
@@ -47,12 +49,12 @@ __device__ inline void bulk_g2s(void *dst, const void *src, uint32_t bytes, uint
                  "l"(src), "r"(bytes), "r"(smem_u32(bar))
                  : "memory");
 }
-__device__ inline void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+__device__ inline void bulk_s2g_nocommit(void *dst, const void *src, uint32_t bytes) {
     asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
                  "r"(smem_u32(src)), "r"(bytes)
                  : "memory");
-    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
 }
+__device__ inline void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N> __device__ inline void bulk_wait_read() {
     asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
 }
@@ -103,16 +105,18 @@ __device__ inline uint8_t *shifted_row(const DevCtx &c, uint8_t *dst, uint64_t s
     return c.ring + base + (within + (shift % c.R) * row_bytes) % ring_bytes;
 }
 
-/// Walks this CTA's contiguous range of units (token, layer, piece) with a
-/// forward-moving span cursor: no division or search per unit.
+/// Walks this CTA's contiguous range of units with a forward-moving span cursor (no
+/// division or search per unit). A unit is `lg` consecutive layers of one token —
+/// contiguous in the arena (token-major pages) — or, for rows larger than a stage,
+/// one piece of one layer row.
 struct Walker {
     uint64_t tok_idx;
-    uint32_t l, piece, cur;
-    __device__ void init(const DevCtx &c, uint32_t n_spans, uint64_t u0, uint32_t pieces) {
+    uint32_t grp, piece, cur;
+    __device__ void init(const DevCtx &c, uint32_t n_spans, uint64_t u0, uint32_t groups, uint32_t pieces) {
         piece = uint32_t(u0 % pieces);
-        const uint64_t row_unit = u0 / pieces;
-        l = uint32_t(row_unit % c.L);
-        tok_idx = row_unit / c.L;
+        const uint64_t gu = u0 / pieces;
+        grp = uint32_t(gu % groups);
+        tok_idx = gu / groups;
         uint32_t lo = 0, hi = n_spans; // last span with tok_prefix <= tok_idx
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) / 2;
@@ -123,45 +127,51 @@ struct Walker {
         }
         cur = lo;
     }
-    __device__ void advance(const DevCtx &c, uint32_t n_spans, uint32_t pieces) {
+    __device__ void advance(const DevCtx &c, uint32_t n_spans, uint32_t groups, uint32_t pieces) {
         if (++piece < pieces)
             return;
         piece = 0;
-        if (++l < c.L)
+        if (++grp < groups)
             return;
-        l = 0;
+        grp = 0;
         ++tok_idx;
         while (cur + 1 < n_spans && c.gspans[cur + 1].tok_prefix <= tok_idx)
             ++cur;
     }
-    __device__ Move resolve(const DevCtx &c, const kvr_slot_state *slots, uint32_t piece_bytes) const {
-        const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
-        const uint64_t off0 = uint64_t(piece) * piece_bytes;
-        Move m = span_row(c, slots, c.gspans[cur], tok_idx, l);
-        if (m.dst) {
-            m.src += off0;
-            m.dst += off0;
-            m.bytes = uint32_t(row_bytes - off0 < piece_bytes ? row_bytes - off0 : piece_bytes);
-        }
-        return m;
-    }
 };
 
-// One warp per CTA; lane 0 drives a kStages-deep ring over the CTA's contiguous
-// unit range: loads run kAhead units in front of the stores, and a buffer is
-// refilled only after the store that last read it has drained (bulk_group read
-// wait with kStages-kAhead-1 groups still allowed in flight).
-__global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
+/// A unit in flight: one bulk load of `bytes` into a stage, `nl` bulk stores of
+/// `row` bytes each (consecutive layers: destinations one ring plane apart).
+struct Unit {
+    uint8_t *dst0;        // destination of the first layer
+    uint64_t dst_stride;  // bytes between the layers' destinations
+    uint32_t row, nl;
+};
+
+// One warp per CTA, one CTA per SM: lane 0 drives a kStages-deep ring of
+// kMaxPiece-byte stages over the CTA's contiguous unit range. Loads run kAhead
+// units in front of the stores; a stage is reloaded only after the stores that
+// read it have drained (bulk_group read wait). A unit is up to kMaxPiece / row
+// consecutive layers of one token: ONE load (contiguous in the arena), then one
+// store per layer into that layer's window ring plane.
+__global__ void __launch_bounds__(32, 1) k_gather(DevCtx c) {
     extern __shared__ __align__(128) uint8_t stage[];
     __shared__ __align__(8) uint64_t full[kStages];
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
     const uint32_t n_spans = c.scan->spans;
-    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
-    const uint32_t pieces = uint32_t((row_bytes + piece_bytes - 1) / piece_bytes);
-    const uint64_t units = c.scan->total_tokens * c.L * pieces;
-    if (units == 0 || (c.scan->status & 4u) || threadIdx.x != 0)
+    const uint64_t tokens = c.scan->total_tokens;
+    if (tokens == 0 || (c.scan->status & 4u) || threadIdx.x != 0)
         return;
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    const uint32_t pieces = row_bytes > kMaxPiece ? uint32_t((row_bytes + kMaxPiece - 1) / kMaxPiece) : 1;
+    // layers per unit: as many as fill a stage, fewer when the step is small (keep
+    // >= 8 units per CTA so every SM streams)
+    uint32_t lg = pieces > 1 ? 1 : uint32_t(c.L < kMaxPiece / row_bytes ? c.L : kMaxPiece / row_bytes);
+    while (lg > 1 && tokens * ((c.L + lg - 1) / lg) < 8ull * gridDim.x)
+        lg = (lg + 1) / 2;
+    const uint32_t groups = (c.L + lg - 1) / lg;
+    const uint64_t units = tokens * groups * pieces;
     const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
     const uint64_t u0 = blockIdx.x * per, u1 = units < u0 + per ? units : u0 + per;
     if (u0 >= u1)
@@ -170,24 +180,37 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
         mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     Walker wk;
-    wk.init(c, n_spans, u0, pieces);
+    wk.init(c, n_spans, u0, groups, pieces);
     const uint64_t drop = c.fault[0], shift = c.fault[1]; // test hooks (off: ~0, 0)
     uint64_t next = u0;
-    Move mv[kStages];
+    Unit mv[kStages];
     uint32_t phase_bits = 0;
     auto issue = [&](int s) {
         while (next < u1) {
-            Move m = wk.resolve(c, slots, piece_bytes);
+            const GSpan &sp = c.gspans[wk.cur];
+            const uint32_t l0 = wk.grp * lg, nl = min(lg, c.L - l0);
+            Move m = span_row(c, slots, sp, wk.tok_idx, l0);
             if (drop != ~0ull && (wk.cur == drop || drop == KVR_FAULT_ALL))
                 m.dst = nullptr;
-            else if (shift && m.dst && c.gspans[wk.cur].kind == 0)
-                m.dst = shifted_row(c, m.dst, shift);
-            ++next;
-            wk.advance(c, n_spans, pieces);
+            Unit u{};
             if (m.dst) {
-                mv[s] = m;
-                mbar_expect_tx(&full[s], m.bytes);
-                bulk_g2s(stage + size_t(s) * piece_bytes, m.src, m.bytes, &full[s]);
+                const uint64_t off0 = uint64_t(wk.piece) * kMaxPiece;
+                u.row = pieces > 1 ? uint32_t(row_bytes - off0 < kMaxPiece ? row_bytes - off0 : kMaxPiece) : uint32_t(row_bytes);
+                u.nl = nl;
+                u.dst0 = m.dst + off0;
+                if (shift && sp.kind == 0)
+                    u.dst0 = shifted_row(c, u.dst0, shift);
+                // the next layer's row: one ring plane (R rows) / far plane further
+                u.dst_stride = (sp.kind == 0 ? uint64_t(c.R) : uint64_t(c.max_chunks)) * row_bytes;
+                m.src += off0;
+            }
+            ++next;
+            wk.advance(c, n_spans, groups, pieces);
+            if (u.dst0) {
+                mv[s] = u;
+                const uint32_t bytes = u.row * u.nl;
+                mbar_expect_tx(&full[s], bytes);
+                bulk_g2s(stage + size_t(s) * kMaxPiece, m.src, bytes, &full[s]);
                 return true;
             }
         }
@@ -200,7 +223,10 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
         const int s = int(stored % kStages);
         mbar_wait(&full[s], (phase_bits >> s) & 1u);
         phase_bits ^= 1u << s;
-        bulk_s2g(mv[s].dst, stage + size_t(s) * piece_bytes, mv[s].bytes);
+        const Unit &u = mv[s];
+        for (uint32_t j = 0; j < u.nl; ++j)
+            bulk_s2g_nocommit(u.dst0 + j * u.dst_stride, stage + size_t(s) * kMaxPiece + size_t(j) * u.row, u.row);
+        bulk_commit();
         ++stored;
         // next load reuses the stage stored (kStages - kAhead) groups ago
         bulk_wait_read<kStages - kAhead - 1>();
@@ -208,6 +234,102 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c, uint32_t piece_bytes) {
             ++issued;
     }
     bulk_wait_all();
+}
+
+// Register-staged variant: every warp of a full-occupancy grid walks its own
+// contiguous range of (token, layer, 4 KiB piece) units; each lane moves 8 int4 of
+// a unit (two units in flight: 16 loads per lane before their stores), so the whole
+// transfer of a small step is in flight at once instead of trickling through one
+// issuing lane per SM. Same work list, same destinations, same fault hooks.
+constexpr uint32_t kVecPiece = 4096; // bytes per unit (8 int4 per lane)
+constexpr int kVecWarps = 8;         // warps per CTA
+
+struct VecUnit {
+    const int4 *src;
+    int4 *dst;
+    uint32_t n16; // int4s in the unit
+};
+
+__global__ void __launch_bounds__(32 * kVecWarps) k_gather_vec(DevCtx c) {
+    const kvr_step_header *h = hdr(c);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint32_t n_spans = c.scan->spans;
+    const uint64_t tokens = c.scan->total_tokens;
+    if (tokens == 0 || (c.scan->status & 4u))
+        return;
+    const uint32_t lane = threadIdx.x & 31;
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    const uint32_t pieces = uint32_t((row_bytes + kVecPiece - 1) / kVecPiece);
+    const uint64_t units = tokens * c.L * pieces;
+    const uint64_t warps = uint64_t(gridDim.x) * kVecWarps;
+    const uint64_t w = uint64_t(blockIdx.x) * kVecWarps + (threadIdx.x >> 5);
+    const uint64_t per = (units + warps - 1) / warps;
+    const uint64_t u0 = w * per, u1 = units < u0 + per ? units : u0 + per;
+    if (u0 >= u1)
+        return;
+    const uint64_t drop = c.fault[0], shift = c.fault[1]; // test hooks (off: ~0, 0)
+    // cursor: (token, layer, piece) of unit u, span cur holding the token
+    uint32_t piece = uint32_t(u0 % pieces), l = uint32_t((u0 / pieces) % c.L);
+    uint64_t tok_idx = u0 / pieces / c.L;
+    uint32_t cur = 0;
+    {
+        uint32_t lo = 0, hi = n_spans;
+        while (hi - lo > 1) {
+            const uint32_t mid = (lo + hi) / 2;
+            if (c.gspans[mid].tok_prefix <= tok_idx)
+                lo = mid;
+            else
+                hi = mid;
+        }
+        cur = lo;
+    }
+    auto next_unit = [&](VecUnit &vu) {
+        const GSpan sp = c.gspans[cur];
+        Move m = span_row(c, slots, sp, tok_idx, l);
+        if (drop != ~0ull && (cur == drop || drop == KVR_FAULT_ALL))
+            m.dst = nullptr;
+        else if (shift && m.dst && sp.kind == 0)
+            m.dst = shifted_row(c, m.dst, shift);
+        const uint64_t off0 = uint64_t(piece) * kVecPiece;
+        const uint64_t n = row_bytes - off0 < kVecPiece ? row_bytes - off0 : kVecPiece;
+        vu.src = reinterpret_cast<const int4 *>(m.src + off0);
+        vu.dst = m.dst ? reinterpret_cast<int4 *>(m.dst + off0) : nullptr;
+        vu.n16 = uint32_t(n / 16);
+        if (++piece == pieces) {
+            piece = 0;
+            if (++l == c.L) {
+                l = 0;
+                ++tok_idx;
+                while (cur + 1 < n_spans && c.gspans[cur + 1].tok_prefix <= tok_idx)
+                    ++cur;
+            }
+        }
+    };
+    constexpr int kPer = kVecPiece / 16 / 32; // int4 per lane per unit
+    for (uint64_t u = u0; u < u1; u += 2) {
+        VecUnit a, b;
+        next_unit(a);
+        const bool two = u + 1 < u1;
+        if (two)
+            next_unit(b);
+        int4 va[kPer], vb[kPer];
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const uint32_t q = lane + 32u * i;
+            if (a.dst && q < a.n16)
+                va[i] = __ldcs(a.src + q);
+            if (two && b.dst && q < b.n16)
+                vb[i] = __ldcs(b.src + q);
+        }
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            const uint32_t q = lane + 32u * i;
+            if (a.dst && q < a.n16)
+                a.dst[q] = va[i];
+            if (two && b.dst && q < b.n16)
+                b.dst[q] = vb[i];
+        }
+    }
 }
 
 // Parity read-back: one CTA per gather-order token; layer rows from the destination
@@ -261,21 +383,29 @@ void launch_read_staged(const DevCtx &c, cudaStream_t s, uint64_t tok_begin, uin
         k_read_staged<<<unsigned(count < 4096 ? count : 4096), 256, 0, s>>>(c, tok_begin, count, out, in_window);
 }
 
-uint32_t gather_piece_bytes(const DevCtx &c) {
-    const uint64_t row = uint64_t(c.row_elems) * c.esz;
-    return uint32_t(row <= kMaxPiece ? row : kMaxPiece);
+namespace {
+// KVR_GATHER=tma selects the TMA bulk-copy kernel (A/B); the default is the
+// register-staged kernel
+bool gather_tma() {
+    static const bool tma = [] {
+        const char *e = getenv("KVR_GATHER");
+        return e && std::string(e) == "tma";
+    }();
+    return tma;
+}
+} // namespace
+
+cudaError_t prepare_gather(const DevCtx &) {
+    return cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kStages * kMaxPiece));
 }
 
-cudaError_t prepare_gather(const DevCtx &c) {
-    const int smem = int(kStages * gather_piece_bytes(c));
-    return cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-}
+const char *gather_variant() { return gather_tma() ? "k_gather (TMA bulk, 1 issuing lane/SM)" : "k_gather_vec"; }
 
 void launch_gather(const DevCtx &c, cudaStream_t s, int sms) {
-    const uint32_t piece = gather_piece_bytes(c);
-    const size_t smem = size_t(kStages) * piece;
-    const int per_sm = int(std::min<size_t>(32, (200u << 10) / smem));
-    k_gather<<<sms * std::max(per_sm, 1), 32, smem, s>>>(c, piece);
+    if (gather_tma())
+        k_gather<<<sms, 32, size_t(kStages) * kMaxPiece, s>>>(c);
+    else
+        k_gather_vec<<<sms * 2, 32 * kVecWarps, 0, s>>>(c); // one wave (2 CTAs per SM)
 }
 
 } // namespace kvr

@@ -12,13 +12,14 @@
 //      within a run, parallel across runs);
 //   4. emit descriptors and trains in train order plus the span list K-gather
 //      walks (with token prefix sums).
+#include <cstdlib>
+
 #include "kvr_internal.cuh"
 
 namespace kvr {
 
 namespace {
 
-constexpr int kScanThreads = 1024;
 constexpr int kMaxNeeds = KVR_MAX_SCAN_NEEDS;
 
 // Exclusive block-wide scan of one value per thread; returns the block total.
@@ -54,18 +55,20 @@ __device__ uint64_t block_exclusive_scan(uint64_t v, uint64_t &excl, uint64_t *w
 
 struct ScanSmem {
     uint64_t warp_tot[32];
+    kvr_need_rec need[kMaxNeeds]; // the step's needs, staged once (no dependent global loads)
     uint32_t need_m[kMaxNeeds];   // non-empty spans per need
     uint32_t need_d[kMaxNeeds];   // descriptors per need
     uint32_t need_base[kMaxNeeds];
 };
 
-__global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
+template <int kScanThreads> __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
     extern __shared__ __align__(16) uint8_t dyn[];
     __shared__ ScanSmem sm;
     __shared__ uint32_t s_status;
     const kvr_step_header *h = hdr(c);
-    const kvr_need_rec *needs = section<kvr_need_rec>(c, h->off_need);
+    const kvr_need_rec *g_needs = section<kvr_need_rec>(c, h->off_need);
     const kvr_span_rec *spans = section<kvr_span_rec>(c, h->off_span);
+    const kvr_need_rec *needs = sm.need;
     const uint32_t cap = c.max_scan;
     // dynamic smem: cap entries per array
     uint64_t *d_off = reinterpret_cast<uint64_t *>(dyn);
@@ -81,6 +84,7 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
     uint32_t *run_cnt = run_start + cap;                      // trains per run -> train base
     uint64_t *sp_b = reinterpret_cast<uint64_t *>(run_cnt + cap); // span byte offset (staged once)
     uint64_t *sp_l = sp_b + cap;                                  // span bytes (0: empty span)
+    uint64_t *sp_first = sp_l + cap;                              // span's first logical token
 
     const uint32_t n_need = h->n_need;
     if (threadIdx.x == 0)
@@ -90,12 +94,16 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
     // every span's byte range staged in shared memory by all threads at once: the
     // per-need insertion sort below then compares in shared memory instead of
     // chasing dependent global loads
-    if (!s_status)
+    if (!s_status) {
         for (uint32_t i = threadIdx.x; i < h->n_span; i += blockDim.x) {
             const kvr_span_rec sp = spans[i];
             sp_b[i] = uint64_t(sp.block) * page + uint64_t(sp.slot_begin) * tb;
             sp_l[i] = uint64_t(sp.slot_count) * tb;
+            sp_first[i] = sp.first_token;
         }
+        for (uint32_t i = threadIdx.x; i < n_need; i += blockDim.x)
+            sm.need[i] = g_needs[i];
+    }
     __syncthreads();
 
     // ---- 1. stage: per-need insertion sort by (offset, length) + fusion ----
@@ -334,18 +342,19 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
             c.descs[i] = o;
             uint64_t g = carry_s + sx, tok = carry_t + tx;
             for (uint32_t k = 0; k < d_nsp[d]; ++k) {
-                const kvr_span_rec sp = spans[sidx[d_first[d] + k]];
+                const uint32_t si = sidx[d_first[d] + k];
+                const uint64_t b = sp_b[si];
                 GSpan gs;
-                gs.first_token = sp.first_token;
+                gs.first_token = sp_first[si];
                 gs.tok_prefix = tok;
-                gs.block = sp.block;
-                gs.slot_begin = sp.slot_begin;
-                gs.slot_count = sp.slot_count;
+                gs.block = uint32_t(b / page);
+                gs.slot_begin = uint32_t((b % page) / tb);
+                gs.slot_count = uint32_t(sp_l[si] / tb);
                 gs.dev_slot = nd.slot;
                 gs.kind = nd.kind;
                 gs.pad = 0;
                 c.gspans[g++] = gs;
-                tok += sp.slot_count;
+                tok += gs.slot_count;
             }
         }
         carry_s += ts;
@@ -366,14 +375,39 @@ __global__ void __launch_bounds__(kScanThreads, 1) k_scan(DevCtx c) {
 
 } // namespace
 
-size_t scan_dynamic_smem(uint32_t cap) { return size_t(cap) * (5 * 8 + 8 * 4); }
+size_t scan_dynamic_smem(uint32_t cap) { return size_t(cap) * (6 * 8 + 8 * 4); }
+
+namespace {
+int scan_threads() {
+    static const int t = [] {
+        const char *e = getenv("KVR_SCAN_THREADS");
+        const int v = e ? atoi(e) : 256;
+        return v == 128 || v == 512 || v == 1024 ? v : 256;
+    }();
+    return t;
+}
+} // namespace
 
 void launch_scan(const DevCtx &c, cudaStream_t s) {
-    k_scan<<<1, kScanThreads, scan_dynamic_smem(c.max_scan), s>>>(c);
+    const size_t smem = scan_dynamic_smem(c.max_scan);
+    switch (scan_threads()) {
+    case 128: k_scan<128><<<1, 128, smem, s>>>(c); break;
+    case 512: k_scan<512><<<1, 512, smem, s>>>(c); break;
+    case 1024: k_scan<1024><<<1, 1024, smem, s>>>(c); break;
+    default: k_scan<256><<<1, 256, smem, s>>>(c); break;
+    }
 }
 
 cudaError_t prepare_scan(uint32_t cap) {
-    return cudaFuncSetAttribute(k_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, int(scan_dynamic_smem(cap)));
+    const int smem = int(scan_dynamic_smem(cap));
+    cudaError_t e = cudaFuncSetAttribute(k_scan<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_scan<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_scan<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_scan<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    return e;
 }
 
 } // namespace kvr

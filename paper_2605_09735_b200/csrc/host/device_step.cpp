@@ -8,10 +8,12 @@
 //   copy_page  -> COW ops;  write -> host blob ops;  write_generated -> write
 //                 ops (token payloads, far summaries);
 //   on_commit  -> page-table edits for sessions bound to a device slot.
-// Within one descriptor the device runs zero -> cow -> blob -> write -> far ->
-// map -> prime -> scan -> gather -> attn. Sequences whose result depends on a
-// different order (a page written and then COW-copied, written twice, ...) are
-// split: the earlier part is flushed as an apply-only descriptor first.
+// Within one descriptor the device runs {zero | cow | blob} (one kernel, no order
+// among them) -> write -> far -> map -> prime -> gather -> attn (queries and K-scan
+// on a parallel branch). Sequences whose result depends on an order the descriptor
+// does not give (a page written or zeroed and then COW-copied, a blob into a copy's
+// destination, a slot written twice, ...) are split: the earlier part is flushed
+// as an apply-only descriptor first.
 #include <algorithm>
 #include <cstring>
 #include <deque>
@@ -495,8 +497,9 @@ struct DeviceStep::Impl {
 
     void copy_page(BlockId src, BlockId dst) {
         drain_deferred(src); // the copy must see src's deferred prefill rows
-        if (wave_slots.count(src) || wave_cow_dst.count(src))
-            flush(); // the copy must see this wave's writes to src
+        if (wave_slots.count(src) || wave_cow_dst.count(src) || zero_pages.count(src))
+            flush(); // the copy must see this wave's writes / zeroing of src (K-apply runs
+                     // zero ops, copies and blobs of one wave concurrently)
         // the copy overwrites dst entirely; a pending zero of dst is moot
         if (zero_pages.erase(dst))
             zero_order.erase(std::remove(zero_order.begin(), zero_order.end(), dst), zero_order.end());
@@ -507,8 +510,8 @@ struct DeviceStep::Impl {
 
     void write_host(BlockId b, uint32_t slot, uint32_t count, const std::byte *bytes) {
         const uint64_t n = uint64_t(count) * g.token_bytes;
-        if (align16(blob.size() + n) + 65536 > g.max_desc_bytes / 2)
-            flush();
+        if (align16(blob.size() + n) + 65536 > g.max_desc_bytes / 2 || wave_cow_dst.count(b))
+            flush(); // (a blob into this wave's copy destination must follow the copy)
         note_slots(b, slot, count);
         blob_ops.push_back({blob.size(), b, slot, count, 0});
         blob.insert(blob.end(), reinterpret_cast<const uint8_t *>(bytes),
