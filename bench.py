@@ -295,7 +295,8 @@ def run_b200(args, rank, local, world) -> dict | None:
 
     latency = args.sync_steps  # synchronise every step: wall latency incl. host work
     fill_cap = 0 if args.config == "c4" else 400  # burst replay runs from step 0
-    cfg = CONFIGS[args.config](fill_cap + args.warmup + args.steps, rank, world)
+    extra = args.sustained + 48  # the sustained run and the K-gather timing step after the timed region
+    cfg = CONFIGS[args.config](fill_cap + args.warmup + args.steps + extra, rank, world)
     if args.prefill_budget:
         cfg["b200"]["prefill_budget"] = args.prefill_budget
     if args.attention_kernel != "auto":
@@ -355,6 +356,26 @@ def run_b200(args, rank, local, world) -> dict | None:
     recs = [d.record(s) for s in range(first, first + args.steps)]
     # in-graph counts (the job-wide single-commit audit ran in the driver per step)
     global_tokens = sum(r.global_emitted for r in recs)
+    # Sustained: the next `--sustained` steps, the same way (device time per step);
+    # reported beside the headline, not folded into it.
+    sus_first = d.progress()[0]
+    for _ in range(args.sustained):
+        d.step()
+    d.sync()
+    sus = [d.record(s) for s in range(sus_first, sus_first + args.sustained)]
+    sus_tokens, sus_dev = reduce_sum([float(sum(r.emitted_tokens for r in sus))], world)[0], \
+        reduce_max([sum(r.device_ms for r in sus) / 1e3], world)[0]
+    # K-gather alone (kvr_dev_time_gather: back-to-back replays on the last step's
+    # descriptor): advance to a step that staged trains (all ranks step together)
+    gstep = None
+    for _ in range(48):
+        r = d.step()
+        d.sync()
+        rec = d.record(r.step)
+        if all_filled(rec.gather_bytes > 0, world):
+            gstep = rec
+            break
+    gather_us = d.device().time_gather(20) * 1e3 if gstep is not None else None
     # inter-token latency: successive step-end %globaltimer stamps (pipelined steps)
     itl_ms = [(recs[i].end_ns - recs[i - 1].end_ns) / 1e6 for i in range(1, len(recs))]
     if args.dump_steps and rank == 0:  # per-step records for latency analysis
@@ -409,6 +430,14 @@ def run_b200(args, rank, local, world) -> dict | None:
         "latency_steps": len(lat_ms), "first_step": first,
         "max_step": max(range(len(recs)), key=lambda i: recs[i].device_ms) + first,
     }
+    out.update({
+        "sustained": {"steps": args.sustained, "value": sus_tokens / sus_dev if sus_dev else None,
+                      "ms_per_step": sus_dev / max(1, args.sustained) * 1e3,
+                      "note": "the steps right after the timed region, timed the same way (device "
+                              "time, max over ranks); admissions and EOS keep arriving"},
+        "gather_kernel": {"bytes_read": gstep.gather_bytes if gstep is not None else None,
+                          "us_per_launch": gather_us, "step": gstep.step if gstep is not None else None},
+    })
     d.close()
     return out
 
@@ -454,17 +483,20 @@ def cpu_baseline_block(res: dict, threads: int | None = None) -> dict:
     cfg = res["cfg"]
     b = cfg["b200"]
     threads = threads or os.cpu_count() or 1
+    fv = cfg["far_view"]
+    window = fv["w_star"] + (fv.get("cap", 0) if fv.get("enabled") else 0)
     leg = cb.decode_step(cfg, live=round(res["live_mean"]), layers=cfg["pager"]["layers"],
-                         q_heads=b["q_heads"], head_dim=b["head_dim"],
-                         window=cfg["far_view"]["w_star"], dma_bytes_per_step=res["dma_mean"],
-                         threads=threads, attention_calls=512 * threads)
+                         q_heads=b["q_heads"], head_dim=b["head_dim"], window=window,
+                         dma_bytes_per_step=res["dma_mean"], threads=threads)
     return {"value": leg["tokens_per_s"], "unit": "tokens/s", "cores": leg["threads"],
             "kind": "reference",
-            "sample": (f"{leg['attention_calls_timed']} of the {leg['attention_calls_per_step']} "
-                       f"reference build_view+attend calls of one {cfg['label']} decode step (W*={cfg['far_view']['w_star']}, hd="
-                       f"{b['head_dim']}) on {leg['threads']} OpenMP threads + run_scenario "
-                       f"control plane (200 steps, 1 thread, kv_head_dim and page "
-                       f"shrunk by one power of two) + memcpy gather of the mean train bytes"),
+            "sample": (f"one whole {cfg['label']} decode step: all {leg['attention_calls_per_step']} "
+                       f"reference build_view+attend calls (W*+far={window}, hd={b['head_dim']}, "
+                       f"extrapolation x{leg['attention_extrapolation']:.0f}) on {leg['threads']} OpenMP "
+                       f"threads over 512 MiB of distinct fp32 histories + run_scenario control plane "
+                       f"(200 steps, 1 thread, kv_head_dim and page shrunk by one power of two: same "
+                       f"decisions) + Pager::read_slots of the mean staged bytes at the real geometry"),
+            "extrapolation": leg["attention_extrapolation"],
             "legs_s": {"control": leg["control_s"], "attention": leg["attention_s"],
                        "gather": leg["gather_s"]}}
 
@@ -490,6 +522,8 @@ def main():
                     help="b200.utility: placement observations (attention = measured by K-mass)")
     ap.add_argument("--utility-every", type=int, default=1,
                     help="b200.utility_every: K-mass runs on every N-th step")
+    ap.add_argument("--sustained", type=int, default=200,
+                    help="steps run and reported (`sustained`) after the timed region")
     ap.add_argument("--prefill-budget", type=int, default=0,
                     help="b200.prefill_budget: cold prompt rows written per step (0 = all)")
     args = ap.parse_args()
@@ -515,7 +549,8 @@ def main():
     value = res["tokens"] / res["dev_s"]
     e2e = res["tokens"] / res["wall_s"]
     attn_gbs = res["attn_bytes"] / res["attn_s"] / 1e9 if res["attn_s"] else 0.0
-    gather_gbs = 2 * res["gather_bytes"] / res["gather_s"] / 1e9 if res["gather_s"] else 0.0
+    gk = res["gather_kernel"]
+    gather_gbs = 2 * gk["bytes_read"] / (gk["us_per_launch"] * 1e-6) / 1e9 if gk["us_per_launch"] else None
     traffic, traffic_src = ncu_traffic(args.config, res["variant"])
     roof_tps = res["tokens"] / (res["attn_bytes_all"] / (world * pk["hbm_gbs"] * 1e9))
     line = {
@@ -523,15 +558,10 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": res["dev_s"] / args.steps * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype,
         "data": f"synthetic: seeded reference payload pattern (fill_token_payload lanes, RNE {dtype})",
-        "config": {
-            "workload": WORKLOADS[args.config],
-            "page_bytes": pc["page_bytes"], "tokens_per_page": pc["page_bytes"] // tb,
-            "tau_bytes": cfg["transport"]["tau_bytes"],
-            "requests_shard": "request_id % n_gpus", "l2": "inputs larger than L2 "
-            f"(~{res['attn_bytes'] / args.steps / 2**30:.1f} GiB of window KV read per step vs 126 MB L2)",
-            "attention_kernel": res["variant"], "fill_steps": res["fill_steps"],
-            "prefill_budget": args.prefill_budget, "utility": args.utility,
-        },
+        "config": bench_config(args, cfg),
+        "run": {"attention_kernel": res["variant"], "fill_steps": res["fill_steps"],
+                "kv_read_per_step_gib": res["attn_bytes"] / args.steps / 2**30},
+        "sustained": res["sustained"],
         "prefill": {"budget_tokens_per_step": args.prefill_budget,
                     "queued_tokens_at_end": res["prefill_backlog"],
                     "never_written_tokens": res["prefill_dropped"],
@@ -539,6 +569,11 @@ def main():
                             "budget, rows behind the window are queued and dropped unwritten if "
                             "their page is recycled before any read"},
         "gather_hbm_gbs": gather_gbs,
+        "gather": {"hbm_gbs": gather_gbs, "frac": gather_gbs / pk["hbm_gbs"] if gather_gbs else None,
+                   "bytes_per_launch": 2 * gk["bytes_read"] if gk["bytes_read"] else None,
+                   "us_per_launch": gk["us_per_launch"],
+                   "basis": "(read + write) train bytes of one step / K-gather alone, 20 back-to-back "
+                            "replays on that step's descriptor (CUDA events)"},
         # decode tok/s roofline = tokens / (KV bytes the attention must read / peak)
         "decode_roofline": {
             "tokens_per_s": roof_tps,
@@ -579,6 +614,17 @@ def main():
     print(json.dumps(line), flush=True)
 
 
+def bench_config(args, cfg: dict) -> dict:
+    """The workload as both arms print it (`config`): static, identical for b200 and reference."""
+    pc = cfg["pager"]
+    tb = 2 * pc["layers"] * pc["kv_head_dim"] * pc["elem_bytes"]
+    return {"workload": WORKLOADS[args.config], "page_bytes": pc["page_bytes"],
+            "tokens_per_page": pc["page_bytes"] // tb, "tau_bytes": cfg["transport"]["tau_bytes"],
+            "requests_shard": "request_id % n_gpus",
+            "l2": "inputs larger than L2 (GiBs of window KV read per step vs 126 MB L2)",
+            "prefill_budget": args.prefill_budget, "utility": args.utility}
+
+
 def spawn_ranks(n: int) -> None:
     """Re-run this command as n ranks, one per GPU (torch.distributed.run, 127.0.0.1)."""
     import socket
@@ -599,37 +645,38 @@ def spawn_ranks(n: int) -> None:
 def reference_arm(args, world) -> dict:
     """The reference's CPU implementation of the step (oracle/_ref) on the same
     workload: run_scenario control plane (shrunk geometry, identical decisions),
-    memcpy of the staged bytes it schedules, and build_view + attend per
-    (session, layer, q-head) on all host threads — a sample per step,
-    extrapolated to the full batch."""
+    Pager::read_slots of the staged bytes it schedules (real geometry), and
+    build_view + attend for every (session, layer, q-head) of the step on all host
+    threads — no extrapolation."""
     from oracle import cpu_baseline as cb
     cfg = CONFIGS[args.config](400, 0, 1)
     b = cfg["b200"]
     ctl = cb.control_plane(cfg)
     live = round(ctl["live_mean"])
-    gbs = cb.memcpy_gbs()
+    t_gather = cb.gather_seconds(cfg, ctl["dma_bytes_per_step"])
     threads = os.cpu_count() or 1
     window = cfg["far_view"]["w_star"] + (cfg["far_view"].get("cap", 0) if cfg["far_view"].get("enabled") else 0)
     calls = live * cfg["pager"]["layers"] * b["q_heads"]
-    sample = min(calls, 512 * threads)
     per_step = []
-    for i in range(args.warmup + args.steps):
-        t_attn = cb.attention_seconds(b["head_dim"], window, sample, threads) * calls / sample
+    for i in range(args.warmup + args.steps):  # every step: all of its attention calls
+        t_attn = cb.attention_seconds(b["head_dim"], window, calls, threads)
         if i >= args.warmup:
-            per_step.append(ctl["seconds_per_step"] + t_attn + 2.0 * ctl["dma_bytes_per_step"] / (gbs * 1e9))
+            per_step.append(ctl["seconds_per_step"] + t_attn + t_gather)
     total = sum(per_step)
     value = live * len(per_step) / total
     return {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total / len(per_step) * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64 (reference attend)",
-            "data": "synthetic", "config": {"workload": WORKLOADS[args.config] + " (same as the b200 arm)"},
+            "data": "synthetic", "config": bench_config(args, cfg),
             "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": threads,
-                             "kind": "reference",
-                             "sample": f"per timed step {sample} of the {calls} reference "
-                                       f"build_view+attend calls of a {cfg['label']} step "
-                                       "(extrapolated), all threads, + run_scenario control plane "
-                                       "(shrunk geometry) + memcpy of its staged bytes"},
+                             "kind": "reference", "extrapolation": 1,
+                             "sample": f"every timed step: all {calls} reference build_view+attend "
+                                       f"calls of a {cfg['label']} step (W*+far={window}) on all "
+                                       "threads over 512 MiB of distinct fp32 histories, + "
+                                       "run_scenario control plane per step (shrunk geometry, same "
+                                       "decisions) + Pager::read_slots of its staged bytes at the "
+                                       "real geometry"},
             "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
 

@@ -27,7 +27,8 @@ namespace kvrail {
 
 /// B200 extension of the scenario (JSON key "b200"; ignored by the reference).
 struct B200Config {
-    int device = -1;          // CUDA device; < 0 = host-only twin driver
+    int device = -1;          // CUDA device; < 0 = host-only twin driver (run_scenario: the
+                              // KVRAIL_B200_DEVICE environment variable, when set)
     uint32_t kv_heads = 0;    // 0: 1 head of kv_head_dim
     uint32_t head_dim = 0;    // 0: kv_head_dim / kv_heads
     uint32_t q_heads = 0;     // 0: kv_heads (MHA); GQA group = q_heads / kv_heads

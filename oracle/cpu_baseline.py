@@ -6,10 +6,12 @@ own sources (oracle/_ref, kind "reference"):
      kv_head_dim and page_bytes shrunk by one power of two (identical tokens-per-page, page
      counts and tau in pages, so every pager / stage / reduce decision is the
      same; only payload bytes shrink), single thread, wall time per step;
-  2. gather: host memcpy of the step's train bytes at the reference's
-     single-thread copy bandwidth (read + write);
+  2. gather: the step's train bytes read through the reference's own
+     Pager::read_slots (a reference Pager at the real geometry holding that many
+     written tokens) into a host staging window, single thread;
   3. attention: kvrail_ref::build_view + kvrail_ref::attend per (session, layer,
-     q-head) over the W*-token window, OpenMP over all host threads.
+     q-head) over the W*-token window, OpenMP over all host threads, cycling over
+     512 MiB of distinct fp32 histories (reads from DRAM, not a cache-hot window).
 tokens/s = live / (t1 + t2 + t3).
 """
 from __future__ import annotations
@@ -24,9 +26,11 @@ from . import bindings as ob
 
 def _lib():
     lib = ob.ref()
-    lib.kvr_ref_cpu_attention_sample.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_int,
+    lib.kvr_ref_cpu_attention_sample.argtypes = [C.c_uint32, C.c_uint32, C.c_uint32, C.c_int, C.c_uint32,
                                                  C.POINTER(C.c_double), C.POINTER(C.c_double)]
     lib.kvr_ref_cpu_memcpy_gbs.argtypes = [C.c_uint64, C.c_int, C.POINTER(C.c_double)]
+    lib.kvr_ref_cpu_gather_seconds.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint64,
+                                               C.c_int, C.POINTER(C.c_double)]
     return lib
 
 
@@ -72,9 +76,13 @@ def control_plane(config: dict, steps: int = 200) -> dict:
     return {"seconds_per_step": wall / steps, "dma_bytes_per_step": dma, "live_mean": live}
 
 
+POOL_BYTES = 512 << 20  # distinct fp32 histories cycled through (beyond any host cache)
+
+
 def attention_seconds(head_dim: int, window: int, calls: int, threads: int) -> float:
     secs, chk = C.c_double(), C.c_double()
-    rc = _lib().kvr_ref_cpu_attention_sample(head_dim, window, calls, threads, C.byref(secs),
+    pool = max(1, POOL_BYTES // (window * 2 * head_dim * 4))
+    rc = _lib().kvr_ref_cpu_attention_sample(head_dim, window, calls, threads, pool, C.byref(secs),
                                              C.byref(chk))
     if rc:
         raise RuntimeError(ob.ref().kvr_ref_last_error().decode())
@@ -89,6 +97,18 @@ def memcpy_gbs(nbytes: int = 256 << 20, reps: int = 4) -> float:
     return g.value
 
 
+def gather_seconds(config: dict, nbytes: float, reps: int = 2) -> float:
+    """Seconds to read `nbytes` of staged tokens through the reference Pager::read_slots
+    at the config's real geometry (one pass, mean of `reps`)."""
+    p = config["pager"]
+    s = C.c_double()
+    rc = _lib().kvr_ref_cpu_gather_seconds(p["page_bytes"], p["layers"], p["kv_head_dim"], p["elem_bytes"],
+                                           int(max(nbytes, 1)), reps, C.byref(s))
+    if rc:
+        raise RuntimeError(ob.ref().kvr_ref_last_error().decode())
+    return s.value
+
+
 def decode_step(config: dict, live: int, layers: int, q_heads: int, head_dim: int, window: int,
                 dma_bytes_per_step: float, threads: int | None = None,
                 attention_calls: int | None = None) -> dict:
@@ -99,12 +119,13 @@ def decode_step(config: dict, live: int, layers: int, q_heads: int, head_dim: in
     t_ctl = control_plane_seconds_per_step(config)
     t_attn_sample = attention_seconds(head_dim, window, calls, threads)
     t_attn = t_attn_sample * calls_per_step / calls
-    gbs = memcpy_gbs()
-    t_gather = 2.0 * dma_bytes_per_step / (gbs * 1e9)
+    t_gather = gather_seconds(config, dma_bytes_per_step)
     total = t_ctl + t_attn + t_gather
     return {
         "tokens_per_s": live / total, "seconds_per_step": total, "control_s": t_ctl,
-        "attention_s": t_attn, "gather_s": t_gather, "memcpy_gbs": gbs, "threads": threads,
+        "attention_s": t_attn, "gather_s": t_gather, "threads": threads,
+        "gather_gbs": 2.0 * dma_bytes_per_step / t_gather / 1e9 if t_gather else None,
+        "attention_extrapolation": calls_per_step / calls,
         "attention_calls_timed": calls, "attention_calls_per_step": calls_per_step,
         "attention_sample_s": t_attn_sample,
     }

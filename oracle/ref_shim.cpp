@@ -503,12 +503,15 @@ void kvr_ref_free(char *p) { std::free(p); }
 // fixed-width view of a `window`-token history through a TokenReader (the
 // near-window gather, far_view.cpp:64-111) and attend over it (far_view.cpp:113-
 // 155). `calls` such (session, head) evaluations run on `threads` OpenMP threads
-// (build_view/attend are serial inside); returns wall seconds.
-int kvr_ref_cpu_attention_sample(uint32_t head_dim, uint32_t window, uint32_t calls, int threads,
+// (build_view/attend are serial inside); returns wall seconds. Calls cycle over
+// `pool` distinct histories (a pool larger than the host caches makes the reads
+// come from DRAM, as a real batch's KV would).
+int kvr_ref_cpu_attention_sample(uint32_t head_dim, uint32_t window, uint32_t calls, int threads, uint32_t pool,
                                  double *seconds, double *checksum) {
     return guard([&] {
         const uint32_t lanes = 2 * head_dim;
-        std::vector<float> hist(size_t(window) * lanes);
+        pool = pool ? pool : 1;
+        std::vector<float> hist(size_t(pool) * window * lanes);
         for (size_t i = 0; i < hist.size(); ++i)
             hist[i] = float(int64_t((i * 2654435761ull) % 2001) - 1000) / 1000.0f;
         std::vector<float> q(head_dim);
@@ -523,8 +526,9 @@ int kvr_ref_cpu_attention_sample(uint32_t head_dim, uint32_t window, uint32_t ca
         const auto t0 = std::chrono::steady_clock::now();
 #pragma omp parallel for num_threads(threads) schedule(dynamic, 4) reduction(+ : sum)
         for (int64_t c = 0; c < int64_t(calls); ++c) {
+            const float *h = hist.data() + size_t(c % pool) * window * lanes;
             TokenReader read = [&](uint64_t tok, float *out) {
-                std::memcpy(out, hist.data() + tok * lanes, lanes * sizeof(float));
+                std::memcpy(out, h + tok * lanes, lanes * sizeof(float));
             };
             SummarizedView v = build_view(read, window, {}, lanes, cfg);
             auto o = attend(v, q, 0, head_dim);
@@ -548,6 +552,48 @@ int kvr_ref_cpu_memcpy_gbs(uint64_t bytes, int reps, double *gbs) {
             std::memcpy(r & 1 ? a.data() : b.data(), r & 1 ? b.data() : a.data(), bytes);
         const auto t1 = std::chrono::steady_clock::now();
         *gbs = 2.0 * double(bytes) * reps / std::chrono::duration<double>(t1 - t0).count() / 1e9;
+    });
+}
+
+// The gather leg through the reference's own API: a reference Pager at the real
+// geometry holding `bytes` of written tokens (whole pages, one session), then
+// Pager::read_slots of every token into a host staging window, page run by page run
+// — the bytes the step's trains stage, copied the way the reference
+// reads them. Returns wall seconds per pass (mean over `reps`).
+int kvr_ref_cpu_gather_seconds(uint64_t page_bytes, uint32_t layers, uint32_t kv_head_dim, uint32_t elem_bytes,
+                               uint64_t bytes, int reps, double *seconds) {
+    return guard([&] {
+        PagerConfig pc;
+        pc.page_bytes = page_bytes;
+        pc.layers = layers;
+        pc.kv_head_dim = kv_head_dim;
+        pc.elem_bytes = elem_bytes;
+        const uint64_t tb = pc.token_bytes(), tpp = pc.tokens_per_page();
+        const uint64_t tokens = (bytes + tb - 1) / tb;
+        pc.arena_pages = uint32_t((tokens + tpp - 1) / tpp + 1);
+        Pager p(pc);
+        p.create_session(1);
+        p.reserve(1, tokens);
+        std::vector<std::byte> payload(tb);
+        for (uint64_t t = 0; t < tokens; ++t) {
+            std::memset(payload.data(), int(t & 0xff), tb);
+            p.write_tokens(1, {t, t + 1}, payload);
+        }
+        p.frame_commit(1, 0);
+        const ViewDescriptor v = p.active_view(1);
+        std::vector<std::byte> window(tokens * tb);
+        double total = 0.0;
+        for (int r = 0; r < reps; ++r) {
+            const auto t0 = std::chrono::steady_clock::now();
+            uint64_t at = 0;
+            for (const ViewEntry &e : v.entries) {
+                const uint32_t n = uint32_t(e.tokens.end - e.tokens.begin);
+                p.read_slots(e.block, e.slot_begin, n, window.data() + at);
+                at += uint64_t(n) * tb;
+            }
+            total += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+        }
+        *seconds = total / reps;
     });
 }
 

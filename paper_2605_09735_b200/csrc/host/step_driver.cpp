@@ -1195,7 +1195,14 @@ RunResult ScenarioDriver::result() const {
 }
 
 RunResult run_scenario_on(const ScenarioConfig &cfg, const std::vector<TraceEvent> &events) {
-    ScenarioDriver d(cfg, events);
+    // Drop-in callers of the reference API (run_scenario, the reference's own
+    // acceptance suite) select the B200 path with KVRAIL_B200_DEVICE=<cuda device>
+    // when their config does not name one (b200.device < 0, the reference's default).
+    ScenarioConfig c = cfg;
+    if (c.b200.device < 0)
+        if (const char *e = std::getenv("KVRAIL_B200_DEVICE"); e && *e)
+            c.b200.device = std::atoi(e);
+    ScenarioDriver d(c, events);
     while (!d.done())
         d.step();
     return d.result();
