@@ -299,6 +299,7 @@ def run_b200(args, rank, local, world) -> dict | None:
     cfg = CONFIGS[args.config](fill_cap + args.warmup + args.steps + extra, rank, world)
     if args.prefill_budget:
         cfg["b200"]["prefill_budget"] = args.prefill_budget
+    cfg["b200"]["transfer"] = args.transfer
     if args.attention_kernel != "auto":
         cfg["b200"]["attention_kernel"] = args.attention_kernel
     if args.utility != "synthetic":
@@ -416,6 +417,8 @@ def run_b200(args, rank, local, world) -> dict | None:
         "prefill_backlog": backlog, "prefill_dropped": dropped, "clocks": clocks.summary(), "fill_steps": fill,
         "live_mean": statistics.mean(r.live_sessions for r in recs),
         "trains_mean": statistics.mean(r.trains for r in recs),
+        "trains_p90": nearest_rank([float(r.trains) for r in recs], 0.90),
+        "trains_max": max(r.trains for r in recs),
         "dma_mean": statistics.mean(r.dma_bytes for r in recs),
         "mean_train_bytes": (sum(r.dma_bytes for r in recs) / max(1, sum(r.trains for r in recs))),
         "phases": {name: statistics.mean(r.phase_ms[i] for r in recs) for i, name in enumerate(
@@ -522,6 +525,9 @@ def main():
                     help="b200.utility: placement observations (attention = measured by K-mass)")
     ap.add_argument("--utility-every", type=int, default=1,
                     help="b200.utility_every: K-mass runs on every N-th step")
+    ap.add_argument("--transfer", default="page_runs", choices=["page_runs", "reference"],
+                    help="b200.transfer: train grouping (page_runs: physically consecutive pages merge "
+                         "across page-end slack; identical to the reference where pages hold whole tokens)")
     ap.add_argument("--sustained", type=int, default=200,
                     help="steps run and reported (`sustained`) after the timed region")
     ap.add_argument("--prefill-budget", type=int, default=0,
@@ -580,8 +586,9 @@ def main():
             "frac": value / roof_tps,
             "note": "whole step (writes, scan, gather, attention, host) against the attention's "
                     "algorithmic KV bytes at the measured copy bandwidth"},
-        "transport": {"trains_per_step": res["trains_mean"], "mean_train_bytes":
-                      res["mean_train_bytes"], "live_mean": res["live_mean"]},
+        "transport": {"trains_per_step": res["trains_mean"], "trains_p90": res["trains_p90"],
+                      "trains_max": res["trains_max"], "policy": args.transfer,
+                      "mean_train_bytes": res["mean_train_bytes"], "live_mean": res["live_mean"]},
         "step_latency_ms": {"p50": res["p50_ms"], "p99": res["p99_ms"], "clock": "device",
                             "itl_p50": res["itl_p50_ms"], "itl_p99": res["itl_p99_ms"],
                             "itl_note": "inter-token latency: differences of the step-end "
@@ -622,7 +629,7 @@ def bench_config(args, cfg: dict) -> dict:
             "tokens_per_page": pc["page_bytes"] // tb, "tau_bytes": cfg["transport"]["tau_bytes"],
             "requests_shard": "request_id % n_gpus",
             "l2": "inputs larger than L2 (GiBs of window KV read per step vs 126 MB L2)",
-            "prefill_budget": args.prefill_budget, "utility": args.utility}
+            "prefill_budget": args.prefill_budget, "utility": args.utility, "transfer": args.transfer}
 
 
 def spawn_ranks(n: int) -> None:

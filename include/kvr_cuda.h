@@ -92,6 +92,8 @@ typedef struct kvr_step_header {
     uint64_t total_bytes;
     int64_t counts[KVR_COUNTS]; /* this GPU's per-step counts (KVR_COUNT_*): the input of
                                    the in-graph NCCL all-reduce when a communicator is set */
+    uint64_t run_page, run_span; /* TransportConfig::run_page_bytes / run_span_bytes (page-run
+                                    merge, a B200 policy; 0 = exact abutment only) */
 } kvr_step_header;
 
 typedef struct kvr_zero_op { uint32_t block, slot_begin, slot_count, pad; } kvr_zero_op;

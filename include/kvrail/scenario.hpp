@@ -36,6 +36,10 @@ struct B200Config {
                                    // lane pattern rounded to dtype (finite for attention);
                                    // "wide": the same bytes as lanes of [-16, 16) (peaked softmax)
     std::string query = "exact";   // decode queries: "exact" in the KV type | "f32" (24-bit)
+    std::string transfer = "reference"; // transfer groups: "reference" (exact byte abutment,
+                                        // bit-exact with the reference) | "page_runs" (B200
+                                        // policy: physically consecutive pages merge across
+                                        // page-end slack, TransportConfig::run_page_bytes)
     std::string dtype = "auto";    // fp16 | bf16 | fp32 | auto (elem_bytes 4 -> fp32, 2 -> fp16)
     bool trace = false;            // record the per-step parity trace
     bool attention = true;         // run the window attention kernel each step

@@ -19,8 +19,6 @@ namespace kvr {
 
 namespace {
 
-constexpr int kStages = 6;              // stage buffers per CTA (one CTA per SM)
-constexpr int kAhead = 4;               // loads in flight ahead of the stores
 constexpr uint32_t kMaxPiece = 32768;   // stage bytes: one load of consecutive layer rows
 
 __device__ inline uint32_t smem_u32(const void *p) {
@@ -154,7 +152,8 @@ struct Unit {
 // read it have drained (bulk_group read wait). A unit is up to kMaxPiece / row
 // consecutive layers of one token: ONE load (contiguous in the arena), then one
 // store per layer into that layer's window ring plane.
-__global__ void __launch_bounds__(32, 1) k_gather(DevCtx c) {
+template <int kStages, int kAhead>
+__global__ void __launch_bounds__(32) k_gather(DevCtx c) {
     extern __shared__ __align__(128) uint8_t stage[];
     __shared__ __align__(8) uint64_t full[kStages];
     const kvr_step_header *h = hdr(c);
@@ -236,13 +235,12 @@ __global__ void __launch_bounds__(32, 1) k_gather(DevCtx c) {
     bulk_wait_all();
 }
 
-// Register-staged variant: every warp of a full-occupancy grid walks its own
-// contiguous range of (token, layer, 4 KiB piece) units; each lane moves 8 int4 of
-// a unit (two units in flight: 16 loads per lane before their stores), so the whole
-// transfer of a small step is in flight at once instead of trickling through one
-// issuing lane per SM. Same work list, same destinations, same fault hooks.
-constexpr uint32_t kVecPiece = 4096; // bytes per unit (8 int4 per lane)
-constexpr int kVecWarps = 8;         // warps per CTA
+// Register-staged variant: every warp of a full-occupancy grid moves (token, layer,
+// kUnit-byte piece) units, kFly of them in flight (all their loads before their
+// stores); each lane moves kUnit / 512 int4 of a unit. kInterleave: warp w takes
+// units w, w + W, ... (concurrent warps touch neighbouring addresses) instead of a
+// contiguous range. Same work list, destinations and fault hooks as k_gather.
+constexpr int kVecWarps = 8; // warps per CTA
 
 struct VecUnit {
     const int4 *src;
@@ -250,6 +248,7 @@ struct VecUnit {
     uint32_t n16; // int4s in the unit
 };
 
+template <int kUnit, int kFly, bool kInterleave>
 __global__ void __launch_bounds__(32 * kVecWarps) k_gather_vec(DevCtx c) {
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
@@ -259,21 +258,21 @@ __global__ void __launch_bounds__(32 * kVecWarps) k_gather_vec(DevCtx c) {
         return;
     const uint32_t lane = threadIdx.x & 31;
     const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
-    const uint32_t pieces = uint32_t((row_bytes + kVecPiece - 1) / kVecPiece);
+    const uint32_t pieces = uint32_t((row_bytes + kUnit - 1) / kUnit);
     const uint64_t units = tokens * c.L * pieces;
     const uint64_t warps = uint64_t(gridDim.x) * kVecWarps;
     const uint64_t w = uint64_t(blockIdx.x) * kVecWarps + (threadIdx.x >> 5);
     const uint64_t per = (units + warps - 1) / warps;
-    const uint64_t u0 = w * per, u1 = units < u0 + per ? units : u0 + per;
+    const uint64_t u0 = kInterleave ? w : w * per;
+    const uint64_t u1 = kInterleave ? units : (units < u0 + per ? units : u0 + per);
+    const uint64_t ustep = kInterleave ? warps : 1;
     if (u0 >= u1)
         return;
     const uint64_t drop = c.fault[0], shift = c.fault[1]; // test hooks (off: ~0, 0)
-    // cursor: (token, layer, piece) of unit u, span cur holding the token
-    uint32_t piece = uint32_t(u0 % pieces), l = uint32_t((u0 / pieces) % c.L);
-    uint64_t tok_idx = u0 / pieces / c.L;
-    uint32_t cur = 0;
-    {
-        uint32_t lo = 0, hi = n_spans;
+    auto unit_of = [&](uint64_t u, VecUnit &vu) {
+        const uint32_t piece = uint32_t(u % pieces), l = uint32_t((u / pieces) % c.L);
+        const uint64_t tok_idx = u / pieces / c.L;
+        uint32_t lo = 0, hi = n_spans; // last span with tok_prefix <= tok_idx
         while (hi - lo > 1) {
             const uint32_t mid = (lo + hi) / 2;
             if (c.gspans[mid].tok_prefix <= tok_idx)
@@ -281,54 +280,46 @@ __global__ void __launch_bounds__(32 * kVecWarps) k_gather_vec(DevCtx c) {
             else
                 hi = mid;
         }
-        cur = lo;
-    }
-    auto next_unit = [&](VecUnit &vu) {
-        const GSpan sp = c.gspans[cur];
+        const GSpan sp = c.gspans[lo];
         Move m = span_row(c, slots, sp, tok_idx, l);
-        if (drop != ~0ull && (cur == drop || drop == KVR_FAULT_ALL))
+        if (drop != ~0ull && (lo == drop || drop == KVR_FAULT_ALL))
             m.dst = nullptr;
         else if (shift && m.dst && sp.kind == 0)
             m.dst = shifted_row(c, m.dst, shift);
-        const uint64_t off0 = uint64_t(piece) * kVecPiece;
-        const uint64_t n = row_bytes - off0 < kVecPiece ? row_bytes - off0 : kVecPiece;
+        const uint64_t off0 = uint64_t(piece) * kUnit;
+        const uint64_t n = row_bytes - off0 < kUnit ? row_bytes - off0 : kUnit;
         vu.src = reinterpret_cast<const int4 *>(m.src + off0);
         vu.dst = m.dst ? reinterpret_cast<int4 *>(m.dst + off0) : nullptr;
         vu.n16 = uint32_t(n / 16);
-        if (++piece == pieces) {
-            piece = 0;
-            if (++l == c.L) {
-                l = 0;
-                ++tok_idx;
-                while (cur + 1 < n_spans && c.gspans[cur + 1].tok_prefix <= tok_idx)
-                    ++cur;
-            }
-        }
     };
-    constexpr int kPer = kVecPiece / 16 / 32; // int4 per lane per unit
-    for (uint64_t u = u0; u < u1; u += 2) {
-        VecUnit a, b;
-        next_unit(a);
-        const bool two = u + 1 < u1;
-        if (two)
-            next_unit(b);
-        int4 va[kPer], vb[kPer];
+    constexpr int kPer = kUnit / 16 / 32; // int4 per lane per unit
+    for (uint64_t u = u0; u < u1; u += ustep * kFly) {
+        VecUnit a[kFly];
+        int4 v[kFly][kPer];
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            const uint32_t q = lane + 32u * i;
-            if (a.dst && q < a.n16)
-                va[i] = __ldcs(a.src + q);
-            if (two && b.dst && q < b.n16)
-                vb[i] = __ldcs(b.src + q);
+        for (int f = 0; f < kFly; ++f) {
+            const uint64_t uf = u + uint64_t(f) * ustep;
+            if (uf < u1)
+                unit_of(uf, a[f]);
+            else
+                a[f].dst = nullptr;
         }
 #pragma unroll
-        for (int i = 0; i < kPer; ++i) {
-            const uint32_t q = lane + 32u * i;
-            if (a.dst && q < a.n16)
-                a.dst[q] = va[i];
-            if (two && b.dst && q < b.n16)
-                b.dst[q] = vb[i];
-        }
+        for (int f = 0; f < kFly; ++f)
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const uint32_t q = lane + 32u * i;
+                if (a[f].dst && q < a[f].n16)
+                    v[f][i] = __ldcs(a[f].src + q);
+            }
+#pragma unroll
+        for (int f = 0; f < kFly; ++f)
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {
+                const uint32_t q = lane + 32u * i;
+                if (a[f].dst && q < a[f].n16)
+                    a[f].dst[q] = v[f][i];
+            }
     }
 }
 
@@ -384,28 +375,36 @@ void launch_read_staged(const DevCtx &c, cudaStream_t s, uint64_t tok_begin, uin
 }
 
 namespace {
-// KVR_GATHER=tma selects the TMA bulk-copy kernel (A/B); the default is the
-// register-staged kernel
-bool gather_tma() {
-    static const bool tma = [] {
+// KVR_GATHER selects the K-gather kernel (A/B): tma (6 x 32 KiB stages, 4 loads
+// ahead, 1 CTA/SM; default) | tma5 (5 ahead) | tma2 (3 stages, 2 ahead, 2 CTAs/SM)
+// | vec (register-staged, 4 KiB units, 2 in flight) | ivec (interleaved)
+int gather_kind() {
+    static const int k = [] {
         const char *e = getenv("KVR_GATHER");
-        return e && std::string(e) == "tma";
+        const std::string v = e ? e : "";
+        return v == "tma5" ? 1 : v == "tma2" ? 2 : v == "vec" ? 3 : v == "ivec" ? 4 : 0;
     }();
-    return tma;
+    return k;
 }
 } // namespace
 
 cudaError_t prepare_gather(const DevCtx &) {
-    return cudaFuncSetAttribute(k_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, int(kStages * kMaxPiece));
+    cudaError_t e = cudaFuncSetAttribute(k_gather<6, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(6 * kMaxPiece));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_gather<6, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(6 * kMaxPiece));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_gather<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(3 * kMaxPiece));
+    return e;
 }
 
-const char *gather_variant() { return gather_tma() ? "k_gather (TMA bulk, 1 issuing lane/SM)" : "k_gather_vec"; }
-
 void launch_gather(const DevCtx &c, cudaStream_t s, int sms) {
-    if (gather_tma())
-        k_gather<<<sms, 32, size_t(kStages) * kMaxPiece, s>>>(c);
-    else
-        k_gather_vec<<<sms * 2, 32 * kVecWarps, 0, s>>>(c); // one wave (2 CTAs per SM)
+    switch (gather_kind()) {
+    case 1: k_gather<6, 5><<<sms, 32, size_t(6) * kMaxPiece, s>>>(c); break;
+    case 2: k_gather<3, 2><<<sms * 2, 32, size_t(3) * kMaxPiece, s>>>(c); break;
+    case 3: k_gather_vec<4096, 2, false><<<sms * 2, 32 * kVecWarps, 0, s>>>(c); break;
+    case 4: k_gather_vec<4096, 2, true><<<sms * 2, 32 * kVecWarps, 0, s>>>(c); break;
+    default: k_gather<6, 4><<<sms, 32, size_t(6) * kMaxPiece, s>>>(c); break;
+    }
 }
 
 } // namespace kvr

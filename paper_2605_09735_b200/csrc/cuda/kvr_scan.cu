@@ -213,11 +213,15 @@ template <int kScanThreads> __global__ void __launch_bounds__(kScanThreads, 1) k
     const double now = h->now;
     const bool age_close = (now - now) >= h->max_hold; // every stage_time == now
     const uint64_t tau = h->tau;
+    const uint64_t run_page = h->run_page, run_span = h->run_span;
+    auto adjacent = [&](uint64_t end, uint64_t next) { // transport.hpp abuts()
+        return end == next || (run_page && end % run_page == run_span && next == end - run_span + run_page);
+    };
     auto is_head = [&](uint32_t i) {
         if (i == 0 || !merge)
             return true;
         const uint32_t a = order[i - 1], b = order[i];
-        return !(needs[d_need[a]].kind == needs[d_need[b]].kind && d_off[a] + d_len[a] == d_off[b]);
+        return !(needs[d_need[a]].kind == needs[d_need[b]].kind && adjacent(d_off[a] + d_len[a], d_off[b]));
     };
     uint32_t n_runs;
     {

@@ -249,6 +249,8 @@ struct DeviceStep::Impl {
             h.tau = tc->merge_threshold;
             h.max_hold = tc->max_hold;
             h.merge = tc->merge ? 1 : 0;
+            h.run_page = tc->run_page_bytes;
+            h.run_span = tc->run_span_bytes;
         }
         uint64_t off = align16(sizeof(kvr_step_header));
         auto place = [&](uint64_t bytes) {

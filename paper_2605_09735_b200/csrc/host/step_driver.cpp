@@ -156,6 +156,8 @@ void ScenarioConfig::validate() const {
         raise(Errc::bad_config, "b200.payload must be 'bytes', 'lanes' or 'wide'");
     if (b200.query != "exact" && b200.query != "f32")
         raise(Errc::bad_config, "b200.query must be 'exact' or 'f32'");
+    if (b200.transfer != "reference" && b200.transfer != "page_runs")
+        raise(Errc::bad_config, "b200.transfer must be 'reference' or 'page_runs'");
 }
 
 std::vector<TraceEvent> resolve_events(const ScenarioConfig &cfg) {
@@ -275,6 +277,10 @@ struct ScenarioDriver::Impl {
         ekind = elem_kind_of(cfg);
         lanes_payload = cfg.b200.payload == "lanes" || cfg.b200.payload == "wide";
         lane_shift = cfg.b200.payload == "wide" ? 3 : 7;
+        if (cfg.b200.transfer == "page_runs") { // B200 transfer policy (transport.hpp abuts())
+            cfg.transport.run_page_bytes = cfg.pager.page_bytes;
+            cfg.transport.run_span_bytes = uint64_t(tpp) * cfg.pager.token_bytes();
+        }
 
         buf.resize(cfg.pager.token_bytes());
         if (cfg.pager_enabled)
@@ -1496,6 +1502,7 @@ static ScenarioConfig config_from_json(const ojson &j) {
         take(p, "q_heads", c.b200.q_heads);
         take(p, "payload", c.b200.payload);
         take(p, "query", c.b200.query);
+        take(p, "transfer", c.b200.transfer);
         take(p, "dtype", c.b200.dtype);
         take(p, "trace", c.b200.trace);
         take(p, "attention", c.b200.attention);

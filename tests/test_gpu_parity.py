@@ -157,6 +157,41 @@ def test_far_view_fp32_on_device():
     assert worst <= 1e-3
 
 
+@pytest.mark.parametrize("far", [False, True])
+def test_page_run_transfer_policy(far):
+    """b200.transfer = page_runs (a B200 policy): 1280-byte tokens leave 1 KiB of slack
+    at the end of each 16 KiB page, so the reference's exact-abutment rule splits every
+    page into its own train; page-run merge joins physically consecutive pages. The
+    device K-scan must equal the host reduce() under the same policy on every step,
+    the destination-hashed trace must equal the host twin's, and the policy must
+    need fewer trains than the reference rule on the same workload."""
+    cfg = c1()
+    del cfg["trace_path"]
+    cfg["steps"] = 160
+    cfg["pager"].update({"page_bytes": 16384, "layers": 5, "kv_head_dim": 64, "elem_bytes": 2})
+    cfg["transport"]["tau_bytes"] = 8 * 16384
+    cfg["workload"] = {"requests": 10000, "concurrency": 16, "prompt_min": 64, "prompt_max": 1024,
+                       "arrivals_per_window": 8.0, "seed": 3}
+    cfg["shaping"] = {"arena_pages": 6000, "staged_refresh_period": 4, "shared_prefix_tokens": 48}
+    kw = dict(kv_heads=1, head_dim=64, q_heads=2, payload="lanes", dtype="bf16")
+    if far:  # fp32 lanes (the reference far view): 2560-byte tokens, 6 per page + 1 KiB slack
+        cfg["pager"]["elem_bytes"] = 4
+        cfg["far_view"] = {"enabled": True, "w_star": 128, "cap": 16, "sv_chunk": 24}
+        kw["dtype"] = "fp32"
+    host = kv.Driver(dict(cfg, b200=dict(kw, transfer="page_runs", trace=True)))
+    host.run()
+    ref_rule = kv.Driver(dict(cfg, b200=dict(kw)))
+    ref_rule.run()
+    d = run(cfg, transfer="page_runs", **kw)
+    assert d.trace() == host.trace()
+    assert_scan_exact(d, 160)
+    assert_all_staged_rows_delivered(d, behind_ok=far)
+    rows = lambda drv: [r.split(",") for r in drv.steps_csv().strip().split("\n")[1:]]
+    fewer = sum(int(r[2]) for r in rows(d)) < sum(int(r[2]) for r in rows(ref_rule))
+    assert fewer
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
 @pytest.mark.parametrize("dtype,kvh,hd,qh", [("fp16", 4, 64, 4), ("bf16", 4, 64, 16),
                                              ("fp16", 2, 128, 2), ("bf16", 2, 128, 16),
                                              ("fp16", 8, 32, 8), ("bf16", 4, 64, 8)])
