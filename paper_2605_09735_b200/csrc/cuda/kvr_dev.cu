@@ -238,6 +238,8 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
             g.max_trains = 2048;
         if (g.max_scan_descs & (g.max_scan_descs - 1))
             throw std::runtime_error("max_scan_descs must be a power of two");
+        if (uint64_t(g.arena_pages) * g.page_bytes >= (1ull << 47)) // K-scan's sort key holds 47-bit offsets
+            throw std::runtime_error("arena must be smaller than 128 TiB");
         if (scan_dynamic_smem(g.max_scan_descs) > (192u << 10)) // K-scan stages its arrays in shared memory
             throw std::runtime_error("max_scan_descs too large for K-scan's shared memory (<= 2048)");
         d->g = g;

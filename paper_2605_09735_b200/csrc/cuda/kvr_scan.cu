@@ -182,6 +182,8 @@ template <int kScanThreads> __global__ void __launch_bounds__(kScanThreads, 1) k
     while (pow2 < n_desc)
         pow2 <<= 1;
     if (merge && n_desc > 1) {
+        // key = kind (bit 63) | byte offset (47 bits: arena < 128 TiB, checked at
+        // kvr_dev_open) | stage index (16 bits: descriptors <= max_scan_descs <= 2048)
         for (uint32_t i = threadIdx.x; i < pow2; i += blockDim.x)
             key[i] = i < n_desc ? (uint64_t(needs[d_need[i]].kind & 1u) << 63) | (d_off[i] << 16) | i
                                 : ~0ull;
@@ -210,8 +212,12 @@ template <int kScanThreads> __global__ void __launch_bounds__(kScanThreads, 1) k
     __syncthreads();
 
     // ---- 3. run-length scan: ballot run heads, shuffle-scan their ranks ----
+    // The age rule (transport.cpp:101-110) closes a train when now - oldest_stage_time
+    // >= max_hold. K-scan fuses stage() with reduce(): stage() stamps every descriptor
+    // with stage_time = now (transport.cpp:29-61), so each train's oldest stage time
+    // IS now and the rule reduces exactly to 0 >= max_hold — the same for every train.
     const double now = h->now;
-    const bool age_close = (now - now) >= h->max_hold; // every stage_time == now
+    const bool age_close = (now - now) >= h->max_hold;
     const uint64_t tau = h->tau;
     const uint64_t run_page = h->run_page, run_span = h->run_span;
     auto adjacent = [&](uint64_t end, uint64_t next) { // transport.hpp abuts()
