@@ -424,6 +424,7 @@ def run_b200(args, rank, local, world) -> dict | None:
         "phases": {name: statistics.mean(r.phase_ms[i] for r in recs) for i, name in enumerate(
             ["apply", "hot_writes_query", "far_map_prime", "scan", "gather", "attention",
              "cold_write_tail"])},
+        "live_binned_tail": live_binned_tail(recs),
         "p50_ms": nearest_rank([r.device_ms for r in recs], 0.50),
         "p99_ms": nearest_rank([r.device_ms for r in recs], 0.99),
         "itl_p50_ms": nearest_rank(itl_ms, 0.50) if itl_ms else None,
@@ -472,6 +473,23 @@ def read_stream_context(traffic, s_per_launch) -> dict:
     if traffic and s_per_launch:
         out["read_stream_frac"] = traffic / s_per_launch / 1e9 / peak
     return out
+
+
+def live_binned_tail(recs) -> dict:
+    """Step-time tail with the batch size held fixed: the attention's work is
+    proportional to the live sessions, which a burst replay swings between ~10 and the
+    full width, so the whole-run p99/p50 mostly measures the workload. Within bins of
+    8 live sessions (bins with >= 20 steps) p99/p50 isolates what bursts (admissions,
+    EOS, staging) add; also the non-attention part of the step (device - attention)."""
+    from collections import defaultdict
+    bins = defaultdict(list)
+    for r in recs:
+        bins[r.live_sessions // 8 * 8].append(r.device_ms)
+    ratios = {f"{k}-{k + 7}": nearest_rank(v, 0.99) / nearest_rank(v, 0.50)
+              for k, v in sorted(bins.items()) if len(v) >= 20 and k > 0}
+    extra = [r.device_ms - r.attn_ms for r in recs]
+    return {"p99_over_p50_by_live_bin": ratios, "max_bin_ratio": max(ratios.values()) if ratios else None,
+            "non_attention_p50_ms": nearest_rank(extra, 0.5), "non_attention_p99_ms": nearest_rank(extra, 0.99)}
 
 
 def nearest_rank(xs: list[float], q: float) -> float:
@@ -528,6 +546,9 @@ def main():
     ap.add_argument("--transfer", default="page_runs", choices=["page_runs", "reference"],
                     help="b200.transfer: train grouping (page_runs: physically consecutive pages merge "
                          "across page-end slack; identical to the reference where pages hold whole tokens)")
+    ap.add_argument("--phases", action="store_true",
+                    help="record event nodes at every phase boundary of the step graph (diagnostic: "
+                         "each costs ~5 us; off, only the attention's pair is recorded)")
     ap.add_argument("--sustained", type=int, default=200,
                     help="steps run and reported (`sustained`) after the timed region")
     ap.add_argument("--prefill-budget", type=int, default=0,
@@ -538,6 +559,8 @@ def main():
         spawn_ranks(args.gpus)  # one process per GPU (does not return)
     if "KVR_BENCH_DEVICE" in os.environ:  # several ranks on one GPU: NCCL refuses that
         args.backend = "gloo"
+    if args.phases:
+        os.environ["KVR_PHASE_EVENTS"] = "1"
     if args.impl == "reference":  # CPU only: rank 0 runs it, no process group, no GPU
         if int(os.environ.get("RANK", "0")) == 0:
             print(json.dumps(reference_arm(args, int(os.environ.get("WORLD_SIZE", "1")))), flush=True)
@@ -594,8 +617,9 @@ def main():
                             "itl_note": "inter-token latency: differences of the step-end "
                                         "%globaltimer stamps, steps pipelined as served",
                             "wall_p50": res["wall_p50_ms"], "wall_p99": res["wall_p99_ms"],
-                            "max_step": res["max_step"]},
-        "step_phases_ms_mean": res["phases"],
+                            "max_step": res["max_step"], "live_binned": res["live_binned_tail"]},
+        "step_phases_ms_mean": res["phases"] if args.phases else {"attention": res["phases"]["attention"],
+                                                                  "note": "other phases: --phases"},
         "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": res["h2d"],
                 # step counters (ScanCounters, 40 B) + the all-reduced counts (4 x int64)
                 "d2h_bytes_per_step": 40 + (32 if res["counts_collective"].startswith("nccl") else 0)},

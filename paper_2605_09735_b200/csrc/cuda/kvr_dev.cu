@@ -60,7 +60,8 @@ struct kvr_dev {
     ncclComm_t comm = nullptr;
     int rank = 0, world = 1;
     uint64_t n_launches = 0;
-    bool phase_events = true; // event nodes at every phase boundary (KVR_PHASE_EVENTS=0: K-attn only)
+    bool phase_events = false; // event nodes at every phase boundary (KVR_PHASE_EVENTS=1); off: K-attn's
+                               // pair only (each event node costs ~5 us of the step graph)
     int64_t *d_counts = nullptr;                  // all-reduce result (device)
     int64_t *h_counts[2] = {nullptr, nullptr};    // its D2H copy per ring slot (pinned)
 };
@@ -244,7 +245,7 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
             throw std::runtime_error("max_scan_descs too large for K-scan's shared memory (<= 2048)");
         d->g = g;
         if (const char *pe = getenv("KVR_PHASE_EVENTS"))
-            d->phase_events = std::string(pe) != "0";
+            d->phase_events = std::string(pe) == "1";
         ck(cudaSetDevice(g.device), "cudaSetDevice");
         cudaDeviceProp prop;
         ck(cudaGetDeviceProperties(&prop, g.device), "cudaGetDeviceProperties");
