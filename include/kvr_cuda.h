@@ -189,7 +189,7 @@ int kvr_dev_sync(kvr_dev *d);
 
 enum {
     KVR_BUF_ARENA = 0,   /* bytes */
-    KVR_BUF_RING = 1,    /* [slot][layer][row][2*d_kv] elements */
+    KVR_BUF_RING = 1,    /* [slot][layer][plane row][2*d_kv] elements (kvr_dev_ring_plane_rows) */
     KVR_BUF_TMAP = 2,    /* [slot][max_tokens] u32 global slot index */
     KVR_BUF_OUT = 3,     /* [slot][layer][q_head][head_dim] f32 */
     KVR_BUF_QUERY = 4,   /* [slot][layer][q_head][head_dim] f32 */
@@ -216,6 +216,9 @@ enum { KVR_FAULT_DROP_SPAN = 1, KVR_FAULT_SHIFT_ROWS = 2 };
 #define KVR_FAULT_ALL (~1ull)
 int kvr_dev_fault(kvr_dev *d, int what, uint64_t arg);
 int kvr_dev_buffer_bytes(kvr_dev *d, int buffer, uint64_t *out);
+/* rows per (slot, layer) plane of KVR_BUF_RING: ring_rows + the guard rows that mirror
+ * rows [0, guard) (the tensor-core attention's whole-tile loads never split) */
+int kvr_dev_ring_plane_rows(kvr_dev *d, uint32_t *out);
 /* time `iters` replays of the last launched step's attention kernel alone
  * (CUDA events on the launch stream); used by bench.py for the roofline */
 int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms_per_launch);

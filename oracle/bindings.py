@@ -214,6 +214,12 @@ def check_driver_window_and_attention(driver, far_images_of=None, only_slots=Non
             got = dev.ring_token(slot, t)
             assert got == want, f"window ring mismatch slot {slot} token {t}"
             window += want
+        # guard rows (tensor-core configs): rows [R, R + G) of every plane mirror [0, G)
+        plane, rows = dev.ring_plane(slot, g.layers - 1)
+        rb = dev.row_bytes()
+        guard = rows - g.ring_rows
+        if guard:
+            assert plane[g.ring_rows * rb:] == plane[:guard * rb], f"ring guard rows of slot {slot} differ"
         # far summaries the attention saw: device far rows == the arena summary slots
         far = dev.far_selection(slot)
         far_imgs = []

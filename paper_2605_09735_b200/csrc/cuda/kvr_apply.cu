@@ -173,7 +173,8 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
     uint32_t slice = uint32_t(u0 - j * slices);
     uint64_t j_cached = ~0ull, tok = 0;
     uint8_t *dst = nullptr, *ring = nullptr;
-    const uint64_t ring_layer = uint64_t(c.R) * c.row_elems * c.esz; // bytes between layers
+    uint64_t mirror = 0; // bytes to the guard copy of the ring row (0: none)
+    const uint64_t ring_layer = uint64_t(c.Rp) * c.row_elems * c.esz; // bytes between layers
     const uint32_t q_base = threadIdx.x;
     for (uint64_t u = u0; u < u1; ++u) {
         if (j != j_cached) {
@@ -185,8 +186,10 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
             dst = c.arena + uint64_t(op.block) * c.page_bytes + (op.slot + k) * c.token_bytes;
             ring = nullptr;
             // inside the live window after this step and not delivered by K-gather
-            if (op.dev_slot != KVR_NO_SLOT && ring_owned_by_writer(c, slots[op.dev_slot], tok))
+            if (op.dev_slot != KVR_NO_SLOT && ring_owned_by_writer(c, slots[op.dev_slot], tok)) {
                 ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
+                mirror = ring_mirror(c, uint32_t(tok % c.R)) * c.esz;
+            }
         }
         if (op.source == 0) {
             int4 v[kPer];
@@ -204,6 +207,8 @@ __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
                 if (ring) {
                     const uint32_t l = q / row_chunks, within = q - l * row_chunks;
                     *reinterpret_cast<int4 *>(ring + l * ring_layer + 16ull * within) = v[x];
+                    if (mirror)
+                        *reinterpret_cast<int4 *>(ring + mirror + l * ring_layer + 16ull * within) = v[x];
                 }
             }
         }
@@ -473,11 +478,14 @@ __global__ void k_prime(DevCtx c) {
                 continue;
             const uint8_t *src = c.arena + gslot_offset(c, gs);
             uint8_t *ring = c.ring + ring_row(c, op.slot, 0, uint32_t(tok % c.R)) * c.esz;
+            const uint64_t mirror = ring_mirror(c, uint32_t(tok % c.R)) * c.esz;
             for (uint64_t q = threadIdx.x; q < c.token_bytes / 16; q += blockDim.x) {
                 const uint64_t byte = 16 * q;
                 const uint64_t l = byte / row_bytes, within = byte % row_bytes;
-                *reinterpret_cast<int4 *>(ring + l * uint64_t(c.R) * row_bytes + within) =
-                    *reinterpret_cast<const int4 *>(src + byte);
+                const int4 v = *reinterpret_cast<const int4 *>(src + byte);
+                *reinterpret_cast<int4 *>(ring + l * uint64_t(c.Rp) * row_bytes + within) = v;
+                if (mirror)
+                    *reinterpret_cast<int4 *>(ring + mirror + l * uint64_t(c.Rp) * row_bytes + within) = v;
             }
         }
     }

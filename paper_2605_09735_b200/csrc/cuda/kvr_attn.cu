@@ -500,7 +500,7 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
         return nullptr;
     }
     const cuuint64_t dims[4] = {c.hd, 2ull * c.Hkv, c.R, uint64_t(c.L) * c.n_slots};
-    const cuuint64_t strides[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
+    const cuuint64_t strides[3] = {row, 2ull * c.Hkv * row, uint64_t(c.Rp) * 2 * c.Hkv * row}; // plane: Rp rows
     const cuuint32_t box[4] = {c.hd, p->G, uint32_t(kTile), 1};
     const cuuint32_t edge_box[4] = {c.hd, p->G, uint32_t(kEdge), 1};
     const cuuint32_t estr[4] = {1, 1, 1, 1};

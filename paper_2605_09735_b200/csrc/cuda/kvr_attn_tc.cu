@@ -219,11 +219,12 @@ template <typename T, int G, int S> __device__ inline void store_split(uint8_t *
             make_uint4(wd[4 * bl], wd[4 * bl + 1], wd[4 * bl + 2], wd[4 * bl + 3]);
 }
 
-/// Tiles of one work item, identical for every role. The near window [lo, w)
-/// is cut into 32-row boxes from L0 = lo rounded down to 32; full 4-box tiles
-/// come first, the remaining 1-3 newest boxes form a tail tile, and far summary
-/// rows are folded into that tail tile when they fit in front of its boxes
-/// (C5: 64 far rows + 1 box = one tile instead of two).
+/// Tiles of one work item, identical for every role. The near window [lo, w) is
+/// cut into 128-row tiles starting exactly at lo (ring row lo mod R: the plane's
+/// 128 guard rows mirror rows [0, 128), so a tile starting anywhere below R is one
+/// contiguous 128-row read — no dead rows at the window's old edge); the 1-127
+/// newest rows form a tail tile of 32-row boxes, and far summary rows are folded
+/// into that tail tile when they fit in front of its boxes.
 struct Item {
     uint32_t slot, layer, head, far_count, far_begin;
     uint32_t n_far;      // far-only tiles (far rows not folded)
@@ -252,17 +253,17 @@ __device__ inline bool item_fill(const DevCtx &c, const kvr_slot_state *slots, I
         return false;
     I.w = st.written;
     I.lo = I.w > c.W ? I.w - c.W : 0;
-    I.L0 = I.lo & ~uint64_t(kSub - 1);
-    const uint64_t E = (I.w + kSub - 1) & ~uint64_t(kSub - 1);
-    const uint32_t nbox = I.w > I.lo ? uint32_t((E - I.L0) / kSub) : 0;
-    I.tail_boxes = nbox & 3u;
+    I.L0 = I.lo; // tiles start at the window's first row (guard rows: no alignment needed)
+    const uint32_t near = uint32_t(I.w - I.lo);
+    const uint32_t n_full = near / kRows;
+    I.tail_boxes = (near % kRows + kSub - 1) / kSub;
     I.far_count = st.far_count;
     I.far_begin = st.far_begin;
     const uint32_t P = (I.far_count + kSub - 1) & ~uint32_t(kSub - 1);
     const bool fold = I.far_count > 0 && I.tail_boxes > 0 && P + kSub * I.tail_boxes <= uint32_t(kRows);
     I.fold_pos = fold ? P : 0;
     I.n_far = I.far_count > 0 && !fold ? (I.far_count + kRows - 1) / kRows : 0;
-    I.n_tiles = I.n_far + (I.tail_boxes > 0) + (nbox >> 2);
+    I.n_tiles = I.n_far + (I.tail_boxes > 0) + n_full;
     return true;
 }
 __device__ inline Tile tile_of(const Item &I, uint32_t k) {
@@ -482,8 +483,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const Tile tl = tile_of(I, k);
             mbar_wait(&empty[s], ph ^ 1);
             const uint32_t st = smem_u32(ring + s * kSideBytes);
-            // near boxes holding a live row: boxes start at or after L0 > lo - 32, so
-            // a box is live iff it starts below w
+            // near boxes holding a live row: boxes start at or after lo, so a box is
+            // live iff it starts below w
             const uint64_t first_tok = tl.tok_r0 + uint64_t(kSub) * tl.box_first;
             const uint32_t n_live =
                 first_tok < I.w ? min(tl.n_boxes, uint32_t((I.w - first_tok + kSub - 1) / kSub)) : 0u;
@@ -505,22 +506,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 r[0], r[1], r[2], r[3], &full[s]);
                 }
             }
-            uint32_t row0 = 0; // ring row of the first box (offsets within an item stay below R)
+            uint32_t row0 = 0; // ring row of the first box (< R); its tile may run into the guard rows
             if (tl.n_boxes) {
                 row0 = row_base + uint32_t(first_tok - I.L0);
                 if (row0 >= c.R)
                     row0 -= c.R;
             }
-            if (kUseTile5d && live_boxes == 0xfu && row0 + kRows <= c.R) {
-                // this half of the whole tile in one op: 5-D view (64 dims, flat ring rows, half, head, K|V)
+            if (kUseTile5d && live_boxes == 0xfu) {
+                // this half of the whole tile in one op: 5-D view (64 dims, flat plane rows, half, head, K|V)
                 if (lane == 0)
-                    tma_load_5d(st, &maps.tile, 0, int(plane * c.R + row0), 0, int(I.head), int(kv), &full[s]);
-            } else if (lane < 8) { // lane = box * 2 + half, 32-row boxes never straddle the ring end
+                    tma_load_5d(st, &maps.tile, 0, int(plane * c.Rp + row0), 0, int(I.head), int(kv), &full[s]);
+            } else if (lane < 8) { // lane = box * 2 + half; boxes end within the guard rows
                 const uint32_t bx = lane >> 1, hf = lane & 1u;
                 if (live_boxes >> bx & 1u) {
-                    uint32_t row = row0 + (bx - tl.box_first) * kSub;
-                    if (row >= c.R)
-                        row -= c.R;
+                    const uint32_t row = row0 + (bx - tl.box_first) * kSub;
                     tma_load_4d(st + hf * kHalfBytes + bx * kSub * 128, &maps.ring, int(hf * 64), kvh0 + int(I.head),
                                 int(row), plane, &full[s]);
                 }
@@ -846,9 +845,9 @@ EncodeFn encoder() {
 /// groups of 2, 4 or 8 with at most 128 far rows per slot.
 bool attn_tc_supported(const DevCtx &c) {
     return c.hd == kHd && c.esz == 2 && (c.group == 1 || c.group == 2 || c.group == 4 || c.group == 8) &&
-           c.far_cap <= kRows &&
-           c.R % kSub == 0;
+           c.far_cap <= kRows && c.R % kSub == 0;
 }
+bool attn_tc_ready(const DevCtx &c) { return attn_tc_supported(c) && c.G >= kRows; } // ring guard rows present
 
 size_t attn_tc_smem() {
     return 1024 + (kKStages + kVStages) * kSideBytes + 2 * kWgBytes + (2 * 2 * 4 * 8 + 2 * 4 * 8) * 4 +
@@ -857,7 +856,7 @@ size_t attn_tc_smem() {
 }
 
 const void *attn_tc_kernel(const DevCtx &c) {
-    if (!attn_tc_supported(c))
+    if (!attn_tc_ready(c))
         return nullptr;
     TcFn fn = c.elem_kind == KVR_ELEM_BF16 ? pick_tc<__nv_bfloat16>(c.group) : pick_tc<__half>(c.group);
     if (fn)
@@ -880,13 +879,13 @@ bool attn_tc_maps(const DevCtx &c, TcMaps *maps) {
                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
     };
-    // 32-row boxes: (head_dim, 2*Hkv heads, R rows, L*n_slots)
-    const cuuint64_t d4[4] = {c.hd, 2ull * c.Hkv, c.R, uint64_t(c.L) * c.n_slots};
-    const cuuint64_t s4[3] = {row, 2ull * c.Hkv * row, uint64_t(c.R) * 2 * c.Hkv * row};
+    // 32-row boxes: (head_dim, 2*Hkv heads, Rp plane rows incl. the guard, L*n_slots)
+    const cuuint64_t d4[4] = {c.hd, 2ull * c.Hkv, c.Rp, uint64_t(c.L) * c.n_slots};
+    const cuuint64_t s4[3] = {row, 2ull * c.Hkv * row, uint64_t(c.Rp) * 2 * c.Hkv * row};
     const cuuint32_t b4[4] = {64, 1, uint32_t(kSub), 1};
-    // whole tiles: (64 dims, flat rows = plane * R + row, half, head, K|V); the box
+    // whole tiles: (64 dims, flat rows = plane * Rp + row, half, head, K|V); the box
     // (box kv = 1) lands as [half][128 rows][64 dims], one K or V half of a stage
-    const cuuint64_t d5[5] = {64, uint64_t(c.L) * c.n_slots * c.R, 2, c.Hkv, 2};
+    const cuuint64_t d5[5] = {64, uint64_t(c.L) * c.n_slots * c.Rp, 2, c.Hkv, 2};
     const cuuint64_t s5[4] = {2ull * c.Hkv * row, 128, row, uint64_t(c.Hkv) * row};
     const cuuint32_t b5[5] = {64, uint32_t(kRows), 2, 1, 1};
     // far rows: (row_elems, n_slots*L*max_chunks rows), 64 x 1 boxes for gather4

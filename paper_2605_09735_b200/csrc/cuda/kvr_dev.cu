@@ -303,7 +303,10 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         const uint64_t arena_bytes = uint64_t(g.arena_pages) * g.page_bytes;
         c.arena = static_cast<uint8_t *>(dalloc(d.get(), arena_bytes, "arena"));
         ck(cudaMemsetAsync(c.arena, 0, arena_bytes, d->stream), "arena zero");
-        const uint64_t ring_elems = uint64_t(c.n_slots) * c.L * c.R * c.row_elems;
+        // guard rows for the tensor-core attention's whole-tile loads (kvr_attn_tc.cu)
+        c.G = (g.attention == 3 || (g.attention == 1 && c.group >= 4)) && attn_tc_supported(c) ? 128 : 0;
+        c.Rp = c.R + c.G;
+        const uint64_t ring_elems = uint64_t(c.n_slots) * c.L * c.Rp * c.row_elems;
         c.ring = static_cast<uint8_t *>(dalloc(d.get(), ring_elems * c.esz, "ring"));
         ck(cudaMemsetAsync(c.ring, 0, ring_elems * c.esz, d->stream), "ring zero");
         const uint64_t tmap_n = uint64_t(c.n_slots) * c.max_tokens;
@@ -560,7 +563,7 @@ int kvr_dev_buffer_bytes(kvr_dev *d, int buffer, uint64_t *out) {
         const DevCtx &c = d->base;
         switch (buffer) {
         case KVR_BUF_ARENA: *out = uint64_t(c.arena_pages) * c.page_bytes; break;
-        case KVR_BUF_RING: *out = uint64_t(c.n_slots) * c.L * c.R * c.row_elems * c.esz; break;
+        case KVR_BUF_RING: *out = uint64_t(c.n_slots) * c.L * c.Rp * c.row_elems * c.esz; break;
         case KVR_BUF_TMAP: *out = uint64_t(c.n_slots) * c.max_tokens * 4; break;
         case KVR_BUF_OUT:
         case KVR_BUF_QUERY: *out = uint64_t(c.n_slots) * c.L * c.Hq * c.hd * 4; break;
@@ -683,6 +686,10 @@ int kvr_dev_utility(kvr_dev *d, uint32_t k, kvr_mass_run *out, uint32_t *counts)
             std::memcpy(out + uint64_t(s) * c.W, d->h_mass[k] + uint64_t(s) * c.W,
                         std::min<uint32_t>(counts[s], c.W) * sizeof(kvr_mass_run));
     });
+}
+
+int kvr_dev_ring_plane_rows(kvr_dev *d, uint32_t *out) {
+    return guard([&] { *out = d->base.Rp; });
 }
 
 int kvr_comm_unique_id(uint8_t id[128]) {

@@ -98,9 +98,17 @@ __device__ inline Move span_row(const DevCtx &c, const kvr_slot_state *slots, co
 /// Test hook: the same position `shift` ring rows further (wrapping in the slot's layer ring).
 __device__ inline uint8_t *shifted_row(const DevCtx &c, uint8_t *dst, uint64_t shift) {
     const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
-    const uint64_t off = uint64_t(dst - c.ring), ring_bytes = uint64_t(c.R) * row_bytes;
-    const uint64_t base = off / ring_bytes * ring_bytes, within = off - base;
-    return c.ring + base + (within + (shift % c.R) * row_bytes) % ring_bytes;
+    const uint64_t off = uint64_t(dst - c.ring), plane = uint64_t(c.Rp) * row_bytes;
+    const uint64_t base = off / plane * plane, within = off - base;
+    return c.ring + base + (within + (shift % c.R) * row_bytes) % (uint64_t(c.R) * row_bytes);
+}
+
+/// Bytes from a ring destination to its guard mirror (0: none; far rows have none).
+__device__ inline uint64_t dst_mirror(const DevCtx &c, const uint8_t *dst) {
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz, plane = uint64_t(c.Rp) * row_bytes;
+    if (!c.G || dst < c.ring || dst >= c.ring + uint64_t(c.n_slots) * c.L * plane)
+        return 0;
+    return (uint64_t(dst - c.ring) % plane) / row_bytes < c.G ? uint64_t(c.R) * row_bytes : 0;
 }
 
 /// Walks this CTA's contiguous range of units with a forward-moving span cursor (no
@@ -143,6 +151,7 @@ struct Walker {
 struct Unit {
     uint8_t *dst0;        // destination of the first layer
     uint64_t dst_stride;  // bytes between the layers' destinations
+    uint64_t mirror;      // bytes to the ring rows' guard copies (0: none)
     uint32_t row, nl;
 };
 
@@ -199,8 +208,9 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c) {
                 u.dst0 = m.dst + off0;
                 if (shift && sp.kind == 0)
                     u.dst0 = shifted_row(c, u.dst0, shift);
-                // the next layer's row: one ring plane (R rows) / far plane further
-                u.dst_stride = (sp.kind == 0 ? uint64_t(c.R) : uint64_t(c.max_chunks)) * row_bytes;
+                // the next layer's row: one ring plane (Rp rows) / far plane further
+                u.dst_stride = (sp.kind == 0 ? uint64_t(c.Rp) : uint64_t(c.max_chunks)) * row_bytes;
+                u.mirror = sp.kind == 0 ? dst_mirror(c, u.dst0) : 0;
                 m.src += off0;
             }
             ++next;
@@ -223,8 +233,12 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c) {
         mbar_wait(&full[s], (phase_bits >> s) & 1u);
         phase_bits ^= 1u << s;
         const Unit &u = mv[s];
-        for (uint32_t j = 0; j < u.nl; ++j)
-            bulk_s2g_nocommit(u.dst0 + j * u.dst_stride, stage + size_t(s) * kMaxPiece + size_t(j) * u.row, u.row);
+        for (uint32_t j = 0; j < u.nl; ++j) {
+            const uint8_t *from = stage + size_t(s) * kMaxPiece + size_t(j) * u.row;
+            bulk_s2g_nocommit(u.dst0 + j * u.dst_stride, from, u.row);
+            if (u.mirror)
+                bulk_s2g_nocommit(u.dst0 + u.mirror + j * u.dst_stride, from, u.row);
+        }
         bulk_commit();
         ++stored;
         // next load reuses the stage stored (kStages - kAhead) groups ago
@@ -245,7 +259,8 @@ constexpr int kVecWarps = 8; // warps per CTA
 struct VecUnit {
     const int4 *src;
     int4 *dst;
-    uint32_t n16; // int4s in the unit
+    uint32_t n16;    // int4s in the unit
+    uint32_t mirror; // int4s to the ring row's guard copy (0: none)
 };
 
 template <int kUnit, int kFly, bool kInterleave>
@@ -291,6 +306,7 @@ __global__ void __launch_bounds__(32 * kVecWarps) k_gather_vec(DevCtx c) {
         vu.src = reinterpret_cast<const int4 *>(m.src + off0);
         vu.dst = m.dst ? reinterpret_cast<int4 *>(m.dst + off0) : nullptr;
         vu.n16 = uint32_t(n / 16);
+        vu.mirror = m.dst && sp.kind == 0 ? uint32_t(dst_mirror(c, m.dst) / 16) : 0;
     };
     constexpr int kPer = kUnit / 16 / 32; // int4 per lane per unit
     for (uint64_t u = u0; u < u1; u += ustep * kFly) {
@@ -317,8 +333,11 @@ __global__ void __launch_bounds__(32 * kVecWarps) k_gather_vec(DevCtx c) {
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
                 const uint32_t q = lane + 32u * i;
-                if (a[f].dst && q < a[f].n16)
+                if (a[f].dst && q < a[f].n16) {
                     a[f].dst[q] = v[f][i];
+                    if (a[f].mirror)
+                        a[f].dst[q + a[f].mirror] = v[f][i];
+                }
             }
     }
 }

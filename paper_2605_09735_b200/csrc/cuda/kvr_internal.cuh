@@ -36,6 +36,7 @@ struct DevCtx {
     uint64_t page_bytes, token_bytes, max_tokens, seed;
     uint32_t tpp, arena_pages, L, Hkv, hd, Hq, group, d_kv, row_elems, esz;
     uint32_t elem_kind, payload_mode, n_slots, W, R, far_cap, chunk_tokens, max_chunks, smap_cap;
+    uint32_t G, Rp; // ring guard rows (rows [0, G) mirrored at [R, R + G)) and plane rows R + G
     uint32_t max_scan, max_trains;
     float lane_scale, lane_bias; // 2-byte lanes: (2^23 + b) * scale - bias = (b - 128) * scale
     uint32_t query_mode;         // KVR_QUERY_*
@@ -92,9 +93,15 @@ __device__ inline uint64_t gslot_offset(const DevCtx &c, uint32_t gs) {
     return uint64_t(gs / c.tpp) * c.page_bytes + uint64_t(gs % c.tpp) * c.token_bytes;
 }
 
-/// Ring element offset of (slot, layer, row).
+/// Ring element offset of (slot, layer, row). A plane holds R rows plus G guard
+/// rows that mirror rows [0, G): a tile of up to G rows starting at any row < R
+/// reads consecutive memory (no split at the ring end).
 __device__ inline uint64_t ring_row(const DevCtx &c, uint32_t slot, uint32_t l, uint32_t row) {
-    return ((uint64_t(slot) * c.L + l) * c.R + row) * c.row_elems;
+    return ((uint64_t(slot) * c.L + l) * c.Rp + row) * c.row_elems;
+}
+/// Element offset from a row to its guard mirror (0: the row has none).
+__device__ inline uint64_t ring_mirror(const DevCtx &c, uint32_t row) {
+    return row < c.G ? uint64_t(c.R) * c.row_elems : 0;
 }
 
 // ---- host launchers (one per kernel file) --------------------------------
@@ -122,6 +129,7 @@ struct AttnPlan;
 AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode);
 // tensor-core variant (kvr_attn_tc.cu)
 bool attn_tc_supported(const DevCtx &c);
+bool attn_tc_ready(const DevCtx &c); // supported and the ring has its guard rows (c.G)
 const void *attn_tc_kernel(const DevCtx &c);
 /// TMA descriptors of the tensor-core kernel: ring in 32-row boxes, ring in whole
 /// 128-row K|V tiles (one op per tile), far rows for gather4.

@@ -59,6 +59,7 @@ struct DeviceStep::Impl {
     std::vector<uint32_t> far_ids;
     std::vector<kvr_slot_state> slots;
     std::vector<uint64_t> staged_count; // per slot: near staged tokens this step
+    uint32_t ring_plane_rows = 0;       // kvr_dev_ring_plane_rows
     std::vector<std::vector<uint64_t>> far_shown; // per slot, as of the last launch
     // K-presum: chunks summarised while their prompt rows were written (far view)
     std::vector<kvr_presum_op> presum_ops;
@@ -614,6 +615,7 @@ DeviceStep::DeviceStep(const kvr_geometry &geometry) : impl_(std::make_unique<Im
     if (!m.g.max_trains)
         m.g.max_trains = 2048;
     m.clean.assign(m.g.arena_pages, 1); // the arena starts zeroed
+    ck(kvr_dev_ring_plane_rows(m.dev, &m.ring_plane_rows));
     m.slots.assign(m.g.n_slots, kvr_slot_state{});
     m.staged_count.assign(m.g.n_slots, 0);
     m.store_ = std::make_shared<DeviceStore>(impl_.get());
@@ -855,7 +857,7 @@ void DeviceStep::read_ring_token(uint32_t slot, uint64_t token, void *out) {
     const kvr_geometry &g = impl_->g;
     const uint64_t row = 2ull * g.kv_heads * g.head_dim * g.elem_bytes;
     for (uint32_t l = 0; l < g.layers; ++l) {
-        const uint64_t off = ((uint64_t(slot) * g.layers + l) * g.ring_rows + token % g.ring_rows) * row;
+        const uint64_t off = ((uint64_t(slot) * g.layers + l) * impl_->ring_plane_rows + token % g.ring_rows) * row;
         ck(kvr_dev_read(impl_->dev, KVR_BUF_RING, off, row, static_cast<uint8_t *>(out) + l * row));
     }
 }

@@ -308,6 +308,7 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_dev_time_gather": [vp, C.c_uint32, C.POINTER(C.c_double)],
         "kvr_dev_read": [vp, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p],
         "kvr_dev_read_staged": [vp, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p],
+        "kvr_dev_ring_plane_rows": [vp, U32P],
         "kvr_dev_fault": [vp, C.c_int, C.c_uint64],
     }
     for name, args in sig.items():
@@ -565,6 +566,17 @@ class Device:
     def row_bytes(self) -> int:
         g = self.geometry
         return 2 * g.kv_heads * g.head_dim * g.elem_bytes
+
+    def ring_plane(self, slot: int, layer: int) -> tuple[bytes, int]:
+        """Raw rows of one (slot, layer) ring plane (ring_rows + guard rows) and the
+        plane's row count."""
+        g = self.geometry
+        rows = C.c_uint32()
+        check(native_lib().kvr_dev_ring_plane_rows(self.raw(), C.byref(rows)))
+        n = rows.value * self.row_bytes()
+        buf = C.create_string_buffer(n)
+        check(native_lib().kvr_dev_read(self.raw(), 1, (slot * g.layers + layer) * n, n, buf))
+        return buf.raw, rows.value
 
     def ring_token(self, slot: int, token: int) -> bytes:
         buf = C.create_string_buffer(self.geometry.token_bytes)
