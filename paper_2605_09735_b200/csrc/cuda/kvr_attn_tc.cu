@@ -325,37 +325,89 @@ __device__ inline bool elect_one() {
     return pred != 0;
 }
 
-/// The j-th active item (live, >= 1 tile) of a CTA belongs to warpgroup j % 2.
-/// (slot, layer, head) of item `it` advance incrementally by gridDim.x: no
-/// divisions on the item stream.
-struct Cursor {
-    uint32_t it, j, slot, layer, head, ds, dl, dh;
-    __device__ void init(const DevCtx &c) {
-        it = blockIdx.x, j = 0;
-        head = it % c.Hkv, layer = (it / c.Hkv) % c.L, slot = it / (c.Hkv * c.L);
-        dh = gridDim.x % c.Hkv, dl = (gridDim.x / c.Hkv) % c.L, ds = gridDim.x / (c.Hkv * c.L);
-    }
-    __device__ void step(const DevCtx &c) {
-        it += gridDim.x;
-        head += dh;
-        layer += dl;
-        if (head >= c.Hkv)
-            head -= c.Hkv, ++layer;
-        slot += ds;
-        if (layer >= c.L)
-            layer -= c.L, ++slot;
-    }
-    __device__ bool next(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items, uint32_t w, Item &I) {
-        for (; it < n_items; step(c)) {
-            I.slot = slot, I.layer = layer, I.head = head;
-            if (!item_fill(c, slots, I) || I.n_tiles == 0)
-                continue;
-            if ((j++ & 1u) == w) {
-                step(c);
-                return true;
-            }
+/// Dynamic item schedule. CTAs claim active items (live, >= 1 tile) from a global
+/// counter (c.attn_sched[0]) instead of a static round robin: measured with the
+/// static split, C3's SMs were busy between 2.14 M and 2.59 M cycles (mean 2.33 M)
+/// of one launch — the slowest CTA set the kernel time. Warp 0's lane 0 claims items
+/// a few ahead of its own tile stream and publishes them in a shared-memory queue;
+/// every role reads the CTA's j-th item from it (item j -> softmax warpgroup j % 2).
+constexpr uint32_t kQ = 64;     // queue entries (roles lag the claimer by < ~10 items)
+constexpr uint32_t kAheadQ = 4; // items claimed ahead of the claimer's own position
+struct ItemQueue {
+    uint32_t item[kQ];
+    uint32_t tail; // items published
+    uint32_t end;  // index of the end of the CTA's stream (~0: not reached)
+};
+__device__ inline uint32_t ld_vol(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.volatile.shared.u32 %0, [%1];" : "=r"(v) : "r"(smem_u32(p)) : "memory");
+    return v;
+}
+__device__ inline void st_vol(uint32_t *p, uint32_t v) {
+    asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+/// Claimer (one thread): publish items until `want` are available or the stream ends.
+__device__ inline void claim_to(ItemQueue *q, uint32_t want, const DevCtx &c, const kvr_slot_state *slots,
+                                uint32_t n_items) {
+    uint32_t tail = q->tail;
+    while (tail < want && q->end == ~0u) {
+        uint32_t it;
+        for (;;) {
+            it = atomicAdd(c.attn_sched, 1u);
+            if (it >= n_items)
+                break;
+            Item I;
+            if (item_of(c, slots, it, I) && I.n_tiles)
+                break;
         }
-        return false;
+        if (it >= n_items) {
+            __threadfence_block();
+            st_vol(&q->end, tail);
+            break;
+        }
+        q->item[tail % kQ] = it;
+        __threadfence_block();
+        st_vol(&q->tail, ++tail);
+    }
+}
+/// The j-th item of the CTA's stream: 1 (in `it`), 0 at the stream's end, -1 not
+/// published yet (only when `wait` is false).
+__device__ inline int queue_get(ItemQueue *q, uint32_t j, uint32_t &it, bool wait = true) {
+    for (;;) {
+        if (j < ld_vol(&q->tail)) {
+            __threadfence_block();
+            it = ld_vol(&q->item[j % kQ]);
+            return 1;
+        }
+        const uint32_t e = ld_vol(&q->end);
+        if (e != ~0u && j >= e)
+            return 0;
+        if (!wait)
+            return -1;
+    }
+}
+
+/// Items j = w, w + 2, ... of the CTA's stream (warpgroup w's items). The claimer
+/// (warp 0) tops the queue up to kAheadQ items past every item it reads.
+struct Cursor {
+    uint32_t j;
+    ItemQueue *q;
+    bool claimer;
+    __device__ void init(ItemQueue *queue, uint32_t w, bool is_claimer) {
+        q = queue, j = w, claimer = is_claimer;
+    }
+    __device__ bool next(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items, uint32_t, Item &I) {
+        if (claimer) {
+            if ((threadIdx.x & 31) == 0)
+                claim_to(q, j + kAheadQ, c, slots, n_items);
+            __syncwarp();
+        }
+        uint32_t it;
+        if (queue_get(q, j, it) <= 0)
+            return false;
+        j += 2;
+        item_of(c, slots, it, I);
+        return true;
     }
 };
 
@@ -363,35 +415,37 @@ struct Cursor {
 /// two warpgroups; an item's tiles are consecutive and the warpgroups overlap at
 /// item boundaries (alternating tiles between the warpgroups measured slower:
 /// C3 1.485 vs 1.431-1.441 ms, C5 0.521 vs 0.500).
-struct Stream { // (no arrays indexed by w: everything stays in registers)
-    Cursor c0, c1;
-    Item I0, I1;
-    bool h0, h1;
-    uint32_t k0, k1, turn;
-    __device__ void init(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items) {
-        c0.init(c);
-        c1.init(c);
-        h0 = c0.next(c, slots, n_items, 0, I0);
-        h1 = c1.next(c, slots, n_items, 1, I1);
-        k0 = k1 = turn = 0;
+struct Stream { // items j = 0, 1, 2, ... in order (item j -> warpgroup j % 2), all tiles of each
+    ItemQueue *q;
+    bool claimer, have;
+    uint32_t j, k;
+    Item cur;
+    __device__ void init(const DevCtx &, const kvr_slot_state *, uint32_t, ItemQueue *queue, bool is_claimer = false) {
+        q = queue, claimer = is_claimer, have = false, j = k = 0;
     }
-    /// Warpgroup, tile index and item of the next tile; false at the end.
-    __device__ bool next(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items, uint32_t &w, uint32_t &kk,
-                         Item &I) {
-        if (!h0 && !h1)
-            return false;
-        w = (turn ? h1 : !h0) ? 1u : 0u;
-        turn = w;
-        if (w) {
-            kk = k1, I = I1;
-            if (++k1 == I1.n_tiles)
-                h1 = c1.next(c, slots, n_items, 1, I1), k1 = 0, turn = 0;
-        } else {
-            kk = k0, I = I0;
-            if (++k0 == I0.n_tiles)
-                h0 = c0.next(c, slots, n_items, 0, I0), k0 = 0, turn = 1;
+    /// Warpgroup, tile index and item of the next tile: 1; 0 at the end; -1 when the
+    /// next item is not published yet and `wait` is false (the PV issuer must never
+    /// block on the queue: its look-ahead can outrun the claimer).
+    __device__ int next(const DevCtx &c, const kvr_slot_state *slots, uint32_t n_items, uint32_t &w, uint32_t &kk,
+                        Item &I, bool wait = true) {
+        if (!have) {
+            if (claimer) {
+                if ((threadIdx.x & 31) == 0)
+                    claim_to(q, j + kAheadQ + 1, c, slots, n_items);
+                __syncwarp();
+            }
+            uint32_t it;
+            const int r = queue_get(q, j, it, wait);
+            if (r <= 0)
+                return r;
+            item_of(c, slots, it, cur);
+            have = true;
+            k = 0;
         }
-        return true;
+        w = j & 1u, kk = k, I = cur;
+        if (++k == cur.n_tiles)
+            have = false, ++j;
+        return 1;
     }
 };
 
@@ -418,6 +472,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint64_t *kempty = kfull + kKStages, *vfull = kempty + kKStages, *vempty = vfull + kVStages;
     WgBars *wb = reinterpret_cast<WgBars *>(vempty + kVStages);
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(wb + 2);
+    ItemQueue *queue = reinterpret_cast<ItemQueue *>(tmem_slot + 4);
 
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
@@ -449,6 +504,9 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        queue->tail = 0;
+        queue->end = ~0u;
+        claim_to(queue, kAheadQ, c, slots, n_items); // the first items, before any role reads
     }
     fence_async_smem();
     if (warp == 1) {
@@ -473,7 +531,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int kvh0 = int(kv * c.Hkv); // first head index of this half in the ring row
         Stream S;
-        S.init(c, slots, n_items);
+        S.init(c, slots, n_items, queue, warp == 0);
         uint32_t s = 0, ph = 0, w, k, row_base = 0;
         Item I;
         while (S.next(c, slots, n_items, w, k, I)) {
@@ -537,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t fmt = std::is_same_v<T, __nv_bfloat16> ? 1u : 0u;
         constexpr uint32_t id_s = idesc(fmt, 0, 1, kRows, SP::NQ); // S^T = K . Q^T (Q MN-major)
         Stream S;
-        S.init(c, slots, n_items);
+        S.init(c, slots, n_items, queue, warp == 0);
         uint32_t s = 0, ph = 0, w = 0, k = 0;
         uint32_t nw0 = 0, nw1 = 0, mw0 = 0, mw1 = 0;
         const uint32_t kbase = smem_u32(kbuf), wg0 = smem_u32(wgbuf);
@@ -580,7 +638,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t id_o = idesc(fmt, 1, 1, kHd, kN); // O^T = V^T . P (both MN-major)
         constexpr uint32_t kFifo = 8; // queued tiles per warpgroup (byte entries of a u64)
         Stream S;
-        S.init(c, slots, n_items);
+        S.init(c, slots, n_items, queue, warp == 0);
         uint32_t w = 0, k = 0, sv = 0, phv = 0;
         uint32_t fw0 = 0, fw1 = 0, pv0 = 0, pv1 = 0; // tiles queued / PVs issued per warpgroup
         uint64_t ring0 = 0, ring1 = 0; // byte (n % 8) = V stage | V phase << 2 | K steps << 3
@@ -591,8 +649,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t vpar = 0;
         const uint32_t vbase = smem_u32(vbuf), wg0 = smem_u32(wgbuf);
         Item I;
-        bool have = S.next(c, slots, n_items, w, k, I);
-        while (have || pv0 < fw0 || pv1 < fw1) {
+        bool have = false, ended = false; // a fetched tile not yet queued / the stream's end seen
+        while (!ended || have || pv0 < fw0 || pv1 < fw1) {
+            if (!have && !ended) {
+                const int r = S.next(c, slots, n_items, w, k, I, false);
+                have = r > 0, ended = r == 0;
+            }
             // queue stream tiles while the next one's warpgroup has room
             while (have && (w ? fw1 - pv1 : fw0 - pv0) < kFifo) {
                 const uint32_t nk = tile_of(I, k).nk;
@@ -606,7 +668,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     sv = 0;
                     phv ^= 1;
                 }
-                have = S.next(c, slots, n_items, w, k, I);
+                const int r = S.next(c, slots, n_items, w, k, I, false);
+                have = r > 0, ended = ended || r == 0;
             }
             uint32_t go = 0;
 #pragma unroll
@@ -667,7 +730,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         uint32_t n = 0, m_items = 0;
         Cursor cur;
-        cur.init(c);
+        cur.init(queue, w, false);
         Item I, In;
         // the next item and its Q are fetched one item ahead (their global loads
         // overlap this item's tiles instead of stalling the item start;
@@ -817,6 +880,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 256;" ::"r"(tmem));
     }
+    // the last CTA to finish resets the item counter for the next launch (every CTA
+    // has claimed past the end by now)
+    if (threadIdx.x == 0 && atomicAdd(c.attn_sched + 1, 1u) == gridDim.x - 1) {
+        c.attn_sched[0] = 0;
+        c.attn_sched[1] = 0;
+        __threadfence();
+    }
 }
 
 using TcFn = void (*)(DevCtx, const TcMaps);
@@ -852,7 +922,7 @@ bool attn_tc_ready(const DevCtx &c) { return attn_tc_supported(c) && c.G >= kRow
 size_t attn_tc_smem() {
     return 1024 + (kKStages + kVStages) * kSideBytes + 2 * kWgBytes + (2 * 2 * 4 * 8 + 2 * 4 * 8) * 4 +
            2 * (kKStages + kVStages) * 8 +
-           2 * sizeof(WgBars) + 16;
+           2 * sizeof(WgBars) + 16 + sizeof(ItemQueue);
 }
 
 const void *attn_tc_kernel(const DevCtx &c) {

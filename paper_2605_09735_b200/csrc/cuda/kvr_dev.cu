@@ -331,6 +331,8 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         c.gspans = static_cast<GSpan *>(dalloc(d.get(), sizeof(GSpan) * c.max_scan, "gspans"));
         c.scan = static_cast<ScanCounters *>(dalloc(d.get(), sizeof(ScanCounters), "scan"));
         ck(cudaMemsetAsync(c.scan, 0, sizeof(ScanCounters), d->stream), "scan zero");
+        c.attn_sched = static_cast<uint32_t *>(dalloc(d.get(), 2 * sizeof(uint32_t), "attention schedule"));
+        ck(cudaMemsetAsync(c.attn_sched, 0, 2 * sizeof(uint32_t), d->stream), "schedule zero");
         {
             const uint64_t off[2] = {~0ull, 0};
             auto *fault = static_cast<uint64_t *>(dalloc(d.get(), sizeof(off), "fault hooks"));

@@ -60,6 +60,7 @@ struct DevCtx {
     kvr_mass_run *mass_runs; // [slot][W]
     uint32_t *mass_count;    // [slot]
     const uint64_t *fault;   // [0] KVR_FAULT_DROP_SPAN, [1] KVR_FAULT_SHIFT_ROWS arguments — test hooks only
+    uint32_t *attn_sched;    // [0] next item to claim, [1] CTAs finished (tensor-core attention)
 };
 
 /// Token `tok` of a slot is written into the ring by K-write / K-prime only when it
