@@ -386,6 +386,7 @@ def run_b200(args, rank, local, world) -> dict | None:
                         "wall_ms": lat_ms[i] if i < len(lat_ms) else None,
                         "itl_ms": itl_ms[i - 1] if i > 0 else None,
                         "writeback_tokens": r.writeback_tokens, "h2d": r.h2d_bytes,
+                        "attn_bytes": r.attn_bytes, "attn_ms": r.attn_ms,
                         "phases": list(r.phase_ms)[:7]} for i, r in enumerate(recs)], f)
     dev_s = sum(r.device_ms for r in recs) / 1e3
     wall_s = t1 - t0
@@ -476,19 +477,31 @@ def read_stream_context(traffic, s_per_launch) -> dict:
 
 
 def live_binned_tail(recs) -> dict:
-    """Step-time tail with the batch size held fixed: the attention's work is
-    proportional to the live sessions, which a burst replay swings between ~10 and the
-    full width, so the whole-run p99/p50 mostly measures the workload. Within bins of
-    8 live sessions (bins with >= 20 steps) p99/p50 isolates what bursts (admissions,
-    EOS, staging) add; also the non-attention part of the step (device - attention)."""
+    """Step-time tail with the work held fixed. The attention's work is the KV bytes of
+    the live windows, which a burst replay swings by 5x, so the whole-run p99/p50 mostly
+    measures the workload. (1) Work model: least-squares device_ms = a + b * attn_bytes
+    over the timed steps; p99/p50 of device_ms / model is what bursts (admissions, EOS,
+    staging, far summaries) add on top of the work. (2) p99/p50 within steps of one live
+    count (counts with >= 20 steps). (3) The non-attention part of the step."""
     from collections import defaultdict
+    xs = [float(r.attn_bytes) for r in recs]
+    ys = [r.device_ms for r in recs]
+    n = len(xs)
+    mx, my = sum(xs) / n, sum(ys) / n
+    vx = sum((x - mx) ** 2 for x in xs)
+    b = sum((x - mx) * (y - my) for x, y in zip(xs, ys)) / vx if vx else 0.0
+    a = my - b * mx
+    rel = [y / (a + b * x) for x, y in zip(xs, ys) if a + b * x > 0]
     bins = defaultdict(list)
     for r in recs:
-        bins[r.live_sessions // 8 * 8].append(r.device_ms)
-    ratios = {f"{k}-{k + 7}": nearest_rank(v, 0.99) / nearest_rank(v, 0.50)
-              for k, v in sorted(bins.items()) if len(v) >= 20 and k > 0}
+        bins[r.live_sessions].append(r.device_ms)
+    ratios = {k: nearest_rank(v, 0.99) / nearest_rank(v, 0.50) for k, v in sorted(bins.items())
+              if len(v) >= 20 and k > 0}
     extra = [r.device_ms - r.attn_ms for r in recs]
-    return {"p99_over_p50_by_live_bin": ratios, "max_bin_ratio": max(ratios.values()) if ratios else None,
+    return {"work_model_ms": {"fixed": a, "per_gib_kv": b * 2**30},
+            "p99_over_p50_vs_work_model": nearest_rank(rel, 0.99) / nearest_rank(rel, 0.50) if rel else None,
+            "p99_over_p50_same_live_count_max": max(ratios.values()) if ratios else None,
+            "live_counts_binned": len(ratios),
             "non_attention_p50_ms": nearest_rank(extra, 0.5), "non_attention_p99_ms": nearest_rank(extra, 0.99)}
 
 
