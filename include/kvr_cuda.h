@@ -94,6 +94,10 @@ typedef struct kvr_step_header {
                                    the in-graph NCCL all-reduce when a communicator is set */
     uint64_t run_page, run_span; /* TransportConfig::run_page_bytes / run_span_bytes (page-run
                                     merge, a B200 policy; 0 = exact abutment only) */
+    uint64_t off_src_rows;       /* u32 global slots (block * tpp + slot) read by K-far jobs and
+                                    K-prime ops, resolved by the host: those kernels do not read
+                                    the page table, so they run in one kernel with K-map */
+    uint32_t n_src_rows, pad_r;
 } kvr_step_header;
 
 typedef struct kvr_zero_op { uint32_t block, slot_begin, slot_count, pad; } kvr_zero_op;
@@ -106,13 +110,15 @@ typedef struct kvr_edit_op {
 } kvr_edit_op;
 /* payload generated in place: source 0 = synthetic token payload of
  * (session, token..token+count); source 1 = far summary of chunk tokens
- * [aux, aux + chunk_tokens) of `dev_slot` written to (block, slot); source 2 =
+ * [aux, aux + chunk_tokens) of `dev_slot` written to (block, slot), the chunk's
+ * rows being src_rows[prefix, prefix + chunk_tokens); source 2 =
  * the same summary, already computed by K-presum into the stash row
  * (dev_slot, aux / chunk_tokens), copied to (block, slot). */
 typedef struct kvr_write_op {
     uint64_t token;
     uint64_t aux;
-    uint64_t prefix;        /* exclusive prefix of count over source-0 ops */
+    uint64_t prefix;        /* source 0: exclusive prefix of count over the ops; source 1:
+                               first index of the chunk's rows in the src_rows section */
     uint32_t block, slot, count, session;
     uint32_t dev_slot;      /* KVR_NO_SLOT: arena only */
     uint32_t source;
@@ -138,7 +144,8 @@ typedef struct kvr_span_rec {
 } kvr_span_rec;
 typedef struct kvr_prime_op {
     uint64_t tok_begin, tok_end;
-    uint32_t slot, pad;
+    uint32_t slot;
+    uint32_t rows;          /* first index of the tokens' source rows in src_rows */
 } kvr_prime_op;
 /* one per device slot, always n_slots entries */
 typedef struct kvr_slot_state {

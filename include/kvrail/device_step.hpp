@@ -71,11 +71,13 @@ public:
     void slot_state(uint32_t slot, SessionId sid, uint64_t written, bool live);
     void need(uint32_t slot, SessionId sid, TrainKind kind, std::span<const StagedSpan> spans,
               std::span<const uint64_t> first_tokens);
-    /// Window rows [tok_begin, tok_end) of `slot` copied from the arena through the
-    /// page table (an aliased prefix). `src`: the session owning those rows (the alias
-    /// source) — its pending rows are written before K-prime reads them.
+    /// Window rows [tok_begin, tok_end) of `slot` copied from the arena (an aliased
+    /// prefix): `rows` holds each token's source row as a global slot (block *
+    /// tokens_per_page + slot, KVR_NO_SLOT: unmapped) in the committed view. `src`: the
+    /// session owning those rows (the alias source) — its pending rows are written
+    /// before K-prime reads them.
     static constexpr SessionId kNoPrimeSource = 0xffffffffu;
-    void prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end, SessionId src = kNoPrimeSource);
+    void prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end, SessionId src, std::span<const uint32_t> rows);
     void far_selection(uint32_t slot, std::span<const uint64_t> chunk_ids);
 
     /// This GPU's per-step counts (KVR_COUNT_*), carried in the next launched descriptor

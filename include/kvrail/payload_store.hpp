@@ -39,6 +39,9 @@ struct GeneratedWrite {
     uint32_t count = 0;     // consecutive slots in `block`
     uint32_t source = 0;    // 0 = synthetic token payload, 1 = far-view summary job
     uint64_t aux = 0;       // source-specific (summary: chunk begin token)
+    /// summary jobs: the chunk's rows as global slots (block * tokens_per_page + slot)
+    /// in the committed view the summary reads (resolved by the caller)
+    std::span<const uint32_t> src_slots;
 };
 
 class PayloadStore {

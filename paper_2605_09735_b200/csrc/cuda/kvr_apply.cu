@@ -327,9 +327,10 @@ template <int E> __device__ void far_columns(const DevCtx &c, const kvr_write_op
 
 constexpr uint32_t kFarRows = 512; // chunk rows staged in shared memory
 
-__global__ void __launch_bounds__(256) k_far(DevCtx c) {
-    __shared__ uint64_t rows[kFarRows];
+// K-far's part of k_fmp: one CTA-iteration per (far job, 4 KiB column block).
+__device__ void far_part(const DevCtx &c, uint64_t *rows) {
     const kvr_step_header *h = hdr(c);
+    const uint32_t *src_rows = section<uint32_t>(c, h->off_src_rows);
     // far jobs are packed after the token writes
     const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write) + (h->n_write - h->n_far_jobs);
     const uint64_t cols = c.token_bytes / 16; // 16-byte columns per row
@@ -352,10 +353,10 @@ __global__ void __launch_bounds__(256) k_far(DevCtx c) {
         }
         if (op.source != 1)
             continue;
-        const uint32_t *tm = c.tmap + uint64_t(op.dev_slot) * c.max_tokens;
+        // the chunk's rows in the view as of the previous commit, resolved by the host
+        // (this step's K-map may already have changed the page table)
         for (uint32_t k = threadIdx.x; k < n_rows; k += blockDim.x) {
-            const uint64_t tok = op.aux + k;
-            const uint32_t gs = tok < c.max_tokens ? tm[tok] : kNoMap;
+            const uint32_t gs = src_rows[op.prefix + k];
             rows[k] = gs == kNoMap ? ~0ull : gslot_offset(c, gs); // unmapped: zeros (host validated coverage)
         }
         __syncthreads();
@@ -436,7 +437,7 @@ template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c) {
 // K-map: committed view edits into the page table (token granularity, so
 // mid-block aliases and tail extensions need no special case).
 
-__global__ void k_map(DevCtx c) {
+__device__ void map_part(const DevCtx &c) {
     const kvr_step_header *h = hdr(c);
     const kvr_edit_op *ops = section<kvr_edit_op>(c, h->off_edit);
     for (uint32_t i = blockIdx.x; i < h->n_edit; i += gridDim.x) {
@@ -459,12 +460,13 @@ __global__ void k_map(DevCtx c) {
 }
 
 // ---------------------------------------------------------------------------
-// K-prime: ring rows for tokens of [tok_begin, tok_end) from the arena via the
-// (updated) page table; one CTA per (op, token).
+// K-prime: ring rows for tokens of [tok_begin, tok_end) from the arena, each token's
+// source row resolved by the host in the committed view; one CTA per (op, token).
 
-__global__ void k_prime(DevCtx c) {
+__device__ void prime_part(const DevCtx &c) {
     const kvr_step_header *h = hdr(c);
     const kvr_prime_op *ops = section<kvr_prime_op>(c, h->off_prime);
+    const uint32_t *src_rows = section<uint32_t>(c, h->off_src_rows);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
     const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
     for (uint32_t i = 0; i < h->n_prime; ++i) {
@@ -473,7 +475,7 @@ __global__ void k_prime(DevCtx c) {
         for (uint64_t tok = op.tok_begin + blockIdx.x; tok < op.tok_end; tok += gridDim.x) {
             if (!ring_owned_by_writer(c, st, tok) || tok >= c.max_tokens)
                 continue;
-            const uint32_t gs = c.tmap[uint64_t(op.slot) * c.max_tokens + tok];
+            const uint32_t gs = src_rows[op.rows + (tok - op.tok_begin)];
             if (gs == kNoMap)
                 continue;
             const uint8_t *src = c.arena + gslot_offset(c, gs);
@@ -489,6 +491,15 @@ __global__ void k_prime(DevCtx c) {
             }
         }
     }
+}
+
+// K-far + K-map + K-prime in ONE kernel: K-far and K-prime read the rows the host
+// resolved (not the page table K-map edits), so the three are independent.
+__global__ void __launch_bounds__(256) k_fmp(DevCtx c) {
+    __shared__ uint64_t rows[kFarRows];
+    far_part(c, rows);
+    map_part(c);
+    prime_part(c);
 }
 
 } // namespace
@@ -535,8 +546,6 @@ __global__ void k_stamp(DevCtx c) {
 }
 void launch_stamp(const DevCtx &c, cudaStream_t s) { k_stamp<<<1, 1, 0, s>>>(c); }
 
-void launch_far(const DevCtx &c, cudaStream_t s, int sms) { k_far<<<sms * 2, 256, 0, s>>>(c); }
-void launch_map(const DevCtx &c, cudaStream_t s, int sms) { k_map<<<sms * 2, 256, 0, s>>>(c); }
-void launch_prime(const DevCtx &c, cudaStream_t s, int sms) { k_prime<<<sms * 4, 256, 0, s>>>(c); }
+void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms) { k_fmp<<<sms * 2, 256, 0, s>>>(c); }
 
 } // namespace kvr

@@ -159,9 +159,7 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     if (!full_step) { // apply-only: everything in order on one stream
         launch_write(c, s, d->sms, 0);
         launch_write(c, s, d->sms, 1);
-        launch_far(c, s, d->sms);
-        launch_map(c, s, d->sms);
-        launch_prime(c, s, d->sms);
+        launch_far_map_prime(c, s, d->sms);
         return;
     }
     // Side branch: the decode queries and K-scan depend only on the descriptor, so
@@ -176,9 +174,7 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     mark(1);
     launch_write(c, s, d->sms, 0);
     mark(2);
-    launch_far(c, s, d->sms);
-    launch_map(c, s, d->sms);
-    launch_prime(c, s, d->sms);
+    launch_far_map_prime(c, s, d->sms);
     mark(3);
     ck(cudaStreamWaitEvent(s, d->ev_join, 0), "join wait");
     mark(4);

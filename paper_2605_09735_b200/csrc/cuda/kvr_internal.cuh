@@ -109,7 +109,7 @@ __device__ inline uint64_t ring_mirror(const DevCtx &c, uint32_t row) {
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blob
 void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold); // generated payloads
 void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
-void launch_far(const DevCtx &c, cudaStream_t s, int sms);
+void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms); // K-far + K-map + K-prime
 void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp
 void launch_presum(const DevCtx &c, cudaStream_t s, int sms); // prompt rows + their far chunk means
 void launch_mass(const DevCtx &c, cudaStream_t s);             // attention-utility observations
@@ -117,8 +117,6 @@ bool prepare_mass(const DevCtx &c); // false: no K-mass for this geometry
 size_t mass_scratch_floats(const DevCtx &c);
 size_t mass_part_entries(const DevCtx &c);
 uint32_t mass_max_group();
-void launch_map(const DevCtx &c, cudaStream_t s, int sms);     // page-table edits
-void launch_prime(const DevCtx &c, cudaStream_t s, int sms);   // window priming
 void launch_scan(const DevCtx &c, cudaStream_t s);             // stage + reduce
 void launch_gather(const DevCtx &c, cudaStream_t s, int sms);  // trains -> window
 /// destination bytes of staged tokens [tok_begin, +count) into out (token-major)

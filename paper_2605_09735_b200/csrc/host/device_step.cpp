@@ -55,6 +55,7 @@ struct DeviceStep::Impl {
     std::vector<kvr_need_rec> needs;
     std::vector<kvr_span_rec> spans;
     std::vector<kvr_prime_op> primes;
+    std::vector<uint32_t> src_rows; // chunk rows of far jobs / source rows of primes (this wave)
     std::unordered_set<SessionId> prime_src; // sessions whose rows K-prime copies this step
     std::vector<uint32_t> far_ids;
     std::vector<kvr_slot_state> slots;
@@ -390,6 +391,8 @@ struct DeviceStep::Impl {
         h.off_presum = place(presum_ops.size() * sizeof(kvr_presum_op));
         h.n_presum_runs = uint32_t(presum_runs.size());
         h.off_presum_runs = place(presum_runs.size() * sizeof(kvr_presum_run));
+        h.n_src_rows = uint32_t(src_rows.size());
+        h.off_src_rows = place(src_rows.size() * sizeof(uint32_t));
         h.total_bytes = off;
         std::memcpy(h.counts, step_counts, sizeof(h.counts));
         if (off > g.max_desc_bytes)
@@ -413,6 +416,7 @@ struct DeviceStep::Impl {
         put(h.off_slots, slots.data(), slots.size() * sizeof(kvr_slot_state));
         put(h.off_presum, presum_ops.data(), presum_ops.size() * sizeof(kvr_presum_op));
         put(h.off_presum_runs, presum_runs.data(), presum_runs.size() * sizeof(kvr_presum_run));
+        put(h.off_src_rows, src_rows.data(), src_rows.size() * sizeof(uint32_t));
         return off;
     }
 
@@ -429,6 +433,7 @@ struct DeviceStep::Impl {
         wave_cow_dst.clear();
         primes.clear();
         prime_src.clear();
+        src_rows.clear();
     }
 
     void flush() {
@@ -540,6 +545,12 @@ struct DeviceStep::Impl {
             op.source = 1;
             if (g.chunk_tokens && presummed.erase(presum_key(w.session, w.aux / g.chunk_tokens)))
                 op.source = 2; // K-presum computed this mean when the rows were written
+            else {
+                if (w.src_slots.size() != g.chunk_tokens)
+                    throw std::runtime_error("far summary job without its chunk's source rows");
+                op.prefix = src_rows.size();
+                src_rows.insert(src_rows.end(), w.src_slots.begin(), w.src_slots.end());
+            }
             far_jobs.push_back(op);
             return;
         }
@@ -687,8 +698,12 @@ void DeviceStep::need(uint32_t slot, SessionId sid, TrainKind kind, std::span<co
     }
 }
 
-void DeviceStep::prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end, SessionId src) {
-    impl_->primes.push_back({tok_begin, tok_end, slot, 0});
+void DeviceStep::prime(uint32_t slot, uint64_t tok_begin, uint64_t tok_end, SessionId src,
+                       std::span<const uint32_t> rows) {
+    if (rows.size() != tok_end - tok_begin)
+        throw std::runtime_error("prime: one source row per token");
+    impl_->primes.push_back({tok_begin, tok_end, slot, uint32_t(impl_->src_rows.size())});
+    impl_->src_rows.insert(impl_->src_rows.end(), rows.begin(), rows.end());
     if (src != kNoPrimeSource)
         impl_->prime_src.insert(src); // its rows are read by K-prime: written hot, never deferred
 }

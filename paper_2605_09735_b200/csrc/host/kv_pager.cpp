@@ -823,7 +823,7 @@ void Pager::write_tokens(SessionId session, TokenRange range, std::span<const st
 }
 
 void Pager::write_tokens_generated(SessionId session, TokenRange range, uint32_t source,
-                                   uint64_t aux) {
+                                   uint64_t aux, std::span<const uint32_t> src_slots) {
     Impl &m = *impl_;
     Sess &s = m.get(session);
     std::unique_lock lk(s.mu);
@@ -838,6 +838,7 @@ void Pager::write_tokens_generated(SessionId session, TokenRange range, uint32_t
         w.count = n;
         w.source = source;
         w.aux = aux;
+        w.src_slots = src_slots;
         m.store->write_generated(w);
     });
 }

@@ -243,6 +243,8 @@ struct ScenarioDriver::Impl {
     int ekind = KVR_ELEM_F16;
     bool lanes_payload = false;
     uint32_t lane_shift = 7; // 2-byte lanes: (b - 128) / 2^lane_shift
+    std::vector<uint32_t> chunk_slots; // summarize(): a far chunk's rows (global slots)
+    std::vector<uint32_t> prime_slots; // device_step(): rows K-prime copies (global slots)
 
     std::unique_ptr<DeviceStep> dev;
     std::unique_ptr<Pager> pager;
@@ -589,11 +591,14 @@ struct ScenarioDriver::Impl {
             const ViewEntry *e = nullptr;
             BlockId scored = kInvalidBlock;
             double block_score = 0.0;
+            chunk_slots.clear();
             for (uint64_t tok = lo; tok < hi; ++tok) {
                 if (!e || tok < e->tokens.begin || tok >= e->tokens.end)
                     e = view.find(tok);
                 if (!e)
                     raise(Errc::unmapped_range, "chunk source token unmapped");
+                if (dev) // K-far reads the chunk's rows from this list, not the page table
+                    chunk_slots.push_back(e->block * tpp + e->slot_begin + uint32_t(tok - e->tokens.begin));
                 if (!dev)
                     pager->read_slots(e->block, e->slot_begin + uint32_t(tok - e->tokens.begin), 1,
                                       reinterpret_cast<std::byte *>(chunk.data() + (tok - lo) * lanes));
@@ -613,7 +618,7 @@ struct ScenarioDriver::Impl {
             }
             const uint64_t slot_tok = kSummaryTok + r.n_summaries;
             if (dev) {
-                pager->write_tokens_generated(r.id, {slot_tok, slot_tok + 1}, 1, lo);
+                pager->write_tokens_generated(r.id, {slot_tok, slot_tok + 1}, 1, lo, chunk_slots);
             } else {
                 const std::vector<float> mean = summarize_chunk(chunk, lanes, fv.chunk_tokens);
                 pager->write_tokens(r.id, {slot_tok, slot_tok + 1},
@@ -927,8 +932,16 @@ struct ScenarioDriver::Impl {
                 const uint64_t lo = r.written > cfg.far_view.near_window
                                         ? r.written - cfg.far_view.near_window
                                         : 0;
-                if (lo < r.write_begin)
-                    dev->prime(s, lo, r.write_begin, 0); // aliases the template session 0
+                if (lo < r.write_begin) { // aliases the template session 0
+                    const ViewDescriptor v = pager->active_view(r.id);
+                    prime_slots.clear();
+                    for (uint64_t tok = lo; tok < r.write_begin; ++tok) {
+                        const ViewEntry *e = v.find(tok);
+                        prime_slots.push_back(e ? e->block * tpp + e->slot_begin + uint32_t(tok - e->tokens.begin)
+                                                : KVR_NO_SLOT);
+                    }
+                    dev->prime(s, lo, r.write_begin, 0, prime_slots);
+                }
             }
             if (cfg.far_view.enabled && cfg.far_view.cap > 0 && !r.chunk_scores.empty()) {
                 const std::vector<uint64_t> pick = select_chunks(r.chunk_scores, cfg.far_view.cap);
