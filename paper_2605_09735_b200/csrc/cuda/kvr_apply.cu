@@ -132,7 +132,7 @@ __device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab,
 // `cold`: 0 = the hot write ops (rows read later in this step), 1 = the cold ops
 // (older prompt rows nothing in this step reads; launched after K-attn).
 template <uint32_t kPer, int kKind> // chunks per thread per unit; payload kind
-__global__ void __launch_bounds__(256) k_write(DevCtx c, int cold) {
+__device__ __forceinline__ void write_body(const DevCtx &c, int cold) {
     __shared__ LaneTable tab;
     const kvr_step_header *h = hdr(c);
     const uint32_t n_hot = h->n_write - h->n_far_jobs - h->n_cold;
@@ -376,7 +376,7 @@ __device__ void far_part(const DevCtx &c, uint64_t *rows) {
 // summed on the fly — the far job of the next step copies the mean from the
 // stash instead of re-reading chunk_tokens rows (same double sums, same order).
 
-template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c) {
+template <int kKind> __device__ __forceinline__ void presum_body(const DevCtx &c) {
     __shared__ LaneTable tab;
     const kvr_step_header *h = hdr(c);
     if (h->n_presum == 0)
@@ -493,6 +493,33 @@ __device__ void prime_part(const DevCtx &c) {
     }
 }
 
+// The step's last kernel stamps its end: the last CTA to finish (a ticket in
+// device memory, reset by that CTA) writes %globaltimer — no separate stamp node.
+__device__ __forceinline__ void stamp_if_last(const DevCtx &c) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(c.attn_sched + 2, 1u) == gridDim.x - 1) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            c.scan->end_ns = t;
+            c.attn_sched[2] = 0;
+        }
+    }
+}
+
+template <uint32_t kPer, int kKind> __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold, int stamp) {
+    write_body<kPer, kKind>(c, cold);
+    if (stamp)
+        stamp_if_last(c);
+}
+
+template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c, int stamp) {
+    presum_body<kKind>(c);
+    if (stamp)
+        stamp_if_last(c);
+}
+
 // K-far + K-map + K-prime in ONE kernel: K-far and K-prime read the rows the host
 // resolved (not the page table K-map edits), so the three are independent.
 __global__ void __launch_bounds__(256) k_fmp(DevCtx c) {
@@ -506,24 +533,24 @@ __global__ void __launch_bounds__(256) k_fmp(DevCtx c) {
 
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms) { k_apply<<<sms * 4, 256, 0, s>>>(c); }
 
-void launch_presum(const DevCtx &c, cudaStream_t s, int sms) {
+void launch_presum(const DevCtx &c, cudaStream_t s, int sms, int stamp) {
     if (!c.stash)
         return;
     if (c.esz == 4)
-        k_presum<kLanes32><<<sms * 4, 256, 0, s>>>(c);
+        k_presum<kLanes32><<<sms * 4, 256, 0, s>>>(c, stamp);
     else if (c.payload_mode == KVR_PAYLOAD_LANES)
-        k_presum<kLanes16><<<sms * 4, 256, 0, s>>>(c);
+        k_presum<kLanes16><<<sms * 4, 256, 0, s>>>(c, stamp);
     else
-        k_presum<kBytes><<<sms * 4, 256, 0, s>>>(c);
+        k_presum<kBytes><<<sms * 4, 256, 0, s>>>(c, stamp);
 }
 
 // cold: 0 hot writes, 1 cold writes (both over the whole GPU)
-void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold) {
+void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp) {
     // hot writes (few decode tokens + window rows): one chunk per thread for
     // spread; cold prompt rows: two chunks per thread for generator ILP
     const int kind = c.esz == 4 ? kLanes32 : c.payload_mode == KVR_PAYLOAD_LANES ? kLanes16 : kBytes;
     auto go = [&](auto per, auto kk) {
-        k_write<decltype(per)::value, decltype(kk)::value><<<sms * 8, 256, 0, s>>>(c, cold);
+        k_write<decltype(per)::value, decltype(kk)::value><<<sms * 8, 256, 0, s>>>(c, cold, stamp);
     };
     using std::integral_constant;
     if (kind == kLanes16)

@@ -189,14 +189,18 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     // on B200, co-running this int-bound generation beside the HBM-bound attention
     // (one CTA per SM on a forked branch) slowed the attention by more than the
     // overlap saved, so the step runs them after it with the whole GPU.
-    launch_write(c, s, d->sms, 1);
-    launch_presum(c, s, d->sms);
+    // the step's last kernel writes the end stamp (with a communicator: a stamp node
+    // after the collective)
+    const int stamp_in_kernel = d->comm ? 0 : 1;
+    launch_write(c, s, d->sms, 1, stamp_in_kernel && !c.stash);
+    launch_presum(c, s, d->sms, stamp_in_kernel);
     // the step's counts summed over every rank (the only cross-GPU traffic)
-    if (d->comm)
+    if (d->comm) {
         nck(nccl().all_reduce(c.desc + offsetof(kvr_step_header, counts), d->d_counts, KVR_COUNTS, ncclInt64,
                               ncclSum, d->comm, s),
             "per-step counts all-reduce");
-    launch_stamp(c, s);
+        launch_stamp(c, s);
+    }
     mark(7);
 }
 
@@ -327,8 +331,8 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         c.gspans = static_cast<GSpan *>(dalloc(d.get(), sizeof(GSpan) * c.max_scan, "gspans"));
         c.scan = static_cast<ScanCounters *>(dalloc(d.get(), sizeof(ScanCounters), "scan"));
         ck(cudaMemsetAsync(c.scan, 0, sizeof(ScanCounters), d->stream), "scan zero");
-        c.attn_sched = static_cast<uint32_t *>(dalloc(d.get(), 2 * sizeof(uint32_t), "attention schedule"));
-        ck(cudaMemsetAsync(c.attn_sched, 0, 2 * sizeof(uint32_t), d->stream), "schedule zero");
+        c.attn_sched = static_cast<uint32_t *>(dalloc(d.get(), 4 * sizeof(uint32_t), "schedule tickets"));
+        ck(cudaMemsetAsync(c.attn_sched, 0, 4 * sizeof(uint32_t), d->stream), "schedule zero");
         {
             const uint64_t off[2] = {~0ull, 0};
             auto *fault = static_cast<uint64_t *>(dalloc(d.get(), sizeof(off), "fault hooks"));

@@ -60,7 +60,8 @@ struct DevCtx {
     kvr_mass_run *mass_runs; // [slot][W]
     uint32_t *mass_count;    // [slot]
     const uint64_t *fault;   // [0] KVR_FAULT_DROP_SPAN, [1] KVR_FAULT_SHIFT_ROWS arguments — test hooks only
-    uint32_t *attn_sched;    // [0] next item to claim, [1] CTAs finished (tensor-core attention)
+    uint32_t *attn_sched;    // [0] next item to claim, [1] CTAs finished (tensor-core attention),
+                             // [2] CTAs finished of the step's last kernel (end stamp)
 };
 
 /// Token `tok` of a slot is written into the ring by K-write / K-prime only when it
@@ -107,11 +108,12 @@ __device__ inline uint64_t ring_mirror(const DevCtx &c, uint32_t row) {
 
 // ---- host launchers (one per kernel file) --------------------------------
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blob
-void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold); // generated payloads
+/// stamp: this launch is the step's last kernel and writes the step-end timestamp
+void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp = 0); // generated payloads
 void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
 void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms); // K-far + K-map + K-prime
 void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp
-void launch_presum(const DevCtx &c, cudaStream_t s, int sms); // prompt rows + their far chunk means
+void launch_presum(const DevCtx &c, cudaStream_t s, int sms, int stamp = 0); // prompt rows + their far chunk means
 void launch_mass(const DevCtx &c, cudaStream_t s);             // attention-utility observations
 bool prepare_mass(const DevCtx &c); // false: no K-mass for this geometry
 size_t mass_scratch_floats(const DevCtx &c);
