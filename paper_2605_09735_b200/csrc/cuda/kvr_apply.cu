@@ -102,6 +102,19 @@ __device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab,
         const uint64_t x = splitmix64(base ^ 0x4000000000000000ull ^ (b0 >> 4));
         const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
         const bool bf = c.elem_kind == KVR_ELEM_BF16;
+        if (!bf) {
+            // fp16: byte b as the half 1024 + b (bits 0x64bb: one PRMT builds two lanes),
+            // then ONE exact HFMA2: (1024 + b) * 2^-s - 1152 * 2^-s = (b - 128) * 2^-s
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);
+                const uint32_t pair = __byte_perm(src, 0x6464u, 0x4040u | k | ((k + 1) << 8));
+                const __half2 v = __hfma2(*reinterpret_cast<const __half2 *>(&pair), c.lane_h2_scale,
+                                          c.lane_h2_bias);
+                w[i] = *reinterpret_cast<const uint32_t *>(&v);
+            }
+            return make_int4(int(w[0]), int(w[1]), int(w[2]), int(w[3]));
+        }
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
             const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);

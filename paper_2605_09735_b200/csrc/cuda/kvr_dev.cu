@@ -284,6 +284,8 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
                 throw std::runtime_error("lane_shift must be <= 12");
             c.lane_scale = 1.0f / float(1u << sh);
             c.lane_bias = 8388608.0f * c.lane_scale + 128.0f * c.lane_scale; // exact: 2^(23-sh) + 2^(7-sh)
+            c.lane_h2_scale = __float2half2_rn(c.lane_scale);              // 2^-sh: exact in fp16 (sh <= 12)
+            c.lane_h2_bias = __float2half2_rn(-1152.0f * c.lane_scale);    // -1152 * 2^-sh: exact
         }
         if (g.query_mode > KVR_QUERY_F32)
             throw std::runtime_error("unknown query_mode");

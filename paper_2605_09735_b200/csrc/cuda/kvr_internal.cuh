@@ -39,6 +39,7 @@ struct DevCtx {
     uint32_t G, Rp; // ring guard rows (rows [0, G) mirrored at [R, R + G)) and plane rows R + G
     uint32_t max_scan, max_trains;
     float lane_scale, lane_bias; // 2-byte lanes: (2^23 + b) * scale - bias = (b - 128) * scale
+    __half2 lane_h2_scale, lane_h2_bias; // fp16 lanes: (1024 + b) * 2^-s - 1152 * 2^-s
     uint32_t query_mode;         // KVR_QUERY_*
     uint8_t *arena;   // arena_pages * page_bytes
     uint8_t *ring;    // [slot][L][R][row_elems] elements
