@@ -307,11 +307,21 @@ def run_b200(args, rank, local, world) -> dict | None:
         cfg["b200"]["utility_every"] = args.utility_every
     d = pkg.Driver(cfg, device=local)
     in_graph = world > 1 and args.backend == "nccl"
+    comm_note = None
     if in_graph:  # the per-step counts all-reduce, captured in every step graph
         import torch.distributed as dist
-        uid = [pkg.kvrail.comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        d.comm_init(uid[0], rank, world)
+        ok, err = 1, None
+        try:
+            uid = [pkg.kvrail.comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(uid, src=0)
+            d.comm_init(uid[0], rank, world)
+        except pkg.kvrail.KvrailError as e:
+            ok, err = 0, str(e)
+        if not all_filled(bool(ok), world):  # every rank or none: the graphs must agree
+            if ok:
+                d.comm_destroy()
+            in_graph = False
+            comm_note = f"in-graph NCCL unavailable ({err or 'on another rank'}): per-step counts via torch.distributed"
     width = cfg["workload"]["concurrency"]
     # fill the fixed-width batch (admissions write whole prompts), then warm up
     fill = 0
@@ -411,7 +421,8 @@ def run_b200(args, rank, local, world) -> dict | None:
         "rank": rank, "cfg": cfg, "recs": recs, "dev_s": dev_s_max, "wall_s": wall_s_max,
         "tokens": tokens_all, "attn_bytes": attn_bytes, "attn_s": attn_s,
         "counts_collective": ("ncclAllReduce in the step graph (kvr_comm_init)" if in_graph else
-                              "torch.distributed all_reduce per step (gloo)" if world > 1 else "none"),
+                              "torch.distributed all_reduce per step" if world > 1 else "none"),
+        "comm_note": comm_note,
         "attn_bytes_all": attn_bytes_all,
         "gather_bytes": gather_bytes, "gather_s": gather_s, "gather_bytes_all": gather_bytes_all,
         "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "captures": captures,
@@ -637,7 +648,7 @@ def main():
                 # step counters (ScanCounters, 40 B) + the all-reduced counts (4 x int64)
                 "d2h_bytes_per_step": 40 + (32 if res["counts_collective"].startswith("nccl") else 0)},
         "multi_gpu": {"n_gpus": world, "shard": "request_id % n_gpus",
-                      "counts_collective": res["counts_collective"]},
+                      "counts_collective": res["counts_collective"], "note": res["comm_note"]},
         "gpu_launches": res["step_kernels"] * args.steps,
         "graph": {"kernels_per_step": res["step_kernels"], "captures": res["captures"],
                   "note": "one CUDA graph per descriptor ring slot, captured once, replayed every step"},

@@ -248,6 +248,7 @@ int kvr_dev_utility(kvr_dev *d, uint32_t ring_slot, kvr_mass_run *out, uint32_t 
 int kvr_comm_unique_id(uint8_t id[128]); /* on one rank; the caller distributes it */
 int kvr_comm_init(kvr_dev *d, const uint8_t id[128], int rank, int world);
 int kvr_comm_world(kvr_dev *d, int *rank, int *world); /* (0, 1) without a communicator */
+int kvr_comm_destroy(kvr_dev *d); /* drop the communicator (before the first launch only) */
 /* kernel nodes in the captured step graph (0 before the first graph launch) */
 int kvr_dev_step_kernels(kvr_dev *d, uint32_t *out);
 /* step graphs captured so far: 2 (one per descriptor ring slot) after the first two

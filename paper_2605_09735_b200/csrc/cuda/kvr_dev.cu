@@ -722,6 +722,18 @@ int kvr_comm_init(kvr_dev *d, const uint8_t id[128], int rank, int world) {
     });
 }
 
+int kvr_comm_destroy(kvr_dev *d) {
+    return guard([&] {
+        if (d->n_launches)
+            throw std::runtime_error("kvr_comm_destroy: the step graphs already hold the collective");
+        if (d->comm)
+            nck(nccl().comm_destroy(d->comm), "ncclCommDestroy");
+        d->comm = nullptr;
+        d->rank = 0;
+        d->world = 1;
+    });
+}
+
 int kvr_comm_world(kvr_dev *d, int *rank, int *world) {
     return guard([&] {
         *rank = d->rank;

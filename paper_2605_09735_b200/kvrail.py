@@ -288,6 +288,7 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_driver_fault": [vp, C.c_int, C.c_uint64],
         "kvr_driver_comm_init": [vp, C.c_char_p, C.c_int, C.c_int],
         "kvr_comm_unique_id": [C.c_char_p],
+        "kvr_comm_destroy": [vp],
         "kvr_device_open": [C.POINTER(Geometry), C.POINTER(vp)],
         "kvr_device_close": [vp],
         "kvr_device_flush": [vp],
@@ -789,6 +790,10 @@ class Driver:
         """Join the in-graph per-step counts all-reduce over NCCL (before the first step)."""
         assert len(unique_id) == 128
         check(native_lib().kvr_driver_comm_init(self.h, unique_id, rank, world))
+
+    def comm_destroy(self) -> None:
+        """Drop the counts communicator again (only before the first step)."""
+        check(native_lib().kvr_comm_destroy(self.device().raw()))
 
     FAULT_DROP_SPAN, FAULT_SHIFT_ROWS, FAULT_ALL = 1, 2, 0xFFFFFFFFFFFFFFFE
 

@@ -119,6 +119,14 @@ def test_in_graph_counts_all_reduce_world_one():
         late = kv.Driver(cfg, device=0)
         late.step()
         late.comm_init(kv.comm_unique_id(), 0, 1)
+    # bench.py's fallback: a communicator dropped again before the first step
+    back = kv.Driver(dict(cfg, steps=8), device=0)
+    back.comm_init(kv.comm_unique_id(), 0, 1)
+    back.comm_destroy()
+    back.run()
+    back.sync()
+    r = back.record(7)
+    assert r.global_live == r.live_sessions
 
 
 def test_bench_spawns_ranks():
