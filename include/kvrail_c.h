@@ -165,6 +165,8 @@ typedef struct kvr_transport_config { /* TransportConfig, transport.hpp:17-23 */
     double max_hold;
     uint32_t max_trains_per_step;
     uint32_t merge;
+    /* B200 page-run merge (0, 0 = the reference's exact abutment; transport.hpp abuts()) */
+    uint64_t run_page_bytes, run_span_bytes;
 } kvr_transport_config;
 
 typedef struct kvr_train { /* DmaTrain, transport.hpp:38-45; descriptors live in a flat array */

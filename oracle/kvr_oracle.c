@@ -306,7 +306,13 @@ int kvo_reduce(const kvr_descriptor *descs, uint64_t n, const kvr_transport_conf
     for (uint64_t i = 0; i < n; ++i) {
         const kvr_descriptor *d = v[i].d;
         if (open) {
-            int adjacent = prev->kind == d->kind && prev->phys_offset + prev->length == d->phys_offset;
+            /* exact abutment (transport.cpp:85-110), or the B200 page-run rule: a descriptor
+             * ending at a page's last token slot abuts the next page's start */
+            const uint64_t end = prev->phys_offset + prev->length;
+            int adjacent = prev->kind == d->kind &&
+                           (end == d->phys_offset ||
+                            (cfg->run_page_bytes && end % cfg->run_page_bytes == cfg->run_span_bytes &&
+                             d->phys_offset == end - cfg->run_span_bytes + cfg->run_page_bytes));
             if (cur.total_bytes >= cfg->merge_threshold)
                 KVO_CLOSE(0);
             else if (now - cur.oldest_stage_time >= cfg->max_hold)

@@ -284,6 +284,8 @@ int kvr_reduce(const kvr_descriptor *descs, uint64_t n, const kvr_transport_conf
         tc.max_hold = cfg->max_hold;
         tc.max_trains_per_step = cfg->max_trains_per_step;
         tc.merge = cfg->merge != 0;
+        tc.run_page_bytes = cfg->run_page_bytes;
+        tc.run_span_bytes = cfg->run_span_bytes;
         const auto t = reduce(std::move(v), tc, now);
         uint64_t k = 0;
         for (uint64_t i = 0; i < t.size(); ++i) {

@@ -129,7 +129,8 @@ class Descriptor(C.Structure):
 
 class TransportConfig(C.Structure):
     _fields_ = [("merge_threshold", C.c_uint64), ("max_hold", C.c_double),
-                ("max_trains_per_step", C.c_uint32), ("merge", C.c_uint32)]
+                ("max_trains_per_step", C.c_uint32), ("merge", C.c_uint32),
+                ("run_page_bytes", C.c_uint64), ("run_span_bytes", C.c_uint64)]
 
 
 class Train(C.Structure):
@@ -496,12 +497,13 @@ def stage(needs: Sequence[tuple[int, int, Sequence[tuple[int, int, int]]]], page
 
 
 def reduce(descs: Sequence[tuple], tau: int, max_hold: float, merge: bool, now: float,
-           api_: Api | None = None):
-    """reduce(): returns [(kind, reason, total_bytes, oldest, issue, [descs...]), ...]."""
+           api_: Api | None = None, run_page: int = 0, run_span: int = 0):
+    """reduce(): returns [(kind, reason, total_bytes, oldest, issue, [descs...]), ...].
+    run_page / run_span: the B200 page-run merge (TransportConfig::run_page_bytes)."""
     a = api_ or api()
     arr = (Descriptor * max(1, len(descs)))(*[
         Descriptor(off, ln, st, k, b, s, 0) for off, ln, st, k, b, s in descs])
-    cfg = TransportConfig(tau, max_hold, 2, int(merge))
+    cfg = TransportConfig(tau, max_hold, 2, int(merge), run_page, run_span)
     cap = len(descs) + 1
     trains = (Train * cap)()
     ordered = (Descriptor * max(1, len(descs)))()

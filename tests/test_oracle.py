@@ -24,7 +24,7 @@ def test_payload_golden():
         assert lib.kvo_fnv1a(buf, row["token_bytes"], 0) == row["fnv"]
 
 
-@pytest.mark.parametrize("elem_bytes,payload", [(2, "bytes"), (4, "bytes"), (2, "lanes")])
+@pytest.mark.parametrize("elem_bytes,payload", [(2, "bytes"), (4, "bytes"), (2, "lanes"), (2, "wide")])
 def test_restated_payload_equals_stored_bytes(elem_bytes, payload):
     """Every written token the twin driver stored (pinned to the reference by
     the staged-byte hashes of the golden traces) equals the restatement."""
@@ -42,6 +42,7 @@ def test_restated_payload_equals_stored_bytes(elem_bytes, payload):
     tb = p.cfg.token_bytes()
     lib = ob.oracle()
     buf = C.create_string_buffer(tb)
+    shift = 3 if payload == "wide" else 7  # lanes (b - 128) / 2^shift
     checked = 0
     for slot, session, written in d.live():
         view = p.active_view(session)
@@ -50,15 +51,27 @@ def test_restated_payload_equals_stored_bytes(elem_bytes, payload):
             if payload == "bytes":
                 lib.kvo_fill_token_payload(cfg["seed"], session, t, tb, elem_bytes, buf)
             else:
-                lib.kvo_fill_token_lanes(cfg["seed"], session, t, tb // elem_bytes, 1, buf)
+                lib.kvo_fill_token_lanes_shift(cfg["seed"], session, t, tb // elem_bytes, 1, shift, buf)
             if t < 64 and got != buf.raw:  # aliased shared prefix holds template-0 bytes
                 if payload == "bytes":
                     lib.kvo_fill_token_payload(cfg["seed"], 0, t, tb, elem_bytes, buf)
                 else:
-                    lib.kvo_fill_token_lanes(cfg["seed"], 0, t, tb // elem_bytes, 1, buf)
+                    lib.kvo_fill_token_lanes_shift(cfg["seed"], 0, t, tb // elem_bytes, 1, shift, buf)
             assert got == buf.raw, (session, t)
             checked += 1
     assert checked > 100
+
+
+def test_f32_query_restatement():
+    """b200.query = f32: 24-bit lanes in [-1, 1), two per splitmix64, generally not
+    representable in fp16 / bf16 (the tensor-core kernel's lo terms are non-zero)."""
+    import numpy as np
+    q = ob.fill_query(7, 3, 11, 2, 5, 128, 2, 1)
+    assert all(-1.0 <= v < 1.0 for v in q) and len(set(q)) == 128
+    assert all(float(np.float32(v)) == v and (v * 2 ** 23).is_integer() for v in q)
+    bf = np.asarray(q, np.float32).view(np.uint32) & 0xFFFF
+    assert (bf != 0).mean() > 0.9
+    assert ob.fill_query(7, 3, 11, 2, 5, 128, 2, 0) != q  # mode 0: the exact byte lanes
 
 
 def test_half_and_bf16_rounding_match_numpy_and_torch():

@@ -123,6 +123,41 @@ def test_random_needs_match_reference_and_restatement(seed, ref_api):
     assert ties == 0 and o_t == mine_t
 
 
+@pytest.mark.parametrize("seed", range(20))
+def test_page_run_merge_matches_restatement(seed):
+    """The B200 page-run rule (TransportConfig::run_page_bytes): 12-token pages with
+    slack (span 12 * TOK of a 16 KiB page). Host reduce() == the C restatement; the
+    policy never joins non-consecutive pages or kinds, and never needs more trains
+    than exact abutment."""
+    rng = random.Random(seed)
+    span = 12 * TOK
+    ds = []
+    for b in rng.sample(range(80), rng.randint(1, 40)):
+        sb = rng.choice([0, 0, 0, rng.randrange(12)])
+        n = rng.choice([12 - sb, rng.randint(1, 12 - sb)])
+        ds.append((b * PAGE + sb * TOK, n * TOK, 5.0, rng.choice([0, 0, 1]), b, 0))
+    tau = rng.choice([4 * PAGE, 16 * PAGE, 1 << 40])
+    mine = kv.reduce(ds, tau, 10.0, True, 5.0, run_page=PAGE, run_span=span)
+    exact = kv.reduce(ds, tau, 10.0, True, 5.0)
+    assert len(mine) <= len(exact)
+    lib = ob.oracle()
+    cfg = kv.TransportConfig(tau, 10.0, 2, 1, PAGE, span)
+    tr = (kv.Train * (len(ds) + 1))()
+    od = (kv.Descriptor * len(ds))()
+    nt, ties = C.c_uint64(), C.c_uint64()
+    arr = (kv.Descriptor * len(ds))(*[kv.Descriptor(o, l, st, k, b, s, 0) for o, l, st, k, b, s in ds])
+    assert lib.kvo_reduce(arr, len(ds), C.byref(cfg), 5.0, tr, len(ds) + 1, C.byref(nt), od, C.byref(ties)) == 0
+    oracle_t = [(t.kind, t.reason, t.total_bytes, t.oldest_stage_time, t.issue_time,
+                 [od[k].astuple() for k in range(t.desc_begin, t.desc_begin + t.desc_count)])
+                for t in tr[:nt.value]]
+    assert oracle_t == mine
+    for kind, _, _, _, _, dd in mine:
+        for a, b in zip(dd, dd[1:]):
+            end = a[0] + a[1]
+            assert a[3] == b[3] == kind
+            assert end == b[0] or (end % PAGE == span and b[0] == end - span + PAGE)
+
+
 def test_reduce_invariants():
     rng = random.Random(31)
     for _ in range(60):
