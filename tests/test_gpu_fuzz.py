@@ -129,3 +129,52 @@ def test_random_workload_tensor_core_attention(seed):
     checked, bad, first = d.device_check()
     assert bad == 0, first
     assert ob.check_driver_window_and_attention(d) <= 1e-3
+
+
+@pytest.mark.parametrize("seed", range(300, 312))
+def test_random_workload_b200_policies(seed):
+    """The round-2 B200 options on random workloads, device against its host twin under
+    the same options: page-run transfer groups on pages with slack (token bytes not
+    dividing the page), prefill budgets, wide payloads and fp32 queries, both attention
+    kernels. Destination-hashed trace == host twin, K-scan == host reduce, every staged
+    row delivered to the window, attention within 1e-3 of the double oracle."""
+    rng = random.Random(seed)
+    layers = rng.choice([3, 5, 6])             # 2 * layers * 256 B tokens: slack in power-of-two pages
+    far = rng.random() < 0.3
+    elem = 4 if far else 2
+    kvh = rng.choice([1, 2])
+    hd = 128
+    tb = 2 * layers * kvh * hd * elem
+    page = 1
+    while page < 8 * tb:
+        page *= 2
+    tpp = page // tb
+    tc = not far and rng.random() < 0.5
+    g = rng.choice([4, 8]) if tc else rng.choice([1, 2])
+    cfg = {
+        "label": f"pol{seed}", "seed": seed, "steps": rng.choice([60, 100]), "warmup_steps": 0,
+        "pager": {"page_bytes": page, "layers": layers, "kv_head_dim": kvh * hd, "elem_bytes": elem},
+        "transport": {"tau_bytes": page * rng.choice([2, 8, 32])},
+        "far_view": {"enabled": far, "w_star": rng.choice([128, 256, 512])},
+        "workload": {"requests": 10000, "concurrency": rng.choice([8, 16]), "prompt_min": 16,
+                     "prompt_max": rng.choice([512, 1500]), "arrivals_per_window": 40.0, "seed": 1},
+        "shaping": {"staged_refresh_period": rng.choice([2, 4]), "shared_prefix_tokens": tpp * 2},
+    }
+    if far:
+        cfg["far_view"].update({"cap": rng.choice([8, 16]), "sv_chunk": tpp * 2})
+    b200 = {"kv_heads": kvh, "head_dim": hd, "q_heads": kvh * g, "transfer": "page_runs",
+            "payload": "lanes" if far else rng.choice(["lanes", "wide"]),
+            "query": "exact" if far else rng.choice(["exact", "f32"]),
+            "dtype": "fp32" if far else rng.choice(["bf16", "fp16"]),
+            "attention_kernel": "tcgen05" if tc else "cuda_core", "trace": True}
+    host = kv.Driver(dict(cfg, b200=dict(b200)))
+    host.run()
+    budget = rng.choice([0, 0, 16, 256])
+    d = kv.Driver(dict(cfg, b200=dict(b200, check=True, prefill_budget=budget)), device=0)
+    d.run()
+    assert d.trace() == host.trace()
+    checked, bad, first = d.device_check()
+    assert bad == 0, first
+    win, behind, missing = d.staged_rows()
+    assert missing == 0 and win > 0
+    assert ob.check_driver_window_and_attention(d) <= 1e-3
