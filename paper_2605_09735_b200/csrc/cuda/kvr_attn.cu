@@ -488,7 +488,10 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
     p->smem = p->stages * stage + size_t(kMaxG) * (wph - 1) * 32 * c.group * (2 + c.hd / 32) * 4 +
               2 * p->stages * 8 + 16;
     p->grid = uint32_t(sms);
-    cudaFuncSetAttribute(p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem));
+    if (cudaFuncSetAttribute(p->fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(p->smem)) != cudaSuccess) {
+        delete p; // a geometry whose stages do not fit shared memory: no plan (open fails loudly)
+        return nullptr;
+    }
 
     // 4-D view of the ring: (head_dim, 2*Hkv heads, R rows, L*n_slots)
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;

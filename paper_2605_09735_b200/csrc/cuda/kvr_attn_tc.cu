@@ -332,7 +332,10 @@ __device__ inline bool elect_one() {
 /// a few ahead of its own tile stream and publishes them in a shared-memory queue;
 /// every role reads the CTA's j-th item from it (item j -> softmax warpgroup j % 2).
 constexpr uint32_t kQ = 64;     // queue entries (roles lag the claimer by < ~10 items)
-constexpr uint32_t kAheadQ = 4; // items claimed ahead of the claimer's own position
+#ifndef KVR_TC_AHEADQ
+#define KVR_TC_AHEADQ 4
+#endif
+constexpr uint32_t kAheadQ = KVR_TC_AHEADQ; // items claimed ahead of the claimer's own position
 struct ItemQueue {
     uint32_t item[kQ];
     uint32_t tail; // items published
@@ -929,8 +932,9 @@ const void *attn_tc_kernel(const DevCtx &c) {
     if (!attn_tc_ready(c))
         return nullptr;
     TcFn fn = c.elem_kind == KVR_ELEM_BF16 ? pick_tc<__nv_bfloat16>(c.group) : pick_tc<__half>(c.group);
-    if (fn)
-        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_tc_smem()));
+    if (fn && cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(attn_tc_smem())) !=
+                  cudaSuccess)
+        return nullptr; // shared-memory request refused: no tensor-core plan (open fails loudly)
     return reinterpret_cast<const void *>(fn);
 }
 

@@ -256,8 +256,8 @@ uint32_t mass_max_group() { return kMaxGroup; }
 bool prepare_mass(const DevCtx &c) {
     if (!rows_kernel(c) || runs_smem(c) > (200u << 10))
         return false;
-    cudaFuncSetAttribute(k_mass_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(runs_smem(c)));
-    return true;
+    return cudaFuncSetAttribute(k_mass_runs, cudaFuncAttributeMaxDynamicSharedMemorySize, int(runs_smem(c))) ==
+           cudaSuccess;
 }
 
 void launch_mass(const DevCtx &c, cudaStream_t s) {
