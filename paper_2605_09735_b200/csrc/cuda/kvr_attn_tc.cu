@@ -350,27 +350,34 @@ __device__ inline void st_vol(uint32_t *p, uint32_t v) {
     asm volatile("st.volatile.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
 /// Claimer (one thread): publish items until `want` are available or the stream ends.
+/// Items are claimed kClaim at a time (one atomic round trip, their slot states loaded
+/// together) — the claimer is warp 0's lane 0, whose K tile loads wait on it.
+#ifndef KVR_TC_CLAIM
+#define KVR_TC_CLAIM 1
+#endif
+constexpr uint32_t kClaim = KVR_TC_CLAIM;
 __device__ inline void claim_to(ItemQueue *q, uint32_t want, const DevCtx &c, const kvr_slot_state *slots,
                                 uint32_t n_items) {
     uint32_t tail = q->tail;
     while (tail < want && q->end == ~0u) {
-        uint32_t it;
-        for (;;) {
-            it = atomicAdd(c.attn_sched, 1u);
-            if (it >= n_items)
-                break;
-            Item I;
-            if (item_of(c, slots, it, I) && I.n_tiles)
-                break;
-        }
-        if (it >= n_items) {
+        const uint32_t base = atomicAdd(c.attn_sched, kClaim);
+        if (base >= n_items) {
             __threadfence_block();
             st_vol(&q->end, tail);
             break;
         }
-        q->item[tail % kQ] = it;
+        bool active[kClaim];
+#pragma unroll
+        for (uint32_t i = 0; i < kClaim; ++i) {
+            Item I;
+            active[i] = base + i < n_items && item_of(c, slots, base + i, I) && I.n_tiles;
+        }
+#pragma unroll
+        for (uint32_t i = 0; i < kClaim; ++i)
+            if (active[i])
+                q->item[(tail++) % kQ] = base + i;
         __threadfence_block();
-        st_vol(&q->tail, ++tail);
+        st_vol(&q->tail, tail);
     }
 }
 /// The j-th item of the CTA's stream: 1 (in `it`), 0 at the stream's end, -1 not
@@ -722,14 +729,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         float *rd = red + w * 2 * 4 * 8;
         float *ld = lred + w * 4 * 8;
         const float scale_log2 = 1.4426950408889634f / sqrtf(float(kHd));
-        if (w == 0) // live slots with an empty window: zero output
-            for (uint32_t it = blockIdx.x; it < n_items; it += gridDim.x) {
-                Item I;
-                if (item_of(c, slots, it, I) && I.n_tiles == 0)
-#pragma unroll
-                    for (int g = 0; g < G; ++g)
-                        c.out[((uint64_t(I.slot) * c.L + I.layer) * c.Hq + uint64_t(I.head) * G + g) * kHd + t] =
-                            0.f;
+        // live slots with an empty view (no near rows, no far rows: no item has a tile):
+        // zero output. One slot-state load per slot — walking this CTA's static share
+        // of items here (one dependent load each) held warpgroup 0 for up to ~100 us.
+        if (w == 0)
+            for (uint32_t s = blockIdx.x; s < c.n_slots; s += gridDim.x) {
+                const kvr_slot_state st = slots[s];
+                if (!st.live || st.written || st.far_count)
+                    continue;
+                float4 *os = reinterpret_cast<float4 *>(c.out + uint64_t(s) * c.L * c.Hq * kHd);
+                for (uint32_t i = t; i < c.L * c.Hq * kHd / 4; i += 128)
+                    os[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         uint32_t n = 0, m_items = 0;
         Cursor cur;
