@@ -155,7 +155,8 @@ __device__ __forceinline__ void write_body(const DevCtx &c, int cold) {
     const uint64_t total = cold ? h->write_tokens_cold : h->write_tokens;
     if (total == 0)
         return;
-    tab.fill(c);
+    if constexpr (kKind == kLanes32) // the lane table serves only the fp32 reference pattern
+        tab.fill(c);
     const uint32_t chunks = uint32_t(c.token_bytes / 16);
     const uint32_t row_chunks = c.row_elems * c.esz / 16;
     // work unit = one blockDim-wide slice of 16-byte chunks of one token, so a
@@ -167,18 +168,8 @@ __device__ __forceinline__ void write_body(const DevCtx &c, int cold) {
     const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
     const uint64_t u0 = blockIdx.x * per, u1 = min(units, u0 + per);
     uint32_t cur = 0;
-    if (u0 < u1) {
-        const uint64_t j0 = u0 / slices;
-        uint32_t lo = 0, hi = n; // last op with prefix <= j0
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) / 2;
-            if (ops[mid].prefix <= j0)
-                lo = mid;
-            else
-                hi = mid;
-        }
-        cur = lo;
-    }
+    if (u0 < u1) // last op with prefix <= j0 (every warp searches: 2-3 rounds of parallel probes)
+        cur = warp_last_le(n, u0 / slices, [&](uint32_t i) { return ops[i].prefix; });
     kvr_write_op op = ops[cur < n ? cur : 0];
     // (token, slice) advance incrementally; per-token addresses are recomputed
     // only when the token changes (no 64-bit division in the loop)
@@ -394,7 +385,8 @@ template <int kKind> __device__ __forceinline__ void presum_body(const DevCtx &c
     const kvr_step_header *h = hdr(c);
     if (h->n_presum == 0)
         return;
-    tab.fill(c);
+    if constexpr (kKind == kLanes32) // the lane table serves only the fp32 reference pattern
+        tab.fill(c);
     constexpr int E = kKind == kLanes32 ? 4 : 2;
     const kvr_presum_op *ops = section<kvr_presum_op>(c, h->off_presum);
     const kvr_presum_run *runs = section<kvr_presum_run>(c, h->off_presum_runs);

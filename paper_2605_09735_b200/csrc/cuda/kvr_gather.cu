@@ -118,20 +118,13 @@ __device__ inline uint64_t dst_mirror(const DevCtx &c, const uint8_t *dst) {
 struct Walker {
     uint64_t tok_idx;
     uint32_t grp, piece, cur;
+    /// (whole warp) position at unit u0: span found by warp_last_le
     __device__ void init(const DevCtx &c, uint32_t n_spans, uint64_t u0, uint32_t groups, uint32_t pieces) {
         piece = uint32_t(u0 % pieces);
         const uint64_t gu = u0 / pieces;
         grp = uint32_t(gu % groups);
         tok_idx = gu / groups;
-        uint32_t lo = 0, hi = n_spans; // last span with tok_prefix <= tok_idx
-        while (hi - lo > 1) {
-            const uint32_t mid = (lo + hi) / 2;
-            if (c.gspans[mid].tok_prefix <= tok_idx)
-                lo = mid;
-            else
-                hi = mid;
-        }
-        cur = lo;
+        cur = warp_last_le(n_spans, tok_idx, [&](uint32_t i) { return c.gspans[i].tok_prefix; });
     }
     __device__ void advance(const DevCtx &c, uint32_t n_spans, uint32_t groups, uint32_t pieces) {
         if (++piece < pieces)
@@ -169,7 +162,7 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c) {
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
     const uint32_t n_spans = c.scan->spans;
     const uint64_t tokens = c.scan->total_tokens;
-    if (tokens == 0 || (c.scan->status & 4u) || threadIdx.x != 0)
+    if (tokens == 0 || (c.scan->status & 4u))
         return;
     const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
     const uint32_t pieces = row_bytes > kMaxPiece ? uint32_t((row_bytes + kMaxPiece - 1) / kMaxPiece) : 1;
@@ -184,11 +177,13 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c) {
     const uint64_t u0 = blockIdx.x * per, u1 = units < u0 + per ? units : u0 + per;
     if (u0 >= u1)
         return;
+    Walker wk;
+    wk.init(c, n_spans, u0, groups, pieces); // the whole warp searches; lane 0 then drives the ring
+    if (threadIdx.x != 0)
+        return;
     for (int s = 0; s < kStages; ++s)
         mbar_init(&full[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    Walker wk;
-    wk.init(c, n_spans, u0, groups, pieces);
     const uint64_t drop = c.fault[0], shift = c.fault[1]; // test hooks (off: ~0, 0)
     uint64_t next = u0;
     Unit mv[kStages];

@@ -107,6 +107,24 @@ __device__ inline uint64_t ring_mirror(const DevCtx &c, uint32_t row) {
     return row < c.G ? uint64_t(c.R) * c.row_elems : 0;
 }
 
+/// Last index i in [0, n) with key(i) <= v for a non-decreasing key with key(0) <= v,
+/// found by the whole warp in <= 3 rounds of 32 parallel probes (n <= 32768) instead
+/// of ~log2(n) dependent loads: the per-CTA start-up search of K-write and K-gather.
+/// Every lane of the warp must call it; all get the same result.
+template <class Key> __device__ inline uint32_t warp_last_le(uint32_t n, uint64_t v, Key key) {
+    const uint32_t lane = threadIdx.x & 31;
+    uint32_t lo = 0, hi = n;
+    while (hi - lo > 1) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t idx = lo + lane * step;
+        const bool p = lane == 0 || (idx < hi && key(idx) <= v);
+        const uint32_t top = 31 - __clz(__ballot_sync(0xffffffffu, p));
+        lo += top * step;
+        hi = min(hi, lo + step);
+    }
+    return lo;
+}
+
 // ---- host launchers (one per kernel file) --------------------------------
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blob
 /// stamp: this launch is the step's last kernel and writes the step-end timestamp
