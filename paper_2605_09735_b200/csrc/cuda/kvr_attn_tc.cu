@@ -63,7 +63,10 @@ constexpr uint32_t kQBytes = 3 * 2048;       // the Q operand: up to 3 column bl
 /// Split terms and MMA widths of a (T, g) variant.
 template <typename T, int G> struct Splits {
     static constexpr bool kBf = std::is_same_v<T, __nv_bfloat16>;
-    static constexpr int QS = kBf ? 3 : 2;                    // q terms
+#ifndef KVR_TC_QS3
+#define KVR_TC_QS3 1
+#endif
+    static constexpr int QS = kBf && KVR_TC_QS3 ? 3 : 2;       // q terms
     static constexpr int PS = kBf && 3 * G <= kN ? 3 : 2;     // p terms
     static constexpr int NQ = QS * G <= 16 ? 16 : 32;         // S MMA N
     static_assert(QS * G <= 24 && PS * G <= kN, "split columns must fit the operand buffers");
