@@ -244,6 +244,108 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c) {
     bulk_wait_all();
 }
 
+// Two-warp variant: warp 0's lane 0 only loads (TMA bulk, global -> shared), warp 1's
+// lane 0 only stores (one bulk store per layer row + guard copies) and hands each stage
+// back through an `empty` mbarrier once its stores have read it — the loads of later
+// units no longer queue behind the store issue of earlier ones (8 stores per unit for
+// 4 KiB rows). Unit descriptions travel through shared memory (released by the loader's
+// arrive on `full`, acquired by the storer's wait).
+template <int kSt>
+__global__ void __launch_bounds__(64) k_gather2(DevCtx c) {
+    extern __shared__ __align__(128) uint8_t stage[];
+    __shared__ __align__(8) uint64_t full[kSt], empty[kSt];
+    __shared__ Unit info[kSt];
+    const kvr_step_header *h = hdr(c);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint32_t n_spans = c.scan->spans;
+    const uint64_t tokens = c.scan->total_tokens;
+    if (tokens == 0 || (c.scan->status & 4u))
+        return;
+    const uint64_t row_bytes = uint64_t(c.row_elems) * c.esz;
+    const uint32_t pieces = row_bytes > kMaxPiece ? uint32_t((row_bytes + kMaxPiece - 1) / kMaxPiece) : 1;
+    uint32_t lg = pieces > 1 ? 1 : uint32_t(c.L < kMaxPiece / row_bytes ? c.L : kMaxPiece / row_bytes);
+    while (lg > 1 && tokens * ((c.L + lg - 1) / lg) < 8ull * gridDim.x)
+        lg = (lg + 1) / 2;
+    const uint32_t groups = (c.L + lg - 1) / lg;
+    const uint64_t units = tokens * groups * pieces;
+    const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
+    const uint64_t u0 = blockIdx.x * per, u1 = units < u0 + per ? units : u0 + per;
+    if (u0 >= u1)
+        return;
+    const uint32_t warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kSt; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    if (warp == 0) { // ---- loader ----
+        Walker wk;
+        wk.init(c, n_spans, u0, groups, pieces);
+        if (lane != 0)
+            return;
+        const uint64_t drop = c.fault[0], shift = c.fault[1]; // test hooks (off: ~0, 0)
+        uint32_t n = 0;
+        for (uint64_t next = u0; next < u1; ++next) {
+            const GSpan &sp = c.gspans[wk.cur];
+            const uint32_t l0 = wk.grp * lg, nl = min(lg, c.L - l0);
+            Move m = span_row(c, slots, sp, wk.tok_idx, l0);
+            if (drop != ~0ull && (wk.cur == drop || drop == KVR_FAULT_ALL))
+                m.dst = nullptr;
+            const uint32_t piece = wk.piece;
+            wk.advance(c, n_spans, groups, pieces);
+            if (!m.dst)
+                continue;
+            Unit u{};
+            const uint64_t off0 = uint64_t(piece) * kMaxPiece;
+            u.row = pieces > 1 ? uint32_t(row_bytes - off0 < kMaxPiece ? row_bytes - off0 : kMaxPiece) : uint32_t(row_bytes);
+            u.nl = nl;
+            u.dst0 = m.dst + off0;
+            if (shift && sp.kind == 0)
+                u.dst0 = shifted_row(c, u.dst0, shift);
+            u.dst_stride = (sp.kind == 0 ? uint64_t(c.Rp) : uint64_t(c.max_chunks)) * row_bytes;
+            u.mirror = sp.kind == 0 ? dst_mirror(c, u.dst0) : 0;
+            const int s = int(n % kSt);
+            if (n >= uint32_t(kSt))
+                mbar_wait(&empty[s], ((n / kSt) - 1) & 1u); // its previous stores have read it
+            info[s] = u;
+            mbar_expect_tx(&full[s], u.row * u.nl);
+            bulk_g2s(stage + size_t(s) * kMaxPiece, m.src + off0, u.row * u.nl, &full[s]);
+            ++n;
+        }
+        // end of the stream: an empty unit, announced without bytes
+        const int s = int(n % kSt);
+        if (n >= uint32_t(kSt))
+            mbar_wait(&empty[s], ((n / kSt) - 1) & 1u);
+        info[s].nl = 0;
+        asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&full[s])) : "memory");
+    } else if (lane == 0) { // ---- storer ----
+        for (uint32_t n = 0;; ++n) {
+            const int s = int(n % kSt);
+            mbar_wait(&full[s], (n / kSt) & 1u);
+            const Unit u = info[s];
+            if (!u.nl)
+                break;
+            for (uint32_t j = 0; j < u.nl; ++j) {
+                const uint8_t *from = stage + size_t(s) * kMaxPiece + size_t(j) * u.row;
+                bulk_s2g_nocommit(u.dst0 + j * u.dst_stride, from, u.row);
+                if (u.mirror)
+                    bulk_s2g_nocommit(u.dst0 + u.mirror + j * u.dst_stride, from, u.row);
+            }
+            bulk_commit();
+            // the previous unit's stores have read their stage: hand it back
+            if (n > 0) {
+                bulk_wait_read<1>();
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[(n - 1) % kSt]))
+                             : "memory");
+            }
+        }
+        bulk_wait_all();
+    }
+}
+
 // Register-staged variant: every warp of a full-occupancy grid moves (token, layer,
 // kUnit-byte piece) units, kFly of them in flight (all their loads before their
 // stores); each lane moves kUnit / 512 int4 of a unit. kInterleave: warp w takes
@@ -389,14 +491,15 @@ void launch_read_staged(const DevCtx &c, cudaStream_t s, uint64_t tok_begin, uin
 }
 
 namespace {
-// KVR_GATHER selects the K-gather kernel (A/B): tma (6 x 32 KiB stages, 4 loads
-// ahead, 1 CTA/SM; default) | tma5 (5 ahead) | tma2 (3 stages, 2 ahead, 2 CTAs/SM)
-// | vec (register-staged, 4 KiB units, 2 in flight) | ivec (interleaved)
+// KVR_GATHER selects the K-gather kernel (A/B): split (loader warp + storer warp, 6 x
+// 32 KiB stages, 1 CTA/SM; default) | tma (one lane loads and stores, 4 loads ahead) |
+// tma5 (5 ahead) | tma2 (3 stages, 2 ahead, 2 CTAs/SM) | vec (register-staged, 4 KiB
+// units, 2 in flight) | ivec (interleaved)
 int gather_kind() {
     static const int k = [] {
         const char *e = getenv("KVR_GATHER");
         const std::string v = e ? e : "";
-        return v == "tma5" ? 1 : v == "tma2" ? 2 : v == "vec" ? 3 : v == "ivec" ? 4 : 0;
+        return v == "tma" ? 0 : v == "tma5" ? 1 : v == "tma2" ? 2 : v == "vec" ? 3 : v == "ivec" ? 4 : 5;
     }();
     return k;
 }
@@ -408,6 +511,8 @@ cudaError_t prepare_gather(const DevCtx &) {
         e = cudaFuncSetAttribute(k_gather<6, 5>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(6 * kMaxPiece));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_gather<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(3 * kMaxPiece));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_gather2<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(6 * kMaxPiece));
     return e;
 }
 
@@ -417,6 +522,7 @@ void launch_gather(const DevCtx &c, cudaStream_t s, int sms) {
     case 2: k_gather<3, 2><<<sms * 2, 32, size_t(3) * kMaxPiece, s>>>(c); break;
     case 3: k_gather_vec<4096, 2, false><<<sms * 2, 32 * kVecWarps, 0, s>>>(c); break;
     case 4: k_gather_vec<4096, 2, true><<<sms * 2, 32 * kVecWarps, 0, s>>>(c); break;
+    case 5: k_gather2<6><<<sms, 64, size_t(6) * kMaxPiece, s>>>(c); break;
     default: k_gather<6, 4><<<sms, 32, size_t(6) * kMaxPiece, s>>>(c); break;
     }
 }
