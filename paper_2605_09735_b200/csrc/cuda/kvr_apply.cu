@@ -83,6 +83,45 @@ struct LaneTable {
 
 enum PayloadKind { kBytes = 0, kLanes16 = 1, kLanes32 = 2 };
 
+/// 2-byte lanes (B200 extension, kvo_fill_token_lanes): one splitmix64 per 8 lanes
+/// (16 bytes) of token `tok` of session `sid`, lane j = byte j of the hash.
+__device__ __forceinline__ uint64_t lanes16_hash(const DevCtx &c, uint32_t sid, uint64_t tok, uint64_t b0) {
+    return splitmix64(c.seed ^ (uint64_t(sid) << 32) ^ (tok << 8) ^ 0x4000000000000000ull ^ (b0 >> 4));
+}
+
+/// bf16 lanes: lane value (b - 128) / 2^shift, computed exactly in fp32 (byte_perm
+/// places b in the mantissa of 2^23 + b, one exact FFMA rescales) into f[8]; the value
+/// has <= 8 significant bits, so its upper 16 bits ARE the bf16 (round-to-nearest-even
+/// of an exact value): one PRMT packs two lanes (no F2FP + repack).
+__device__ __forceinline__ int4 lanes16_bf16(const DevCtx &c, uint64_t x, float f[8]) {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);
+        f[2 * i] = fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | k)), c.lane_scale, -c.lane_bias);
+        f[2 * i + 1] =
+            fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | (k + 1))), c.lane_scale, -c.lane_bias);
+        w[i] = __byte_perm(__float_as_uint(f[2 * i]), __float_as_uint(f[2 * i + 1]), 0x7632);
+    }
+    return make_int4(int(w[0]), int(w[1]), int(w[2]), int(w[3]));
+}
+
+/// fp16 lanes: byte b as the half 1024 + b (bits 0x64bb: one PRMT builds two lanes),
+/// then ONE exact HFMA2: (1024 + b) * 2^-s - 1152 * 2^-s = (b - 128) * 2^-s.
+__device__ __forceinline__ int4 lanes16_f16(const DevCtx &c, uint64_t x) {
+    const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
+    uint32_t w[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);
+        const uint32_t pair = __byte_perm(src, 0x6464u, 0x4040u | k | ((k + 1) << 8));
+        const __half2 v = __hfma2(*reinterpret_cast<const __half2 *>(&pair), c.lane_h2_scale, c.lane_h2_bias);
+        w[i] = *reinterpret_cast<const uint32_t *>(&v);
+    }
+    return make_int4(int(w[0]), int(w[1]), int(w[2]), int(w[3]));
+}
+
 // 16 payload bytes starting at byte `b0` of token `tok` of session `sid`.
 template <int kKind>
 __device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab, uint32_t sid, uint64_t tok,
@@ -95,40 +134,12 @@ __device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab,
         for (int i = 0; i < 4; ++i)
             w[i] = tab(splitmix64(base ^ (lane0 + i)));
     } else if constexpr (kKind == kLanes16) {
-        // 2-byte lanes (B200 extension, kvo_fill_token_lanes): one splitmix64 per
-        // 8 lanes (16 bytes), lane j = byte j: (b - 128) / 2^shift, exact in fp16 / bf16
-        // (arithmetic, no table: byte_perm places byte b in the mantissa of 2^23 + b,
-        // one exact FFMA maps it to (b - 128) / 2^shift, and a pack converts two lanes)
-        const uint64_t x = splitmix64(base ^ 0x4000000000000000ull ^ (b0 >> 4));
-        const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
-        const bool bf = c.elem_kind == KVR_ELEM_BF16;
-        if (!bf) {
-            // fp16: byte b as the half 1024 + b (bits 0x64bb: one PRMT builds two lanes),
-            // then ONE exact HFMA2: (1024 + b) * 2^-s - 1152 * 2^-s = (b - 128) * 2^-s
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-                const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);
-                const uint32_t pair = __byte_perm(src, 0x6464u, 0x4040u | k | ((k + 1) << 8));
-                const __half2 v = __hfma2(*reinterpret_cast<const __half2 *>(&pair), c.lane_h2_scale,
-                                          c.lane_h2_bias);
-                w[i] = *reinterpret_cast<const uint32_t *>(&v);
-            }
-            return make_int4(int(w[0]), int(w[1]), int(w[2]), int(w[3]));
+        const uint64_t x = lanes16_hash(c, sid, tok, b0);
+        if (c.elem_kind == KVR_ELEM_BF16) {
+            float f[8];
+            return lanes16_bf16(c, x, f);
         }
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const uint32_t src = i < 2 ? lo : hi, k = 2 * (i & 1);
-            const float v0 = fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | k)), c.lane_scale, -c.lane_bias);
-            const float v1 =
-                fmaf(__uint_as_float(__byte_perm(src, 0x4B000000u, 0x7440 | (k + 1))), c.lane_scale, -c.lane_bias);
-            if (bf) {
-                const __nv_bfloat162 p = __floats2bfloat162_rn(v0, v1);
-                w[i] = *reinterpret_cast<const uint32_t *>(&p);
-            } else {
-                const __half2 p = __floats2half2_rn(v0, v1);
-                w[i] = *reinterpret_cast<const uint32_t *>(&p);
-            }
-        }
+        return lanes16_f16(c, x);
     } else { // reference byte pattern: one splitmix per byte
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -408,9 +419,21 @@ template <int kKind> __device__ __forceinline__ void presum_body(const DevCtx &c
         // the same double as the reference's double sum (far_view.cpp:36-46), without
         // a conversion and an FP64 add per lane per row
         float accf[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        const bool bf = kKind == kLanes16 && c.elem_kind == KVR_ELEM_BF16;
         for (uint32_t r = op.run_begin; r < op.run_begin + op.run_count; ++r) {
             const kvr_presum_run run = runs[r];
             uint8_t *dst = c.arena + uint64_t(run.block) * c.page_bytes + uint64_t(run.slot) * c.token_bytes + 16 * col;
+            if (bf) { // bf16 lanes: the generator's exact fp32 values feed the sum directly
+                for (uint32_t k = 0; k < run.count; ++k) {
+                    float f[8];
+                    const int4 v = lanes16_bf16(c, lanes16_hash(c, op.session, run.token + k, 16 * col), f);
+                    *reinterpret_cast<int4 *>(dst + uint64_t(k) * c.token_bytes) = v;
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+                        accf[i] += f[i];
+                }
+                continue;
+            }
             for (uint32_t k = 0; k < run.count; ++k) {
                 const int4 v = payload16<kKind>(c, tab, op.session, run.token + k, 16 * col);
                 *reinterpret_cast<int4 *>(dst + uint64_t(k) * c.token_bytes) = v;
@@ -418,9 +441,7 @@ template <int kKind> __device__ __forceinline__ void presum_body(const DevCtx &c
                     const uint32_t w[4] = {uint32_t(v.x), uint32_t(v.y), uint32_t(v.z), uint32_t(v.w)};
 #pragma unroll
                     for (int i = 0; i < 4; ++i) {
-                        const float2 f = c.elem_kind == KVR_ELEM_BF16
-                                             ? __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w[i]))
-                                             : __half22float2(*reinterpret_cast<const __half2 *>(&w[i]));
+                        const float2 f = __half22float2(*reinterpret_cast<const __half2 *>(&w[i]));
                         accf[2 * i] += f.x, accf[2 * i + 1] += f.y;
                     }
                 } else {

@@ -3,6 +3,8 @@
 // (read + write) figure. Two variants over a buffer far larger than L2:
 //   ldg  — 16-byte vector loads, 8 in flight per thread, grid = 4 x #SMs x 512 threads
 //   tma  — cp.async.bulk global->shared, 4 x 48 KiB stages per CTA, one CTA per SM
+//   stg  — write stream: 16-byte streaming stores, same grid as ldg (the ceiling of the
+//          cold prompt writers K-write / K-presum, which only write)
 // nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o read_peak scripts/read_peak.cu
 #include <cstdio>
 #include <cstdint>
@@ -27,6 +29,13 @@ __global__ void __launch_bounds__(512) ldg(const int4 *__restrict__ p, size_t n,
     }
     if (acc == 0x7fffffff)
         *sink = acc;
+}
+
+__global__ void __launch_bounds__(512) stg(int4 *__restrict__ p, size_t n) {
+    const size_t stride = size_t(gridDim.x) * blockDim.x;
+    const int4 v = make_int4(int(threadIdx.x), int(blockIdx.x), 1, 2);
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += stride)
+        __stcs(p + i, v);
 }
 
 constexpr int kStages = 4;
@@ -92,12 +101,14 @@ int main() {
     cudaEvent_t a, b;
     cudaEventCreate(&a);
     cudaEventCreate(&b);
-    for (int v = 0; v < 2; ++v) {
+    for (int v = 0; v < 3; ++v) {
         float best = 1e30f;
         for (int it = 0; it < 6; ++it) {
             cudaEventRecord(a);
             if (v == 0)
                 ldg<<<4 * sms, 512>>>(reinterpret_cast<const int4 *>(p), bytes / 16, sink);
+            else if (v == 2)
+                stg<<<4 * sms, 512>>>(reinterpret_cast<int4 *>(p), bytes / 16);
             else
                 tma<<<sms, 32, kStages * kChunk>>>(p, bytes, sink);
             cudaEventRecord(b);
@@ -107,8 +118,9 @@ int main() {
             if (it > 0 && ms < best)
                 best = ms;
         }
-        std::printf("{\"variant\": \"%s\", \"bytes\": %zu, \"ms\": %.4f, \"read_gbs\": %.1f}\n", v ? "tma" : "ldg",
-                    bytes, best, bytes / (best * 1e6));
+        std::printf("{\"variant\": \"%s\", \"bytes\": %zu, \"ms\": %.4f, \"%s\": %.1f}\n",
+                    v == 0 ? "ldg" : v == 1 ? "tma" : "stg", bytes, best, v == 2 ? "write_gbs" : "read_gbs",
+                    bytes / (best * 1e6));
     }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
