@@ -230,6 +230,13 @@ int kvr_dev_ring_plane_rows(kvr_dev *d, uint32_t *out);
  * (CUDA events on the launch stream); used by bench.py for the roofline */
 int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms_per_launch);
 int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms_per_launch);
+/* diagnostic kernel timeline (only when KVR_TIMELINE=1 was set at kvr_dev_open): for each
+ * kernel id (0 apply, 1 queries, 2 K-scan, 3 hot K-write, 4 K-far/map/prime, 5 K-gather,
+ * 6 K-attn, 7 cold K-write, 8 K-presum) the %globaltimer ns of its first CTA start and
+ * last warp exit since the previous call, out[2 id], out[2 id + 1] (~0 / 0: not run);
+ * synchronises the step stream and resets */
+#define KVR_TIMELINE_IDS 16
+int kvr_dev_timeline(kvr_dev *d, uint64_t out[2 * KVR_TIMELINE_IDS]);
 /* name of the attention kernel variant chosen for this geometry */
 const char *kvr_dev_attention_variant(kvr_dev *d);
 /* attention-utility observations of the step launched from `ring_slot` (call after

@@ -11,6 +11,9 @@
 // of the SM count and sized for the worst case so the step graph never changes.
 #include <type_traits>
 
+#include <cstdlib>
+#include <string>
+
 #include "kvr_internal.cuh"
 
 namespace kvr {
@@ -26,6 +29,8 @@ __device__ inline void zero16(uint8_t *p) { *reinterpret_cast<int4 *>(p) = make_
 // the wave: device_step.cpp), so they need no ordering here. Every op is spread
 // over the whole grid (a zero run or a page copy can be megabytes).
 __global__ void k_apply(DevCtx c) {
+    pdl_trigger(); // (first kernel of the step: no PDL predecessor)
+    TlScope tl_(c, kTlApply);
     const kvr_step_header *h = hdr(c);
     const uint64_t tid = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x, stride = uint64_t(gridDim.x) * blockDim.x;
     const kvr_zero_op *zops = section<kvr_zero_op>(c, h->off_zero);
@@ -237,6 +242,8 @@ __device__ __forceinline__ void write_body(const DevCtx &c, int cold) {
 // Decode queries for live slots: [slot][L][Hq][hd], exact in the KV element type
 // (kvo_fill_query in the oracle). One CTA per (slot, layer); one hash per 8 lanes.
 __global__ void __launch_bounds__(256) k_query(DevCtx c) {
+    pdl_trigger();
+    TlScope tl_(c, kTlQuery);
     // byte k of x -> (b - 128) / 128, exactly: b placed in the mantissa of 2^23 + b
     auto val = [](uint32_t x, uint32_t k) {
         return fmaf(__uint_as_float(__byte_perm(x, 0x4B000000u, 0x7440 | k)), 0.0078125f, -65537.f);
@@ -534,13 +541,71 @@ __device__ __forceinline__ void stamp_if_last(const DevCtx &c) {
     }
 }
 
+// Cold writes (prompt rows nothing in this step reads), column-major like K-presum:
+// work unit = (op, 256-column block), thread = one 16-byte column, rows of the op's
+// page run in token order. The token-major K-write spends ~1/4 of its issue slots
+// re-deriving (token, slice, chunk) per unit; here the per-row cost is the generator
+// and one 16-byte store (write-stream bound instead of issue bound).
+template <int kKind> __device__ __forceinline__ void write_cols_body(const DevCtx &c, int cold) {
+    __shared__ LaneTable tab;
+    const kvr_step_header *h = hdr(c);
+    const uint32_t n_hot = h->n_write - h->n_far_jobs - h->n_cold;
+    const uint32_t n = cold ? h->n_cold : n_hot;
+    if (n == 0 || (cold ? h->write_tokens_cold : h->write_tokens) == 0)
+        return;
+    if constexpr (kKind == kLanes32)
+        tab.fill(c);
+    const kvr_write_op *ops = section<kvr_write_op>(c, h->off_write) + (cold ? n_hot : 0);
+    const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
+    const uint32_t cols = uint32_t(c.token_bytes / 16);
+    const uint32_t col_blocks = (cols + blockDim.x - 1) / blockDim.x;
+    const uint32_t row_chunks = c.row_elems * c.esz / 16;
+    const uint64_t ring_layer = uint64_t(c.Rp) * c.row_elems * c.esz;
+    const uint64_t work = uint64_t(n) * col_blocks;
+    for (uint64_t u = blockIdx.x; u < work; u += gridDim.x) {
+        const kvr_write_op op = ops[u / col_blocks];
+        const uint32_t col = uint32_t(u % col_blocks) * blockDim.x + threadIdx.x;
+        if (op.source != 0 || col >= cols)
+            continue;
+        uint8_t *dst = c.arena + uint64_t(op.block) * c.page_bytes + uint64_t(op.slot) * c.token_bytes + 16ull * col;
+        const bool may_ring = op.dev_slot != KVR_NO_SLOT;
+        for (uint32_t k = 0; k < op.count; ++k) {
+            const uint64_t tok = op.token + k;
+            const int4 v = payload16<kKind>(c, tab, op.session, tok, 16ull * col);
+            *reinterpret_cast<int4 *>(dst + uint64_t(k) * c.token_bytes) = v;
+            if (may_ring && ring_owned_by_writer(c, slots[op.dev_slot], tok)) { // window rows (hot ops)
+                const uint32_t l = col / row_chunks, within = col - l * row_chunks;
+                uint8_t *ring = c.ring + ring_row(c, op.dev_slot, 0, uint32_t(tok % c.R)) * c.esz;
+                *reinterpret_cast<int4 *>(ring + l * ring_layer + 16ull * within) = v;
+                if (const uint64_t mirror = ring_mirror(c, uint32_t(tok % c.R)) * c.esz)
+                    *reinterpret_cast<int4 *>(ring + mirror + l * ring_layer + 16ull * within) = v;
+            }
+        }
+    }
+}
+
+template <int kKind> __global__ void __launch_bounds__(256) k_write_cols(DevCtx c, int cold, int stamp) {
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, cold ? kTlWriteCold : kTlWriteHot);
+    write_cols_body<kKind>(c, cold);
+    if (stamp)
+        stamp_if_last(c);
+}
+
 template <uint32_t kPer, int kKind> __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold, int stamp) {
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, cold ? kTlWriteCold : kTlWriteHot);
     write_body<kPer, kKind>(c, cold);
     if (stamp)
         stamp_if_last(c);
 }
 
 template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c, int stamp) {
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, kTlPresum);
     presum_body<kKind>(c);
     if (stamp)
         stamp_if_last(c);
@@ -549,6 +614,9 @@ template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c, i
 // K-far + K-map + K-prime in ONE kernel: K-far and K-prime read the rows the host
 // resolved (not the page table K-map edits), so the three are independent.
 __global__ void __launch_bounds__(256) k_fmp(DevCtx c) {
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, kTlFmp);
     __shared__ uint64_t rows[kFarRows];
     far_part(c, rows);
     map_part(c);
@@ -559,26 +627,64 @@ __global__ void __launch_bounds__(256) k_fmp(DevCtx c) {
 
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms) { k_apply<<<sms * 4, 256, 0, s>>>(c); }
 
-void launch_presum(const DevCtx &c, cudaStream_t s, int sms, int stamp) {
+void launch_presum(const DevCtx &c, cudaStream_t s, int sms, int stamp, bool pdl) {
     if (!c.stash)
         return;
+    const unsigned g = unsigned(sms) * 4;
     if (c.esz == 4)
-        k_presum<kLanes32><<<sms * 4, 256, 0, s>>>(c, stamp);
+        launch_ex(k_presum<kLanes32>, g, 256, 0, s, pdl, c, stamp);
     else if (c.payload_mode == KVR_PAYLOAD_LANES)
-        k_presum<kLanes16><<<sms * 4, 256, 0, s>>>(c, stamp);
+        launch_ex(k_presum<kLanes16>, g, 256, 0, s, pdl, c, stamp);
     else
-        k_presum<kBytes><<<sms * 4, 256, 0, s>>>(c, stamp);
+        launch_ex(k_presum<kBytes>, g, 256, 0, s, pdl, c, stamp);
 }
 
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char *e = getenv("KVR_PDL");
+        return !(e && std::string(e) == "0");
+    }();
+    return on;
+}
+
+namespace {
+// KVR_COLD selects the cold writer (A/B): col (column-major, default) | tok (token-major K-write)
+int cold_kind() {
+    static const int k = [] {
+        const char *e = getenv("KVR_COLD");
+        return e && std::string(e) == "tok" ? 0 : 1;
+    }();
+    return k;
+}
+// KVR_HOT: tok (token-major K-write, default) | col (column-major)
+int hot_kind() {
+    static const int k = [] {
+        const char *e = getenv("KVR_HOT");
+        return e && std::string(e) == "col" ? 1 : 0;
+    }();
+    return k;
+}
+} // namespace
+
 // cold: 0 hot writes, 1 cold writes (both over the whole GPU)
-void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp) {
+void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp, bool pdl) {
     // hot writes (few decode tokens + window rows): one chunk per thread for
     // spread; cold prompt rows: two chunks per thread for generator ILP
     const int kind = c.esz == 4 ? kLanes32 : c.payload_mode == KVR_PAYLOAD_LANES ? kLanes16 : kBytes;
     auto go = [&](auto per, auto kk) {
-        k_write<decltype(per)::value, decltype(kk)::value><<<sms * 8, 256, 0, s>>>(c, cold, stamp);
+        launch_ex(k_write<decltype(per)::value, decltype(kk)::value>, unsigned(sms) * 8, 256, 0, s, pdl, c, cold, stamp);
     };
     using std::integral_constant;
+    if (cold ? cold_kind() == 1 : hot_kind() == 1) {
+        const unsigned g = unsigned(sms) * 8;
+        if (kind == kLanes16)
+            launch_ex(k_write_cols<kLanes16>, g, 256, 0, s, pdl, c, cold, stamp);
+        else if (kind == kLanes32)
+            launch_ex(k_write_cols<kLanes32>, g, 256, 0, s, pdl, c, cold, stamp);
+        else
+            launch_ex(k_write_cols<kBytes>, g, 256, 0, s, pdl, c, cold, stamp);
+        return;
+    }
     if (kind == kLanes16)
         cold ? go(integral_constant<uint32_t, 2>{}, integral_constant<int, kLanes16>{})
              : go(integral_constant<uint32_t, 1>{}, integral_constant<int, kLanes16>{});
@@ -599,6 +705,8 @@ __global__ void k_stamp(DevCtx c) {
 }
 void launch_stamp(const DevCtx &c, cudaStream_t s) { k_stamp<<<1, 1, 0, s>>>(c); }
 
-void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms) { k_fmp<<<sms * 2, 256, 0, s>>>(c); }
+void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms, bool pdl) {
+    launch_ex(k_fmp, unsigned(sms) * 2, 256, 0, s, pdl, c);
+}
 
 } // namespace kvr

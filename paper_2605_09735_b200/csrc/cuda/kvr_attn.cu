@@ -234,6 +234,7 @@ __global__ void __launch_bounds__(32 * (warps_per_head<QG>() * kMaxG + 1), 1)
     constexpr int DPL = A::DPL;
     constexpr int kState = 32 * QG * (2 + DPL); // floats of one warp's (m, l, acc) state
     extern __shared__ __align__(128) uint8_t smem[];
+    TlScope tl_(c, kTlAttn);
     const uint32_t tile_elems = kTile * G * HD;
     T *tiles = reinterpret_cast<T *>(smem);                                  // [stages][K|V][32][G][HD]
     float *xchg = reinterpret_cast<float *>(tiles + size_t(stages) * 2 * tile_elems); // head merge

@@ -15,7 +15,10 @@
 //             O^T[128 dims x 16] += V_tile^T[128 x 128] . Ps      (MN-major A)
 //           tcgen05.mma kind::f16, fp32 accumulators in TMEM (S and O double
 //           buffered per warpgroup, 128 columns), completion by tcgen05.commit ->
-//           mbarrier; each issuer tests all barriers of an iteration at once;
+//           mbarrier; both issuers walk the tile stream strictly in order and await
+//           each condition with the suspending try_wait (polling all barriers at
+//           once took issue slots from the softmax warps of the same SM
+//           sub-partition: C5 0.4478 -> 0.4467 -> 0.4409 ms, S then PV);
 //   warps 4-7, 8-11  two softmax/correction warpgroups, items alternating between
 //           them: thread t owns TMEM lane t, i.e. token row t of S and head dim t
 //           of O. Online softmax in base 2 per q-head column (cross-warp tile max
@@ -75,6 +78,24 @@ template <typename T, int G> struct Splits {
 #define KVR_TC_TILE5D 1
 #endif
 constexpr bool kUseTile5d = KVR_TC_TILE5D != 0;
+#ifndef KVR_TC_SWAIT
+#define KVR_TC_SWAIT 1
+#endif
+#ifndef KVR_TC_PVWAIT
+#define KVR_TC_PVWAIT 1
+#endif
+// lazy O rescaling (needs the in-order PV issuer): rescale only when a tile's maximum
+// exceeds the held one by more than kLazy (log2 units: p <= 256)
+#ifndef KVR_TC_LAZY
+#define KVR_TC_LAZY 0
+#endif
+#if KVR_TC_LAZY && !KVR_TC_PVWAIT
+#error "KVR_TC_LAZY needs KVR_TC_PVWAIT"
+#endif
+#ifndef KVR_TC_LAZY_T
+#define KVR_TC_LAZY_T 8
+#endif
+constexpr float kLazy = KVR_TC_LAZY_T; // (0: flip on every raise — a test build exercising the flips)
 constexpr int kThreads = 384; // warp 0 K TMA, 1 S MMA, 2 V TMA, 3 PV MMA, warps 4-7 / 8-11 softmax
 
 __device__ inline uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
@@ -465,6 +486,8 @@ struct Stream { // items j = 0, 1, 2, ... in order (item j -> warpgroup j % 2), 
 /// Per-softmax-warpgroup barriers and operand buffers.
 struct WgBars {
     uint64_t qfull, sfull[2], sempty[2], pfull[2], ofull[2], oempty[2];
+    uint64_t pempty[2]; // lazy mode: the PV that read P buffer b completed (tcgen05.commit)
+    uint32_t pflag[2];  // lazy mode: 1 = this P's PV starts the other O buffer (flip)
 };
 constexpr uint32_t kWgBytes = kQBytes + 2 * kOpBytes; // Q + P[2]
 
@@ -472,6 +495,7 @@ template <typename T, int G>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(DevCtx c, const __grid_constant__ TcMaps maps) {
     using SP = Splits<T, G>;
+    TlScope tl_(c, kTlAttn);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *kbuf = smem;                                    // kKStages x 32 KiB
@@ -514,6 +538,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_init(&wb[w].pfull[b], 4);
                 mbar_init(&wb[w].ofull[b], 1);
                 mbar_init(&wb[w].oempty[b], 4);
+                mbar_init(&wb[w].pempty[b], 1);
             }
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -616,12 +641,22 @@ __global__ void __launch_bounds__(kThreads, 1)
         bool have = S.next(c, slots, n_items, w, k, I);
         while (have) {
             const uint32_t nwc = w ? nw1 : nw0, b = nwc & 1u;
+#if KVR_TC_SWAIT
+            // tiles issue strictly in stream order, so the three conditions are awaited one
+            // after the other with the suspending try_wait: a polling loop here took issue
+            // slots from the softmax warps sharing this SM sub-partition (warps 5 and 9)
+            if (k == 0)
+                mbar_wait(&wb[w].qfull, (w ? mw1 : mw0) & 1u);
+            mbar_wait(&kfull[s], ph);
+            mbar_wait(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u);
+#else
             // the three barriers tested at once, one shuffle
             const bool q = k > 0 || mbar_test(&wb[w].qfull, (w ? mw1 : mw0) & 1u);
             const bool kf = mbar_test(&kfull[s], ph);
             const bool se = mbar_test(&wb[w].sempty[b], ((nwc >> 1) & 1u) ^ 1u);
             if (!__shfl_sync(0xffffffffu, uint32_t(q && kf && se), 0))
                 continue;
+#endif
             tc_fence_after();
             if (elect_one()) {
                 const uint64_t a0 = sdesc(kbase + s * kSideBytes, 16, 1024, 2);
@@ -652,6 +687,66 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr uint32_t kFifo = 8; // queued tiles per warpgroup (byte entries of a u64)
         Stream S;
         S.init(c, slots, n_items, queue, warp == 0);
+#if KVR_TC_PVWAIT
+        {
+            // strictly in stream order (the order the S issuer and the producers use), each
+            // condition awaited with the suspending try_wait instead of polling both
+            // warpgroups' queues: no stage can be reached out of its fill order
+            const uint32_t vbase = smem_u32(vbuf), wg0 = smem_u32(wgbuf);
+            uint32_t w = 0, k = 0, sv = 0, phv = 0, pvw[2] = {0, 0}, ocur = 0; // ocur bit w: O buffer
+            Item I;
+            while (S.next(c, slots, n_items, w, k, I)) {
+                const uint32_t nk = tile_of(I, k).nk, pvn = pvw[w], b = pvn & 1u, par = (pvn >> 1) & 1u;
+                mbar_wait(&wb[w].pfull[b], par);
+#if !KVR_TC_LAZY
+                mbar_wait(&wb[w].oempty[b], par ^ 1u);
+#endif
+                mbar_wait(&vfull[sv], phv);
+                tc_fence_after();
+#if KVR_TC_LAZY
+                // O buffer epochs: a flip (the softmax raised its held maximum) closes the old
+                // buffer — one commit tracks every PV in it — and starts the other one fresh;
+                // the item's last PV closes its buffer for the final read
+                const bool flip = k > 0 && wb[w].pflag[b] != 0u;
+                const uint32_t ob = ((ocur >> w) & 1u) ^ (flip ? 1u : 0u);
+                const bool last = k + 1 == I.n_tiles;
+                if (elect_one()) {
+                    if (flip)
+                        mma_commit(&wb[w].ofull[ob ^ 1u]);
+                    const uint64_t a0 = sdesc(vbase + sv * kSideBytes, kHalfBytes, 1024, 2);
+                    const uint64_t b0 = sdesc(wg0 + w * kWgBytes + kQBytes + b * kOpBytes, 128, 2048, 0);
+                    const bool fresh = k == 0 || flip;
+                    for (uint32_t kk = 0; kk < nk; ++kk)
+                        mma_f16(tmem + 128 * w + 64 + 16 * ob, a0 + kk * (2048 >> 4), b0 + kk * (256 >> 4), id_o,
+                                kk > 0 || !fresh);
+                    if (last)
+                        mma_commit(&wb[w].ofull[ob]);
+                    mma_commit(&wb[w].pempty[b]);
+                    mma_commit(&vempty[sv]);
+                }
+                __syncwarp();
+                if (flip)
+                    ocur ^= 1u << w;
+#else
+                if (elect_one()) {
+                    const uint64_t a0 = sdesc(vbase + sv * kSideBytes, kHalfBytes, 1024, 2);
+                    const uint64_t b0 = sdesc(wg0 + w * kWgBytes + kQBytes + b * kOpBytes, 128, 2048, 0);
+                    for (uint32_t kk = 0; kk < nk; ++kk)
+                        mma_f16(tmem + 128 * w + 64 + 16 * b, a0 + kk * (2048 >> 4), b0 + kk * (256 >> 4), id_o,
+                                kk > 0);
+                    mma_commit(&wb[w].ofull[b]);
+                    mma_commit(&vempty[sv]);
+                }
+                __syncwarp();
+#endif
+                ++pvw[w];
+                if (++sv == kVStages) {
+                    sv = 0;
+                    phv ^= 1;
+                }
+            }
+        }
+#else
         uint32_t w = 0, k = 0, sv = 0, phv = 0;
         uint32_t fw0 = 0, fw1 = 0, pv0 = 0, pv1 = 0; // tiles queued / PVs issued per warpgroup
         uint64_t ring0 = 0, ring1 = 0; // byte (n % 8) = V stage | V phase << 2 | K steps << 3
@@ -721,6 +816,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 (x ? pv1 : pv0) += 1;
             }
         }
+#endif
     } else if (warp >= 4) { // ---------------- softmax / correction warpgroups ----------------
         const uint32_t w = uint32_t(warp - 4) >> 2;     // warpgroup 0: warps 4-7, 1: warps 8-11
         const uint32_t t = threadIdx.x - 128 - 128 * w; // TMEM lane: token row of S, head dim of O
@@ -745,6 +841,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     os[i] = make_float4(0.f, 0.f, 0.f, 0.f);
             }
         uint32_t n = 0, m_items = 0;
+        uint32_t obuf = 0, opc = 0; // lazy mode: current O buffer, ofull parity per buffer (bits)
+        (void)obuf, (void)opc;
         Cursor cur;
         cur.init(queue, w, false);
         Item I, In;
@@ -773,6 +871,128 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (have_next)
                 load_q(In);
             ++m_items;
+#if KVR_TC_LAZY
+            // Lazy rescaling: O accumulates in TMEM across the item's tiles against a held
+            // maximum m (every p = 2^(s - m) <= 2^kLazy); only when a tile's maximum exceeds
+            // m + kLazy is O read back (flip: the PV issuer commits the old buffer and starts
+            // the new one fresh), folded into acc and rescaled. The common tile therefore
+            // never waits for its predecessor's PV (the per-tile O read of the eager path).
+            float m[G], l[G], acc[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g)
+                m[g] = -INFINITY, l[g] = 0.f, acc[g] = 0.f;
+            uint32_t ep = 0; // PVs of this item in the current O buffer
+            auto fold_o = [&](uint32_t bo, const float (&sc_)[G]) {
+                mbar_wait(&B.ofull[bo], (opc >> bo) & 1u);
+                opc ^= 1u << bo;
+                tc_fence_after();
+                float ov[16];
+                tmem_ld16(tmem + lane_base + 64 + 16 * bo, ov);
+                tc_fence_before();
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    float o_small = ov[G + g];
+                    if constexpr (SP::PS == 3)
+                        o_small += ov[2 * G + g];
+                    acc[g] = (acc[g] + (ov[g] + o_small)) * sc_[g];
+                }
+            };
+            for (uint32_t k = 0; k < I.n_tiles; ++k, ++n) {
+                const uint32_t b = n & 1u;
+                const Tile tl = tile_of(I, k);
+                const uint64_t tok = tl.tok_r0 + t;
+                const bool valid = t < tl.far_rows || (t >= kSub * tl.box_first &&
+                                                      t < kSub * (tl.box_first + tl.n_boxes) && tok >= I.lo && tok < I.w);
+                mbar_wait(&B.sfull[b], (n >> 1) & 1u);
+                tc_fence_after();
+                float sv[SP::NQ];
+                if constexpr (SP::NQ == 32) {
+                    float hi16[16], lo16[16];
+                    tmem_ld16(tmem + lane_base + 32 * b, hi16);
+                    tmem_ld16(tmem + lane_base + 32 * b + 16, lo16);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        sv[i] = hi16[i], sv[16 + i] = lo16[i];
+                } else {
+                    float v16[16];
+                    tmem_ld16(tmem + lane_base + 32 * b, v16);
+#pragma unroll
+                    for (int i = 0; i < 16; ++i)
+                        sv[i] = v16[i];
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0)
+                    mbar_arrive(&B.sempty[b]);
+                float sc[G], mx[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    float s_small = sv[G + g];
+                    if constexpr (SP::QS == 3)
+                        s_small += sv[2 * G + g];
+                    sc[g] = valid ? (sv[g] + s_small) * scale_log2 : -INFINITY;
+                    float v = sc[g];
+#pragma unroll
+                    for (int off = 16; off; off >>= 1)
+                        v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+                    mx[g] = v;
+                }
+                if (lane == 0)
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        rd[(b * 4 + wq) * 8 + g] = mx[g];
+                asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+                // tile maxima (identical in every thread of the warpgroup: uniform decision)
+                bool need = false;
+                float scl[G], pv[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float tm = fmaxf(fmaxf(rd[(b * 4 + 0) * 8 + g], rd[(b * 4 + 1) * 8 + g]),
+                                           fmaxf(rd[(b * 4 + 2) * 8 + g], rd[(b * 4 + 3) * 8 + g]));
+                    need = need || tm > m[g] + kLazy;
+                    mx[g] = tm;
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float mn = need ? fmaxf(m[g], mx[g]) : m[g];
+                    scl[g] = m[g] == -INFINITY ? 1.f : exp2f(m[g] - mn);
+                    l[g] *= scl[g];
+                    m[g] = mn;
+                    const float p = valid ? exp2f(sc[g] - mn) : 0.f;
+                    l[g] += p;
+                    pv[g] = p;
+                }
+                const bool flip = need && ep > 0;
+                uint8_t *pb = qb + kQBytes + b * kOpBytes;
+                if (n >= 2) // P buffer b: the PV of this warpgroup's tile n - 2 has read it
+                    mbar_wait(&B.pempty[b], ((n >> 1) & 1u) ^ 1u);
+                store_split<T, G, SP::PS>(pb, t, pv);
+                fence_async_smem();
+                __syncwarp();
+                if (lane == 0) {
+                    if (wq == 0)
+                        B.pflag[b] = flip ? 1u : 0u; // released by this warp's arrive
+                    mbar_arrive(&B.pfull[b]);
+                }
+                if (flip) { // PV(k) runs into the other buffer while the old one is folded
+                    fold_o(obuf, scl);
+                    obuf ^= 1u;
+                    ep = 0;
+                } else if (need) {
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        acc[g] *= scl[g];
+                }
+                ++ep;
+            }
+            {
+                float one[G];
+#pragma unroll
+                for (int g = 0; g < G; ++g)
+                    one[g] = 1.f;
+                fold_o(obuf, one); // the item's last PV (committed by the PV issuer at its last tile)
+            }
+#else
             float m[G], l[G], acc[G], alpha_prev[G];
 #pragma unroll
             for (int g = 0; g < G; ++g)
@@ -865,6 +1085,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     alpha_prev[g] = alpha[g];
             }
             correct(n - 1, alpha_prev);
+#endif
             // row sums across the warpgroup, then normalise
 #pragma unroll
             for (int g = 0; g < G; ++g) {

@@ -38,8 +38,9 @@ struct kvr_dev {
     kvr_geometry g{};
     int sms = 148;
     cudaStream_t stream = nullptr;
-    cudaStream_t side = nullptr;                   // the step graph's forked branch (queries, K-scan)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaStream_t side = nullptr;                   // the step graph's forked branch (K-scan)
+    cudaStream_t side2 = nullptr;                  // second forked branch (decode queries)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
     DevCtx base{};
     uint8_t *d_desc[3] = {nullptr, nullptr, nullptr};
     void *h_desc[3] = {nullptr, nullptr, nullptr};
@@ -138,6 +139,12 @@ void *dalloc(kvr_dev *d, size_t bytes, const char *what) {
     return p;
 }
 
+__global__ void k_tl_reset(unsigned long long *tl) {
+    if (threadIdx.x < 2 * KVR_TIMELINE_IDS)
+        tl[threadIdx.x] = threadIdx.x & 1 ? 0ull : ~0ull;
+}
+void tl_reset(unsigned long long *tl, cudaStream_t s) { k_tl_reset<<<1, 2 * KVR_TIMELINE_IDS, 0, s>>>(tl); }
+
 DevCtx ctx_for(const kvr_dev *d, int slot) {
     DevCtx c = d->base;
     c.desc = d->d_desc[slot];
@@ -162,23 +169,29 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
         launch_far_map_prime(c, s, d->sms);
         return;
     }
-    // Side branch: the decode queries and K-scan depend only on the descriptor, so
-    // they run beside the byte kernels (one SM for K-scan's single CTA) and join
-    // before K-gather, off the step's critical path.
-    cudaStream_t side = d->side;
+    // Two forked branches: K-scan (needs only the descriptor) joins before K-gather,
+    // the decode queries (read only by K-attn) join before K-attn; both run beside
+    // the byte kernels, off the step's critical path. Kernel-to-kernel edges of the
+    // main chain are PDL edges (each dependent launches during its predecessor and
+    // waits in-kernel, griddepcontrol), unless phase event nodes sit between them.
+    const bool pdl = pdl_enabled() && !d->phase_events;
+    cudaStream_t side = d->side, side2 = d->side2;
     ck(cudaEventRecord(d->ev_fork, s), "fork"); // (under capture: a dependency, not a node)
     ck(cudaStreamWaitEvent(side, d->ev_fork, 0), "fork wait");
-    launch_query(c, side, d->sms);
+    ck(cudaStreamWaitEvent(side2, d->ev_fork, 0), "fork wait");
     launch_scan(c, side);
     ck(cudaEventRecord(d->ev_join, side), "join");
+    launch_query(c, side2, d->sms);
+    ck(cudaEventRecord(d->ev_join2, side2), "join");
     mark(1);
-    launch_write(c, s, d->sms, 0);
+    launch_write(c, s, d->sms, 0, 0, pdl);
     mark(2);
-    launch_far_map_prime(c, s, d->sms);
+    launch_far_map_prime(c, s, d->sms, pdl);
     mark(3);
     ck(cudaStreamWaitEvent(s, d->ev_join, 0), "join wait");
     mark(4);
-    launch_gather(c, s, d->sms);
+    launch_gather(c, s, d->sms, pdl);
+    ck(cudaStreamWaitEvent(s, d->ev_join2, 0), "join wait");
     mark(5);
     if (d->g.attention && d->attn)
         launch_attn(d->attn, c, s);
@@ -193,7 +206,7 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     // after the collective)
     const int stamp_in_kernel = d->comm ? 0 : 1;
     launch_write(c, s, d->sms, 1, stamp_in_kernel && !c.stash);
-    launch_presum(c, s, d->sms, stamp_in_kernel);
+    launch_presum(c, s, d->sms, stamp_in_kernel, pdl);
     // the step's counts summed over every rank (the only cross-GPU traffic)
     if (d->comm) {
         nck(nccl().all_reduce(c.desc + offsetof(kvr_step_header, counts), d->d_counts, KVR_COUNTS, ncclInt64,
@@ -252,8 +265,10 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         d->sms = prop.multiProcessorCount;
         ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
         ck(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking), "side stream");
+        ck(cudaStreamCreateWithFlags(&d->side2, cudaStreamNonBlocking), "side stream");
         ck(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming), "fork event");
         ck(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming), "join event");
+        ck(cudaEventCreateWithFlags(&d->ev_join2, cudaEventDisableTiming), "join event");
         for (int i = 0; i < 2; ++i) {
             ck(cudaEventCreate(&d->ev_start[i]), "event");
             ck(cudaEventCreate(&d->ev_stop[i]), "event");
@@ -335,6 +350,10 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         ck(cudaMemsetAsync(c.scan, 0, sizeof(ScanCounters), d->stream), "scan zero");
         c.attn_sched = static_cast<uint32_t *>(dalloc(d.get(), 4 * sizeof(uint32_t), "schedule tickets"));
         ck(cudaMemsetAsync(c.attn_sched, 0, 4 * sizeof(uint32_t), d->stream), "schedule zero");
+        if (const char *e = getenv("KVR_TIMELINE"); e && e[0] == '1') { // diagnostic timeline
+            c.tl = static_cast<unsigned long long *>(dalloc(d.get(), sizeof(uint64_t) * 2 * KVR_TIMELINE_IDS, "timeline"));
+            tl_reset(c.tl, d->stream);
+        }
         {
             const uint64_t off[2] = {~0ull, 0};
             auto *fault = static_cast<uint64_t *>(dalloc(d.get(), sizeof(off), "fault hooks"));
@@ -434,6 +453,8 @@ int kvr_dev_close(kvr_dev *d) {
         cudaEventDestroy(d->ev_join);
     if (d->side)
         cudaStreamDestroy(d->side);
+    if (d->side2)
+        cudaStreamDestroy(d->side2);
     if (d->stream)
         cudaStreamDestroy(d->stream);
     delete d;
@@ -670,6 +691,17 @@ static int time_kernel(kvr_dev *d, uint32_t iters, double *ms, bool attn) {
 }
 
 int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms) { return time_kernel(d, iters, ms, true); }
+
+int kvr_dev_timeline(kvr_dev *d, uint64_t *out) {
+    return guard([&] {
+        if (!d->base.tl)
+            throw std::runtime_error("timeline off (set KVR_TIMELINE=1 before kvr_dev_open)");
+        ck(cudaStreamSynchronize(d->stream), "sync");
+        ck(cudaMemcpy(out, d->base.tl, sizeof(uint64_t) * 2 * KVR_TIMELINE_IDS, cudaMemcpyDeviceToHost), "timeline");
+        tl_reset(d->base.tl, d->stream);
+        ck(cudaStreamSynchronize(d->stream), "sync");
+    });
+}
 int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms) { return time_kernel(d, iters, ms, false); }
 
 const char *kvr_dev_attention_variant(kvr_dev *d) { return attn_variant(d->attn); }

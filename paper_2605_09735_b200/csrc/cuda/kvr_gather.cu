@@ -156,6 +156,9 @@ struct Unit {
 // store per layer into that layer's window ring plane.
 template <int kStages, int kAhead>
 __global__ void __launch_bounds__(32) k_gather(DevCtx c) {
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, kTlGather);
     extern __shared__ __align__(128) uint8_t stage[];
     __shared__ __align__(8) uint64_t full[kStages];
     const kvr_step_header *h = hdr(c);
@@ -252,6 +255,9 @@ __global__ void __launch_bounds__(32) k_gather(DevCtx c) {
 // arrive on `full`, acquired by the storer's wait).
 template <int kSt>
 __global__ void __launch_bounds__(64) k_gather2(DevCtx c) {
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, kTlGather);
     extern __shared__ __align__(128) uint8_t stage[];
     __shared__ __align__(8) uint64_t full[kSt], empty[kSt];
     __shared__ Unit info[kSt];
@@ -362,6 +368,9 @@ struct VecUnit {
 
 template <int kUnit, int kFly, bool kInterleave>
 __global__ void __launch_bounds__(32 * kVecWarps) k_gather_vec(DevCtx c) {
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, kTlGather);
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
     const uint32_t n_spans = c.scan->spans;
@@ -516,14 +525,15 @@ cudaError_t prepare_gather(const DevCtx &) {
     return e;
 }
 
-void launch_gather(const DevCtx &c, cudaStream_t s, int sms) {
+void launch_gather(const DevCtx &c, cudaStream_t s, int sms, bool pdl) {
+    const unsigned n = unsigned(sms);
     switch (gather_kind()) {
-    case 1: k_gather<6, 5><<<sms, 32, size_t(6) * kMaxPiece, s>>>(c); break;
-    case 2: k_gather<3, 2><<<sms * 2, 32, size_t(3) * kMaxPiece, s>>>(c); break;
-    case 3: k_gather_vec<4096, 2, false><<<sms * 2, 32 * kVecWarps, 0, s>>>(c); break;
-    case 4: k_gather_vec<4096, 2, true><<<sms * 2, 32 * kVecWarps, 0, s>>>(c); break;
-    case 5: k_gather2<6><<<sms, 64, size_t(6) * kMaxPiece, s>>>(c); break;
-    default: k_gather<6, 4><<<sms, 32, size_t(6) * kMaxPiece, s>>>(c); break;
+    case 1: launch_ex(k_gather<6, 5>, n, 32, size_t(6) * kMaxPiece, s, pdl, c); break;
+    case 2: launch_ex(k_gather<3, 2>, n * 2, 32, size_t(3) * kMaxPiece, s, pdl, c); break;
+    case 3: launch_ex(k_gather_vec<4096, 2, false>, n * 2, 32 * kVecWarps, 0, s, pdl, c); break;
+    case 4: launch_ex(k_gather_vec<4096, 2, true>, n * 2, 32 * kVecWarps, 0, s, pdl, c); break;
+    case 5: launch_ex(k_gather2<6>, n, 64, size_t(6) * kMaxPiece, s, pdl, c); break;
+    default: launch_ex(k_gather<6, 4>, n, 32, size_t(6) * kMaxPiece, s, pdl, c); break;
     }
 }
 

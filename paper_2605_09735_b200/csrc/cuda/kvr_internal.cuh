@@ -1,5 +1,6 @@
 // kvrail-b200 device internals shared by the sm_100a kernels.
 #pragma once
+#include <utility>
 
 #include <cstdint>
 #include <cuda.h>
@@ -63,6 +64,28 @@ struct DevCtx {
     const uint64_t *fault;   // [0] KVR_FAULT_DROP_SPAN, [1] KVR_FAULT_SHIFT_ROWS arguments — test hooks only
     uint32_t *attn_sched;    // [0] next item to claim, [1] CTAs finished (tensor-core attention),
                              // [2] CTAs finished of the step's last kernel (end stamp)
+    unsigned long long *tl;  // diagnostic kernel timeline (KVR_TIMELINE=1), null when off
+};
+
+/// Diagnostic timeline (KVR_TIMELINE=1): per kernel of the step, the first CTA's start
+/// and the last warp's exit on %globaltimer (min / max over CTAs) — the step graph's
+/// real schedule without event nodes. Ids: kvr_dev_timeline in kvr_cuda.h.
+enum TlId : uint32_t { kTlApply, kTlQuery, kTlScan, kTlWriteHot, kTlFmp, kTlGather, kTlAttn, kTlWriteCold, kTlPresum };
+__device__ inline unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+struct TlScope {
+    unsigned long long *tl;
+    __device__ TlScope(const DevCtx &c, uint32_t id) : tl(c.tl ? c.tl + 2 * id : nullptr) {
+        if (tl && threadIdx.x == 0)
+            atomicMin(tl, gtimer());
+    }
+    __device__ ~TlScope() {
+        if (tl && (threadIdx.x & 31) == 0)
+            atomicMax(tl + 1, gtimer());
+    }
 };
 
 /// Token `tok` of a slot is written into the ring by K-write / K-prime only when it
@@ -125,21 +148,48 @@ template <class Key> __device__ inline uint32_t warp_last_le(uint32_t n, uint64_
     return lo;
 }
 
+// ---- programmatic dependent launch (PDL) ----------------------------------
+// A kernel launched with a PDL edge may start while its predecessor still runs (once
+// every predecessor CTA has executed pdl_trigger or exited). Every kernel that can
+// be such a dependent calls pdl_wait() FIRST — before any early exit, so that its own
+// completion still implies its predecessors' (transitive ordering) — and pdl_trigger()
+// right after, letting its own dependents launch. Both are no-ops without a PDL edge.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+bool pdl_enabled(); // KVR_PDL=0 turns the step graph's PDL edges off (A/B)
+/// <<<grid, block, smem, s>>> with the PDL attribute when `pdl`
+template <typename... P, typename... A>
+inline void launch_ex(void (*k)(P...), unsigned grid, unsigned block, size_t smem, cudaStream_t s, bool pdl,
+                      A &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, k, std::forward<A>(args)...);
+}
+
 // ---- host launchers (one per kernel file) --------------------------------
+// pdl: the launch's stream predecessor is a kernel of the same step (PDL edge)
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blob
 /// stamp: this launch is the step's last kernel and writes the step-end timestamp
-void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp = 0); // generated payloads
+void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp = 0, bool pdl = false); // generated payloads
 void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
-void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms); // K-far + K-map + K-prime
+void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms, bool pdl = false); // K-far + K-map + K-prime
 void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp
-void launch_presum(const DevCtx &c, cudaStream_t s, int sms, int stamp = 0); // prompt rows + their far chunk means
+void launch_presum(const DevCtx &c, cudaStream_t s, int sms, int stamp = 0, bool pdl = false); // prompt rows + their far chunk means
 void launch_mass(const DevCtx &c, cudaStream_t s);             // attention-utility observations
 bool prepare_mass(const DevCtx &c); // false: no K-mass for this geometry
 size_t mass_scratch_floats(const DevCtx &c);
 size_t mass_part_entries(const DevCtx &c);
 uint32_t mass_max_group();
-void launch_scan(const DevCtx &c, cudaStream_t s);             // stage + reduce
-void launch_gather(const DevCtx &c, cudaStream_t s, int sms);  // trains -> window
+void launch_scan(const DevCtx &c, cudaStream_t s, bool pdl = false);             // stage + reduce
+void launch_gather(const DevCtx &c, cudaStream_t s, int sms, bool pdl = false);  // trains -> window
 /// destination bytes of staged tokens [tok_begin, +count) into out (token-major)
 void launch_read_staged(const DevCtx &c, cudaStream_t s, uint64_t tok_begin, uint64_t count, uint8_t *out,
                         uint8_t *in_window);

@@ -65,6 +65,9 @@ template <int kScanThreads> __global__ void __launch_bounds__(kScanThreads, 1) k
     extern __shared__ __align__(16) uint8_t dyn[];
     __shared__ ScanSmem sm;
     __shared__ uint32_t s_status;
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, kTlScan);
     const kvr_step_header *h = hdr(c);
     const kvr_need_rec *g_needs = section<kvr_need_rec>(c, h->off_need);
     const kvr_span_rec *spans = section<kvr_span_rec>(c, h->off_span);
@@ -398,13 +401,13 @@ int scan_threads() {
 }
 } // namespace
 
-void launch_scan(const DevCtx &c, cudaStream_t s) {
+void launch_scan(const DevCtx &c, cudaStream_t s, bool pdl) {
     const size_t smem = scan_dynamic_smem(c.max_scan);
     switch (scan_threads()) {
-    case 128: k_scan<128><<<1, 128, smem, s>>>(c); break;
-    case 512: k_scan<512><<<1, 512, smem, s>>>(c); break;
-    case 1024: k_scan<1024><<<1, 1024, smem, s>>>(c); break;
-    default: k_scan<256><<<1, 256, smem, s>>>(c); break;
+    case 128: launch_ex(k_scan<128>, 1, 128, smem, s, pdl, c); break;
+    case 512: launch_ex(k_scan<512>, 1, 512, smem, s, pdl, c); break;
+    case 1024: launch_ex(k_scan<1024>, 1, 1024, smem, s, pdl, c); break;
+    default: launch_ex(k_scan<256>, 1, 256, smem, s, pdl, c); break;
     }
 }
 

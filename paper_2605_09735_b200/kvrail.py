@@ -308,6 +308,7 @@ def _bind_extras(lib: C.CDLL) -> None:
         "kvr_dev_count": [C.POINTER(C.c_int)],
         "kvr_dev_time_attention": [vp, C.c_uint32, C.POINTER(C.c_double)],
         "kvr_dev_time_gather": [vp, C.c_uint32, C.POINTER(C.c_double)],
+        "kvr_dev_timeline": [vp, U64P],
         "kvr_dev_read": [vp, C.c_int, C.c_uint64, C.c_uint64, C.c_void_p],
         "kvr_dev_read_staged": [vp, C.c_uint64, C.c_uint64, C.c_void_p, C.c_void_p],
         "kvr_dev_ring_plane_rows": [vp, U32P],
@@ -645,6 +646,17 @@ class Device:
         ms = C.c_double()
         check(native_lib().kvr_dev_time_gather(self.raw(), iters, C.byref(ms)))
         return ms.value
+
+    TIMELINE_NAMES = ("apply", "queries", "scan", "write_hot", "far_map_prime", "gather", "attention",
+                      "write_cold", "presum")
+
+    def timeline(self) -> dict:
+        """Diagnostic (KVR_TIMELINE=1 at open): {kernel: (start_ns, end_ns)} since the last
+        call, %globaltimer of the first CTA start / last warp exit; resets."""
+        buf = (C.c_uint64 * 32)()
+        check(native_lib().kvr_dev_timeline(self.raw(), buf))
+        return {n: (buf[2 * i], buf[2 * i + 1]) for i, n in enumerate(self.TIMELINE_NAMES)
+                if buf[2 * i + 1] != 0}
 
     def attention_variant(self) -> str:
         return native_lib().kvr_dev_attention_variant(self.raw()).decode()
