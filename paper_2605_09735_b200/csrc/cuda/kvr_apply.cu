@@ -11,6 +11,7 @@
 // of the SM count and sized for the worst case so the step graph never changes.
 #include <type_traits>
 
+#include <algorithm>
 #include <cstdlib>
 #include <string>
 
@@ -270,12 +271,26 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
             }
             continue;
         }
-        for (uint32_t i = threadIdx.x; i < per_layer / 8; i += blockDim.x) { // 8 lanes per hash
-            const uint32_t head = (8 * i) >> hd_shift, d8 = i & ((c.hd >> 3) - 1);
-            const uint64_t x = splitmix64(base ^ (uint64_t(head) << 8) ^ d8);
-            const uint32_t lo = uint32_t(x), hi = uint32_t(x >> 32);
-            q[2 * i] = make_float4(val(lo, 0), val(lo, 1), val(lo, 2), val(lo, 3));
-            q[2 * i + 1] = make_float4(val(hi, 0), val(hi, 1), val(hi, 2), val(hi, 3));
+        // 8 lanes per hash, four independent hashes per thread in flight (ILP: the
+        // splitmix chains overlap; one hash per iteration left the kernel latency-bound)
+        const uint32_t n8 = per_layer / 8;
+        for (uint32_t i0 = threadIdx.x; i0 < n8; i0 += 4 * blockDim.x) {
+            uint64_t x[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                const uint32_t head = (8 * i) >> hd_shift, d8 = i & ((c.hd >> 3) - 1);
+                x[u] = splitmix64(base ^ (uint64_t(head) << 8) ^ d8);
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t i = i0 + u * blockDim.x;
+                if (i >= n8)
+                    break;
+                const uint32_t lo = uint32_t(x[u]), hi = uint32_t(x[u] >> 32);
+                q[2 * i] = make_float4(val(lo, 0), val(lo, 1), val(lo, 2), val(lo, 3));
+                q[2 * i + 1] = make_float4(val(hi, 0), val(hi, 1), val(hi, 2), val(hi, 3));
+            }
         }
     }
 }
@@ -611,6 +626,19 @@ template <int kKind> __global__ void __launch_bounds__(256) k_presum(DevCtx c, i
         stamp_if_last(c);
 }
 
+// The step's tail in ONE kernel: the cold prompt rows (column-major) and K-presum's
+// chunks (disjoint rows) — one launch gap after K-attn instead of two.
+template <int kKind> __global__ void __launch_bounds__(256) k_tail(DevCtx c, int stamp) {
+    pdl_wait();
+    pdl_trigger();
+    TlScope tl_(c, kTlWriteCold); // (cold rows and K-presum: one span)
+    write_cols_body<kKind>(c, 1);
+    if (c.stash)
+        presum_body<kKind>(c);
+    if (stamp)
+        stamp_if_last(c);
+}
+
 // K-far + K-map + K-prime in ONE kernel: K-far and K-prime read the rows the host
 // resolved (not the page table K-map edits), so the three are independent.
 __global__ void __launch_bounds__(256) k_fmp(DevCtx c) {
@@ -625,7 +653,19 @@ __global__ void __launch_bounds__(256) k_fmp(DevCtx c) {
 
 } // namespace
 
-void launch_apply(const DevCtx &c, cudaStream_t s, int sms) { k_apply<<<sms * 4, 256, 0, s>>>(c); }
+// Grids of the small pre-attention kernels (x KVR_GRID_SCALE, default 2: apply 4,
+// hot K-write 8, queries 4 CTAs per SM). Timeline A/B on C5 (attention start after the
+// first kernel): scale 1 52.9 us (the queries branch took 28 us and crowded K-fmp),
+// scale 2 45.1 us, the previous grids (queries 8 per SM) 49.3 us.
+int grid_scale() {
+    static const int k = [] {
+        const char *e = getenv("KVR_GRID_SCALE");
+        return e ? std::max(1, atoi(e)) : 2;
+    }();
+    return k;
+}
+
+void launch_apply(const DevCtx &c, cudaStream_t s, int sms) { k_apply<<<sms * 2 * grid_scale(), 256, 0, s>>>(c); }
 
 void launch_presum(const DevCtx &c, cudaStream_t s, int sms, int stamp, bool pdl) {
     if (!c.stash)
@@ -671,12 +711,12 @@ void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp,
     // hot writes (few decode tokens + window rows): one chunk per thread for
     // spread; cold prompt rows: two chunks per thread for generator ILP
     const int kind = c.esz == 4 ? kLanes32 : c.payload_mode == KVR_PAYLOAD_LANES ? kLanes16 : kBytes;
+    const unsigned g = unsigned(sms) * (cold ? 8 : 4 * grid_scale());
     auto go = [&](auto per, auto kk) {
-        launch_ex(k_write<decltype(per)::value, decltype(kk)::value>, unsigned(sms) * 8, 256, 0, s, pdl, c, cold, stamp);
+        launch_ex(k_write<decltype(per)::value, decltype(kk)::value>, g, 256, 0, s, pdl, c, cold, stamp);
     };
     using std::integral_constant;
     if (cold ? cold_kind() == 1 : hot_kind() == 1) {
-        const unsigned g = unsigned(sms) * 8;
         if (kind == kLanes16)
             launch_ex(k_write_cols<kLanes16>, g, 256, 0, s, pdl, c, cold, stamp);
         else if (kind == kLanes32)
@@ -696,7 +736,22 @@ void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp,
              : go(integral_constant<uint32_t, 1>{}, integral_constant<int, kBytes>{});
 }
 
-void launch_query(const DevCtx &c, cudaStream_t s, int sms) { k_query<<<sms * 8, 256, 0, s>>>(c); }
+void launch_tail(const DevCtx &c, cudaStream_t s, int sms, int stamp, bool pdl) {
+    if (cold_kind() != 1) { // token-major cold K-write, then K-presum
+        launch_write(c, s, sms, 1, stamp && !c.stash, pdl);
+        launch_presum(c, s, sms, stamp, pdl);
+        return;
+    }
+    const unsigned g = unsigned(sms) * 8;
+    if (c.esz == 4)
+        launch_ex(k_tail<kLanes32>, g, 256, 0, s, pdl, c, stamp);
+    else if (c.payload_mode == KVR_PAYLOAD_LANES)
+        launch_ex(k_tail<kLanes16>, g, 256, 0, s, pdl, c, stamp);
+    else
+        launch_ex(k_tail<kBytes>, g, 256, 0, s, pdl, c, stamp);
+}
+
+void launch_query(const DevCtx &c, cudaStream_t s, int sms) { k_query<<<sms * 2 * grid_scale(), 256, 0, s>>>(c); }
 
 __global__ void k_stamp(DevCtx c) {
     uint64_t t;

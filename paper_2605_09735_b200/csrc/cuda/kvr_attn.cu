@@ -234,6 +234,9 @@ __global__ void __launch_bounds__(32 * (warps_per_head<QG>() * kMaxG + 1), 1)
     constexpr int DPL = A::DPL;
     constexpr int kState = 32 * QG * (2 + DPL); // floats of one warp's (m, l, acc) state
     extern __shared__ __align__(128) uint8_t smem[];
+    pdl_wait();
+    pdl_trigger();
+    AttnSpan span_(c);
     TlScope tl_(c, kTlAttn);
     const uint32_t tile_elems = kTile * G * HD;
     T *tiles = reinterpret_cast<T *>(smem);                                  // [stages][K|V][32][G][HD]
@@ -527,12 +530,12 @@ AttnPlan *make_attn_plan(const DevCtx &c, int sms, int device, int mode) {
     return p;
 }
 
-void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s) {
+void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s, bool pdl) {
     if (p->tc) {
-        launch_attn_tc(p->tc, c, p->tc_maps, p->grid, s);
+        launch_attn_tc(p->tc, c, p->tc_maps, p->grid, s, pdl);
         return;
     }
-    p->fn<<<p->grid, p->threads, p->smem, s>>>(c, p->map, p->edge_map, p->G, p->stages);
+    launch_ex(p->fn, p->grid, p->threads, p->smem, s, pdl, c, p->map, p->edge_map, p->G, p->stages);
 }
 
 void free_attn_plan(AttnPlan *p) { delete p; }

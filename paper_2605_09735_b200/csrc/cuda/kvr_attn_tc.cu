@@ -495,6 +495,9 @@ template <typename T, int G>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(DevCtx c, const __grid_constant__ TcMaps maps) {
     using SP = Splits<T, G>;
+    pdl_wait();
+    pdl_trigger();
+    AttnSpan span_(c);
     TlScope tl_(c, kTlAttn);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1204,8 +1207,8 @@ bool attn_tc_maps(const DevCtx &c, TcMaps *maps) {
            enc(&maps->far, 2, c.far, df, sf, bf);
 }
 
-void launch_attn_tc(const void *fn, const DevCtx &c, const TcMaps &maps, uint32_t grid, cudaStream_t s) {
-    reinterpret_cast<TcFn>(const_cast<void *>(fn))<<<grid, kThreads, attn_tc_smem(), s>>>(c, maps);
+void launch_attn_tc(const void *fn, const DevCtx &c, const TcMaps &maps, uint32_t grid, cudaStream_t s, bool pdl) {
+    launch_ex(reinterpret_cast<TcFn>(const_cast<void *>(fn)), grid, kThreads, attn_tc_smem(), s, pdl, c, maps);
 }
 
 } // namespace kvr

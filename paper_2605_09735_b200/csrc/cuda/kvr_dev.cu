@@ -40,7 +40,12 @@ struct kvr_dev {
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;                   // the step graph's forked branch (K-scan)
     cudaStream_t side2 = nullptr;                  // second forked branch (decode queries)
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+    // the step's copies run on their own streams, off the graph stream: the descriptor
+    // H2D of step t+1 overlaps step t's graph, the stats D2H of step t overlaps t+1's
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t ev_copied[2] = {}, ev_stats[2] = {};
+    ScanCounters *scans[2] = {}; // per ring slot: the D2H of step t never races t+1's K-scan
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_fork2 = nullptr, ev_join2 = nullptr;
     DevCtx base{};
     uint8_t *d_desc[3] = {nullptr, nullptr, nullptr};
     void *h_desc[3] = {nullptr, nullptr, nullptr};
@@ -63,7 +68,7 @@ struct kvr_dev {
     uint64_t n_launches = 0;
     bool phase_events = false; // event nodes at every phase boundary (KVR_PHASE_EVENTS=1); off: K-attn's
                                // pair only (each event node costs ~5 us of the step graph)
-    int64_t *d_counts = nullptr;                  // all-reduce result (device)
+    int64_t *d_counts = nullptr;                  // all-reduce result (device), one row per ring slot
     int64_t *h_counts[2] = {nullptr, nullptr};    // its D2H copy per ring slot (pinned)
 };
 
@@ -145,9 +150,24 @@ __global__ void k_tl_reset(unsigned long long *tl) {
 }
 void tl_reset(unsigned long long *tl, cudaStream_t s) { k_tl_reset<<<1, 2 * KVR_TIMELINE_IDS, 0, s>>>(tl); }
 
+// KVR_QFORK: where the decode-queries branch forks (root | apply | hot; default apply).
+// Timeline A/B, K-attn start after the step's first kernel (C5 / C3 / C2 us): root
+// 47.5 / 74.4 / 90.2 (its CTAs crowd K-apply), apply 41.3 / 69.9 / 85.2, hot 46.6 /
+// 68.5 / 85.4. K-scan forks at the root (one CTA).
+int query_fork() {
+    static const int k = [] {
+        const char *e = getenv("KVR_QFORK");
+        const std::string v = e ? e : "";
+        return v == "root" ? 0 : v == "hot" ? 2 : 1;
+    }();
+    return k;
+}
+
 DevCtx ctx_for(const kvr_dev *d, int slot) {
     DevCtx c = d->base;
     c.desc = d->d_desc[slot];
+    if (slot < 2 && d->scans[slot])
+        c.scan = d->scans[slot];
     return c;
 }
 
@@ -156,14 +176,14 @@ DevCtx ctx_for(const kvr_dev *d, int slot) {
 void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, bool capturing = false) {
     cudaStream_t s = d->stream;
     auto mark = [&](int i) {
-        if (k >= 0 && (d->phase_events || i == 5 || i == 6)) // K-attn's pair is always kept
+        if (k >= 0 && d->phase_events) // (K-attn times itself: AttnSpan)
             ck(capturing ? cudaEventRecordWithFlags(d->ev_phase[k][i], s, cudaEventRecordExternal)
                          : cudaEventRecord(d->ev_phase[k][i], s),
                "phase event");
     };
     mark(0);
-    launch_apply(c, s, d->sms);
     if (!full_step) { // apply-only: everything in order on one stream
+        launch_apply(c, s, d->sms);
         launch_write(c, s, d->sms, 0);
         launch_write(c, s, d->sms, 1);
         launch_far_map_prime(c, s, d->sms);
@@ -174,17 +194,30 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     // the byte kernels, off the step's critical path. Kernel-to-kernel edges of the
     // main chain are PDL edges (each dependent launches during its predecessor and
     // waits in-kernel, griddepcontrol), unless phase event nodes sit between them.
+    // The branches fork at the graph's root, beside K-apply (neither reads what it
+    // writes): a fork edge after K-apply cost ~11 us before they started (timeline).
     const bool pdl = pdl_enabled() && !d->phase_events;
     cudaStream_t side = d->side, side2 = d->side2;
+    const int qfork = query_fork(); // 0 root, 1 after K-apply, 2 after the hot K-write
+    auto fork_queries = [&] {
+        ck(cudaEventRecord(d->ev_fork2, s), "fork");
+        ck(cudaStreamWaitEvent(side2, d->ev_fork2, 0), "fork wait");
+        launch_query(c, side2, d->sms);
+        ck(cudaEventRecord(d->ev_join2, side2), "join");
+    };
     ck(cudaEventRecord(d->ev_fork, s), "fork"); // (under capture: a dependency, not a node)
     ck(cudaStreamWaitEvent(side, d->ev_fork, 0), "fork wait");
-    ck(cudaStreamWaitEvent(side2, d->ev_fork, 0), "fork wait");
     launch_scan(c, side);
     ck(cudaEventRecord(d->ev_join, side), "join");
-    launch_query(c, side2, d->sms);
-    ck(cudaEventRecord(d->ev_join2, side2), "join");
+    if (qfork == 0)
+        fork_queries();
+    launch_apply(c, s, d->sms);
+    if (qfork == 1)
+        fork_queries();
     mark(1);
     launch_write(c, s, d->sms, 0, 0, pdl);
+    if (qfork == 2)
+        fork_queries();
     mark(2);
     launch_far_map_prime(c, s, d->sms, pdl);
     mark(3);
@@ -194,7 +227,7 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     ck(cudaStreamWaitEvent(s, d->ev_join2, 0), "join wait");
     mark(5);
     if (d->g.attention && d->attn)
-        launch_attn(d->attn, c, s);
+        launch_attn(d->attn, c, s, pdl);
     mark(6);
     if (c.utility)
         launch_mass(c, s);
@@ -205,11 +238,12 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     // the step's last kernel writes the end stamp (with a communicator: a stamp node
     // after the collective)
     const int stamp_in_kernel = d->comm ? 0 : 1;
-    launch_write(c, s, d->sms, 1, stamp_in_kernel && !c.stash);
-    launch_presum(c, s, d->sms, stamp_in_kernel, pdl);
+    // (after K-mass, a plain edge: K-mass is not a PDL dependent)
+    launch_tail(c, s, d->sms, stamp_in_kernel, pdl && !c.utility && d->g.attention && d->attn);
     // the step's counts summed over every rank (the only cross-GPU traffic)
     if (d->comm) {
-        nck(nccl().all_reduce(c.desc + offsetof(kvr_step_header, counts), d->d_counts, KVR_COUNTS, ncclInt64,
+        nck(nccl().all_reduce(c.desc + offsetof(kvr_step_header, counts), d->d_counts + (k > 0 ? k : 0) * KVR_COUNTS,
+                              KVR_COUNTS, ncclInt64,
                               ncclSum, d->comm, s),
             "per-step counts all-reduce");
         launch_stamp(c, s);
@@ -263,12 +297,25 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         cudaDeviceProp prop;
         ck(cudaGetDeviceProperties(&prop, g.device), "cudaGetDeviceProperties");
         d->sms = prop.multiProcessorCount;
-        ck(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking), "stream");
-        ck(cudaStreamCreateWithFlags(&d->side, cudaStreamNonBlocking), "side stream");
-        ck(cudaStreamCreateWithFlags(&d->side2, cudaStreamNonBlocking), "side stream");
+        // stream priorities become node priorities of the captured step graph
+        // (instantiated with cudaGraphInstantiateFlagUseNodePriority): the main chain
+        // and K-scan (on the critical path before K-gather) high, the decode queries
+        // (needed only by K-attn, ~20 us later) low, so their CTAs do not crowd K-fmp
+        int prio_low = 0, prio_high = 0;
+        ck(cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high), "stream priorities");
+        ck(cudaStreamCreateWithPriority(&d->stream, cudaStreamNonBlocking, prio_high), "stream");
+        ck(cudaStreamCreateWithPriority(&d->side, cudaStreamNonBlocking, prio_high), "side stream");
+        ck(cudaStreamCreateWithPriority(&d->side2, cudaStreamNonBlocking, prio_low), "side stream");
+        ck(cudaStreamCreateWithFlags(&d->h2d, cudaStreamNonBlocking), "copy stream");
+        ck(cudaStreamCreateWithFlags(&d->d2h, cudaStreamNonBlocking), "copy stream");
+        for (int i = 0; i < 2; ++i) {
+            ck(cudaEventCreateWithFlags(&d->ev_copied[i], cudaEventDisableTiming), "copy event");
+            ck(cudaEventCreateWithFlags(&d->ev_stats[i], cudaEventDisableTiming), "copy event");
+        }
         ck(cudaEventCreateWithFlags(&d->ev_fork, cudaEventDisableTiming), "fork event");
         ck(cudaEventCreateWithFlags(&d->ev_join, cudaEventDisableTiming), "join event");
         ck(cudaEventCreateWithFlags(&d->ev_join2, cudaEventDisableTiming), "join event");
+        ck(cudaEventCreateWithFlags(&d->ev_fork2, cudaEventDisableTiming), "fork event");
         for (int i = 0; i < 2; ++i) {
             ck(cudaEventCreate(&d->ev_start[i]), "event");
             ck(cudaEventCreate(&d->ev_stop[i]), "event");
@@ -346,8 +393,11 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
         c.trains = static_cast<kvr_train *>(dalloc(d.get(), sizeof(kvr_train) * c.max_trains, "trains"));
         c.descs = static_cast<kvr_descriptor *>(dalloc(d.get(), sizeof(kvr_descriptor) * c.max_scan, "descs"));
         c.gspans = static_cast<GSpan *>(dalloc(d.get(), sizeof(GSpan) * c.max_scan, "gspans"));
-        c.scan = static_cast<ScanCounters *>(dalloc(d.get(), sizeof(ScanCounters), "scan"));
-        ck(cudaMemsetAsync(c.scan, 0, sizeof(ScanCounters), d->stream), "scan zero");
+        for (int i = 0; i < 2; ++i) {
+            d->scans[i] = static_cast<ScanCounters *>(dalloc(d.get(), sizeof(ScanCounters), "scan"));
+            ck(cudaMemsetAsync(d->scans[i], 0, sizeof(ScanCounters), d->stream), "scan zero");
+        }
+        c.scan = d->scans[0];
         c.attn_sched = static_cast<uint32_t *>(dalloc(d.get(), 4 * sizeof(uint32_t), "schedule tickets"));
         ck(cudaMemsetAsync(c.attn_sched, 0, 4 * sizeof(uint32_t), d->stream), "schedule zero");
         if (const char *e = getenv("KVR_TIMELINE"); e && e[0] == '1') { // diagnostic timeline
@@ -373,7 +423,7 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
             d->h_counts[i] = static_cast<int64_t *>(p);
             std::memset(p, 0, KVR_COUNTS * sizeof(int64_t));
         }
-        d->d_counts = static_cast<int64_t *>(dalloc(d.get(), KVR_COUNTS * sizeof(int64_t), "counts"));
+        d->d_counts = static_cast<int64_t *>(dalloc(d.get(), 2 * KVR_COUNTS * sizeof(int64_t), "counts"));
         if (g.utility) {
             if (!g.attention || g.utility_layer >= g.layers || c.group > mass_max_group())
                 throw std::runtime_error("utility: needs attention, utility_layer < layers and q-group <= 16");
@@ -417,7 +467,15 @@ int kvr_dev_close(kvr_dev *d) {
         return KVR_OK;
     if (d->stream)
         cudaStreamSynchronize(d->stream);
+    if (d->h2d)
+        cudaStreamSynchronize(d->h2d);
+    if (d->d2h)
+        cudaStreamSynchronize(d->d2h);
     for (int i = 0; i < 2; ++i) {
+        if (d->ev_copied[i])
+            cudaEventDestroy(d->ev_copied[i]);
+        if (d->ev_stats[i])
+            cudaEventDestroy(d->ev_stats[i]);
         if (d->graph[i])
             cudaGraphExecDestroy(d->graph[i]);
         if (d->ev_start[i])
@@ -451,10 +509,18 @@ int kvr_dev_close(kvr_dev *d) {
         cudaEventDestroy(d->ev_fork);
     if (d->ev_join)
         cudaEventDestroy(d->ev_join);
+    if (d->ev_join2)
+        cudaEventDestroy(d->ev_join2);
+    if (d->ev_fork2)
+        cudaEventDestroy(d->ev_fork2);
     if (d->side)
         cudaStreamDestroy(d->side);
     if (d->side2)
         cudaStreamDestroy(d->side2);
+    if (d->h2d)
+        cudaStreamDestroy(d->h2d);
+    if (d->d2h)
+        cudaStreamDestroy(d->d2h);
     if (d->stream)
         cudaStreamDestroy(d->stream);
     delete d;
@@ -477,9 +543,18 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
             throw std::runtime_error("step descriptor exceeds max_desc_bytes");
         const auto *h = static_cast<const kvr_step_header *>(d->h_desc[k]);
         const DevCtx c = ctx_for(d, int(k));
-        ck(cudaEventRecord(d->ev_start[k], d->stream), "event");
-        ck(cudaMemcpyAsync(d->d_desc[k], d->h_desc[k], desc_bytes, cudaMemcpyHostToDevice, d->stream),
+        // descriptor H2D on the copy stream once slot k's previous graph is done with
+        // d_desc[k]; the graph stream waits for it (and for slot k's previous stats
+        // D2H, which read this slot's counters) — both overlap the graph in flight
+        ck(cudaStreamWaitEvent(d->h2d, d->ev_stop[k], 0), "slot free");
+        ck(cudaMemcpyAsync(d->d_desc[k], d->h_desc[k], desc_bytes, cudaMemcpyHostToDevice, d->h2d),
            "descriptor H2D");
+        ck(cudaEventRecord(d->ev_copied[k], d->h2d), "copy event");
+        ck(cudaStreamWaitEvent(d->stream, d->ev_copied[k], 0), "descriptor wait");
+        ck(cudaStreamWaitEvent(d->stream, d->ev_stats[k], 0), "stats slot wait");
+        if (c.utility) // K-mass buffers are shared by both slots: the other slot's D2H first
+            ck(cudaStreamWaitEvent(d->stream, d->ev_stats[k ^ 1], 0), "mass D2H wait");
+        ck(cudaEventRecord(d->ev_start[k], d->stream), "event");
         if (d->g.use_graph) {
             if (!d->graph[k]) {
                 cudaGraph_t graph;
@@ -498,7 +573,8 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
                 }
                 d->graph_kernels = kernels;
                 ++d->graph_captures;
-                ck(cudaGraphInstantiate(&d->graph[k], graph, 0), "graph instantiate");
+                ck(cudaGraphInstantiate(&d->graph[k], graph, cudaGraphInstantiateFlagUseNodePriority),
+                   "graph instantiate");
                 cudaGraphDestroy(graph);
             }
             ck(cudaGraphLaunch(d->graph[k], d->stream), "graph launch");
@@ -506,23 +582,27 @@ int kvr_dev_launch(kvr_dev *d, uint32_t k, uint64_t desc_bytes) {
             run_step_kernels(d, c, true, int(k), false);
             ck(cudaGetLastError(), "step launch");
         }
-        ck(cudaMemcpyAsync(d->h_scan[k], c.scan, sizeof(ScanCounters), cudaMemcpyDeviceToHost, d->stream),
+        ck(cudaEventRecord(d->ev_stop[k], d->stream), "event");
+        // stats D2H on the other copy stream, after the graph
+        ck(cudaStreamWaitEvent(d->d2h, d->ev_stop[k], 0), "graph done");
+        ck(cudaMemcpyAsync(d->h_scan[k], c.scan, sizeof(ScanCounters), cudaMemcpyDeviceToHost, d->d2h),
            "stats D2H");
         if (d->comm)
-            ck(cudaMemcpyAsync(d->h_counts[k], d->d_counts, KVR_COUNTS * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                               d->stream),
+            ck(cudaMemcpyAsync(d->h_counts[k], d->d_counts + k * KVR_COUNTS, KVR_COUNTS * sizeof(int64_t),
+                               cudaMemcpyDeviceToHost,
+                               d->d2h),
                "counts D2H");
         else
             std::memcpy(d->h_counts[k], h->counts, KVR_COUNTS * sizeof(int64_t));
         if (c.utility && h->step % c.utility == 0) {
             ck(cudaMemcpyAsync(d->h_mass_count[k], c.mass_count, uint64_t(c.n_slots) * 4, cudaMemcpyDeviceToHost,
-                               d->stream),
+                               d->d2h),
                "mass count D2H");
             ck(cudaMemcpyAsync(d->h_mass[k], c.mass_runs, uint64_t(c.n_slots) * c.W * sizeof(kvr_mass_run),
-                               cudaMemcpyDeviceToHost, d->stream),
+                               cudaMemcpyDeviceToHost, d->d2h),
                "mass D2H");
         }
-        ck(cudaEventRecord(d->ev_stop[k], d->stream), "event");
+        ck(cudaEventRecord(d->ev_stats[k], d->d2h), "stats event");
         d->launched[k] = h->step;
         d->in_flight[k] = true;
         ++d->n_launches;
@@ -552,7 +632,7 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
         std::memset(out, 0, sizeof(*out));
         if (!d->in_flight[k])
             return;
-        ck(cudaEventSynchronize(d->ev_stop[k]), "step wait");
+        ck(cudaEventSynchronize(d->ev_stats[k]), "step wait"); // (after ev_stop: the D2H follows it)
         float ms = 0.f;
         ck(cudaEventElapsedTime(&ms, d->ev_start[k], d->ev_stop[k]), "elapsed");
         const ScanCounters &sc = *d->h_scan[k];
@@ -560,12 +640,16 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
         out->device_ms = ms;
         for (int j = 0; j < 7; ++j) {
             float t = 0.f;
-            if (d->phase_events || j == 5)
+            if (d->phase_events)
                 ck(cudaEventElapsedTime(&t, d->ev_phase[k][j], d->ev_phase[k][j + 1]), "elapsed");
             out->phase_ms[j] = t;
         }
         out->gather_ms = out->phase_ms[4];
-        out->attn_ms = out->phase_ms[5];
+        // K-attn's own span (first CTA start to last exit) unless phase events bracket it
+        out->attn_ms = d->phase_events ? out->phase_ms[5]
+                       : sc.attn_t1 > sc.attn_t0 ? double(sc.attn_t1 - sc.attn_t0) * 1e-6 : 0.0;
+        if (!d->phase_events)
+            out->phase_ms[5] = float(out->attn_ms);
         out->trains = sc.trains;
         out->descriptors = sc.descriptors;
         out->spans = sc.spans;
@@ -580,7 +664,10 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
 }
 
 int kvr_dev_sync(kvr_dev *d) {
-    return guard([&] { ck(cudaStreamSynchronize(d->stream), "sync"); });
+    return guard([&] {
+        ck(cudaStreamSynchronize(d->stream), "sync");
+        ck(cudaStreamSynchronize(d->d2h), "sync");
+    });
 }
 
 int kvr_dev_buffer_bytes(kvr_dev *d, int buffer, uint64_t *out) {
@@ -620,7 +707,7 @@ int kvr_dev_read(kvr_dev *d, int buffer, uint64_t offset, uint64_t bytes, void *
         case KVR_BUF_FAR: base = c.far; break;
         case KVR_BUF_TRAINS: base = c.trains; break;
         case KVR_BUF_DESCS: base = c.descs; break;
-        case KVR_BUF_SCAN: base = c.scan; break;
+        case KVR_BUF_SCAN: base = d->scans[d->launched[1] > d->launched[0] ? 1 : 0]; break; // the last step's
         case KVR_BUF_SMAP: base = c.smap; break;
         }
         ck(cudaStreamSynchronize(d->stream), "read sync");
@@ -633,7 +720,8 @@ int kvr_dev_read_staged(kvr_dev *d, uint64_t tok_begin, uint64_t count, void *ou
     return guard([&] {
         ck(cudaStreamSynchronize(d->stream), "read sync");
         ScanCounters sc{};
-        ck(cudaMemcpy(&sc, d->base.scan, sizeof(sc), cudaMemcpyDeviceToHost), "scan counters");
+        ck(cudaMemcpy(&sc, d->scans[d->launched[1] > d->launched[0] ? 1 : 0], sizeof(sc), cudaMemcpyDeviceToHost),
+           "scan counters");
         if (tok_begin + count > sc.total_tokens)
             throw std::runtime_error("read_staged: tokens past the last step's gather list");
         if (!count)

@@ -30,6 +30,7 @@ struct ScanCounters {
     uint64_t total_tokens;
     uint64_t train_bytes;
     uint64_t end_ns; // %globaltimer when the step's last kernel ran (inter-token latency)
+    uint64_t attn_t0, attn_t1; // K-attn's first CTA start / last warp exit (%globaltimer; reset by K-scan)
 };
 
 /// Everything a kernel needs: geometry + device buffers. Passed by value.
@@ -76,15 +77,46 @@ __device__ inline unsigned long long gtimer() {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     return t;
 }
-struct TlScope {
-    unsigned long long *tl;
-    __device__ TlScope(const DevCtx &c, uint32_t id) : tl(c.tl ? c.tl + 2 * id : nullptr) {
-        if (tl && threadIdx.x == 0)
-            atomicMin(tl, gtimer());
+/// K-attn's own span on %globaltimer into the step counters (the step graph has no
+/// event nodes around it, so the kernel times itself; ncu's gpu__time_duration
+/// is the same span: first CTA start to last CTA exit).
+/// A (start, end) pair on %globaltimer over a kernel: min over CTA starts, max over CTA
+/// exits. Construct at the top of the kernel (every thread, before any exit); the exit
+/// stamp is ONE global atomic per CTA, by its last warp to leave (counted in shared
+/// memory) — one atomic per warp on one address serialised ~10k atomics per launch.
+struct SpanStamp {
+    unsigned long long *t;
+    unsigned *left;
+    __device__ void open(unsigned long long *t_, unsigned *cnt) {
+        t = t_, left = cnt;
+        if (threadIdx.x == 0) {
+            *left = (blockDim.x + 31) / 32;
+            atomicMin(t, gtimer());
+        }
+        __syncthreads();
+    }
+    __device__ void close() {
+        if ((threadIdx.x & 31) == 0 && atomicSub(left, 1u) == 1u)
+            atomicMax(t + 1, gtimer());
+    }
+};
+struct AttnSpan : SpanStamp {
+    __device__ explicit AttnSpan(const DevCtx &c) {
+        __shared__ unsigned cnt;
+        open(reinterpret_cast<unsigned long long *>(&c.scan->attn_t0), &cnt);
+    }
+    __device__ ~AttnSpan() { close(); }
+};
+struct TlScope : SpanStamp {
+    __device__ TlScope(const DevCtx &c, uint32_t id) {
+        __shared__ unsigned cnt;
+        t = nullptr;
+        if (c.tl) // (uniform)
+            open(c.tl + 2 * id, &cnt);
     }
     __device__ ~TlScope() {
-        if (tl && (threadIdx.x & 31) == 0)
-            atomicMax(tl + 1, gtimer());
+        if (t)
+            close();
     }
 };
 
@@ -182,6 +214,8 @@ void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp 
 void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
 void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms, bool pdl = false); // K-far + K-map + K-prime
 void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp
+/// the step's tail after K-attn: cold prompt rows + K-presum (stamp: writes the end stamp)
+void launch_tail(const DevCtx &c, cudaStream_t s, int sms, int stamp, bool pdl);
 void launch_presum(const DevCtx &c, cudaStream_t s, int sms, int stamp = 0, bool pdl = false); // prompt rows + their far chunk means
 void launch_mass(const DevCtx &c, cudaStream_t s);             // attention-utility observations
 bool prepare_mass(const DevCtx &c); // false: no K-mass for this geometry
@@ -208,8 +242,9 @@ struct TcMaps {
 };
 // (tile: one K or V half of a 128-row tile per op — the two halves have separate rings)
 bool attn_tc_maps(const DevCtx &c, TcMaps *maps);
-void launch_attn_tc(const void *fn, const DevCtx &c, const TcMaps &maps, uint32_t grid, cudaStream_t s);
-void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s);
+void launch_attn_tc(const void *fn, const DevCtx &c, const TcMaps &maps, uint32_t grid, cudaStream_t s,
+                    bool pdl = false);
+void launch_attn(const AttnPlan *p, const DevCtx &c, cudaStream_t s, bool pdl = false);
 void free_attn_plan(AttnPlan *p);
 const char *attn_variant(const AttnPlan *p);
 

@@ -383,6 +383,8 @@ template <int kScanThreads> __global__ void __launch_bounds__(kScanThreads, 1) k
         c.scan->status = s_status;
         c.scan->total_tokens = ok ? carry_t : 0;
         c.scan->train_bytes = bytes;
+        c.scan->attn_t0 = ~0ull; // K-attn (after the join) stamps its span
+        c.scan->attn_t1 = 0;
     }
 }
 
