@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(32 * (warps_per_head<QG>() * kMaxG + 1), 1)
     constexpr int DPL = A::DPL;
     constexpr int kState = 32 * QG * (2 + DPL); // floats of one warp's (m, l, acc) state
     extern __shared__ __align__(128) uint8_t smem[];
-    pdl_wait();
-    pdl_trigger();
+    pdl_wait(); // (no early trigger: the tail's CTAs, resident beside a CUDA-core K-attn CTA
+                // and waiting, cost it ~0.6 % on C2; they launch as K-attn's CTAs exit)
     AttnSpan span_(c);
     TlScope tl_(c, kTlAttn);
     const uint32_t tile_elems = kTile * G * HD;

@@ -495,10 +495,6 @@ template <typename T, int G>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(DevCtx c, const __grid_constant__ TcMaps maps) {
     using SP = Splits<T, G>;
-    pdl_wait();
-    pdl_trigger();
-    AttnSpan span_(c);
-    TlScope tl_(c, kTlAttn);
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *kbuf = smem;                                    // kKStages x 32 KiB
@@ -559,6 +555,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // PDL: everything above touches only shared memory, TMEM, the descriptor and the
+    // claim counter (reset by the previous launch), so it overlaps the predecessor's
+    // tail; the roles below read what K-gather and the queries wrote
+    pdl_wait(); // (no early trigger: the tail's CTAs, resident beside a CUDA-core K-attn CTA
+                // and waiting, cost it ~0.6 % on C2; they launch as K-attn's CTAs exit)
+    AttnSpan span_(c);
+    TlScope tl_(c, kTlAttn);
 
     if (warp == 0 || warp == 2) { // ---------------- producers: warp 0 streams K, warp 2 streams V ----------------
         const uint32_t kv = warp == 2 ? 1u : 0u;
