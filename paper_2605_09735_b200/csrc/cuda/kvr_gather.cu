@@ -508,7 +508,7 @@ int gather_kind() {
     static const int k = [] {
         const char *e = getenv("KVR_GATHER");
         const std::string v = e ? e : "";
-        return v == "tma" ? 0 : v == "tma5" ? 1 : v == "tma2" ? 2 : v == "vec" ? 3 : v == "ivec" ? 4 : 5;
+        return v == "tma" ? 0 : v == "tma5" ? 1 : v == "tma2" ? 2 : v == "vec" ? 3 : v == "ivec" ? 4 : v == "split7" ? 6 : 5;
     }();
     return k;
 }
@@ -522,6 +522,8 @@ cudaError_t prepare_gather(const DevCtx &) {
         e = cudaFuncSetAttribute(k_gather<3, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(3 * kMaxPiece));
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_gather2<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(6 * kMaxPiece));
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_gather2<7>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(7 * kMaxPiece));
     return e;
 }
 
@@ -533,6 +535,7 @@ void launch_gather(const DevCtx &c, cudaStream_t s, int sms, bool pdl) {
     case 3: launch_ex(k_gather_vec<4096, 2, false>, n * 2, 32 * kVecWarps, 0, s, pdl, c); break;
     case 4: launch_ex(k_gather_vec<4096, 2, true>, n * 2, 32 * kVecWarps, 0, s, pdl, c); break;
     case 5: launch_ex(k_gather2<6>, n, 64, size_t(6) * kMaxPiece, s, pdl, c); break;
+    case 6: launch_ex(k_gather2<7>, n, 64, size_t(7) * kMaxPiece, s, pdl, c); break;
     default: launch_ex(k_gather<6, 4>, n, 32, size_t(6) * kMaxPiece, s, pdl, c); break;
     }
 }

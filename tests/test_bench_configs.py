@@ -52,3 +52,19 @@ def test_cpu_baseline_scaling_keeps_tokens_per_page():
         tb2 = 2 * s["layers"] * s["kv_head_dim"] * s["elem_bytes"]
         assert p["page_bytes"] // tb == s["page_bytes"] // tb2
         assert s["page_bytes"] & (s["page_bytes"] - 1) == 0
+
+
+def test_tail_against_the_fixed_shape():
+    """bench.live_binned_tail: the tail of all steps against the median full-width step
+    (the static graph's own step), beside the work-model and per-live-count readings."""
+    from types import SimpleNamespace as R
+    recs = [R(live_sessions=64, device_ms=0.48 + 0.001 * (i % 10), attn_ms=0.43, attn_bytes=3e9) for i in range(100)]
+    recs += [R(live_sessions=20, device_ms=0.25, attn_ms=0.2, attn_bytes=1e9) for _ in range(100)]
+    recs.append(R(live_sessions=64, device_ms=0.57, attn_ms=0.5, attn_bytes=3e9))
+    t = bench.live_binned_tail(recs, 64)
+    fw = t["full_width"]
+    assert fw["width"] == 64 and fw["steps"] == 101
+    assert abs(fw["p50_ms"] - 0.485) < 1e-9  # nearest rank: the 51st of 101
+    assert abs(fw["max_all_steps_over_p50"] - 0.57 / 0.485) < 1e-9
+    assert fw["p99_all_steps_over_p50"] <= fw["max_all_steps_over_p50"]
+    assert bench.live_binned_tail(recs, 128)["full_width"] is None  # no step at that width
