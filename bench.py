@@ -404,7 +404,8 @@ def run_b200(args, rank, local, world) -> dict | None:
     attn_bytes = sum(r.attn_bytes for r in recs)
     attn_s = sum(r.attn_ms for r in recs) / 1e3
     gather_bytes = sum(r.gather_bytes for r in recs)
-    gather_s = sum(r.gather_ms for r in recs) / 1e3
+    gather_s = sum(r.gather_ms for r in recs if r.gather_bytes) / 1e3
+    gather_steps = sum(1 for r in recs if r.gather_bytes)
     h2d = sum(r.h2d_bytes for r in recs) / args.steps
     dev = d.device()
     variant = dev.attention_variant()
@@ -425,6 +426,7 @@ def run_b200(args, rank, local, world) -> dict | None:
         "comm_note": comm_note,
         "attn_bytes_all": attn_bytes_all,
         "gather_bytes": gather_bytes, "gather_s": gather_s, "gather_bytes_all": gather_bytes_all,
+        "gather_steps": gather_steps,
         "h2d": h2d, "variant": variant, "step_kernels": step_kernels, "captures": captures,
         "prefill_backlog": backlog, "prefill_dropped": dropped, "clocks": clocks.summary(), "fill_steps": fill,
         "live_mean": statistics.mean(r.live_sessions for r in recs),
@@ -485,6 +487,15 @@ def read_stream_context(traffic, s_per_launch) -> dict:
     if traffic and s_per_launch:
         out["read_stream_frac"] = traffic / s_per_launch / 1e9 / peak
     return out
+
+
+def in_graph_gather(res, pk) -> dict | None:
+    """K-gather inside the timed steps' graphs: (read + write) train bytes / its in-kernel
+    span, summed over the steps that staged trains (queries and K-scan run beside it)."""
+    if not res["gather_s"] or not res["gather_bytes"]:
+        return None
+    gbs = 2 * res["gather_bytes"] / res["gather_s"] / 1e9
+    return {"hbm_gbs": gbs, "frac": gbs / pk["hbm_gbs"], "ms_per_step": res["gather_s"] * 1e3 / max(1, res["gather_steps"])}
 
 
 def live_binned_tail(recs, width: int = 0) -> dict:
@@ -637,8 +648,10 @@ def main():
         "gather": {"hbm_gbs": gather_gbs, "frac": gather_gbs / pk["hbm_gbs"] if gather_gbs else None,
                    "bytes_per_launch": 2 * gk["bytes_read"] if gk["bytes_read"] else None,
                    "us_per_launch": gk["us_per_launch"],
-                   "basis": "(read + write) train bytes of one step / K-gather alone, 20 back-to-back "
-                            "replays on that step's descriptor (CUDA events)"},
+                   "basis": "(read + write) train bytes of one step / K-gather alone: the mean of 20 "
+                            "launches' own spans (first-CTA start to last exit on %globaltimer, ncu's "
+                            "gpu__time_duration) on that step's descriptor",
+                   "in_graph": in_graph_gather(res, pk)},
         # decode tok/s roofline = tokens / (KV bytes the attention must read / peak)
         "decode_roofline": {
             "tokens_per_s": roof_tps,

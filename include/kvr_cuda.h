@@ -226,13 +226,14 @@ int kvr_dev_buffer_bytes(kvr_dev *d, int buffer, uint64_t *out);
 /* rows per (slot, layer) plane of KVR_BUF_RING: ring_rows + the guard rows that mirror
  * rows [0, guard) (the tensor-core attention's whole-tile loads never split) */
 int kvr_dev_ring_plane_rows(kvr_dev *d, uint32_t *out);
-/* time `iters` replays of the last launched step's attention kernel alone
- * (CUDA events on the launch stream); used by bench.py for the roofline */
+/* `iters` launches of the last launched step's attention (K-gather) kernel alone: the
+ * mean of each launch's own span (first-CTA start to last exit, %globaltimer — the
+ * quantity ncu reports as gpu__time_duration; launch gaps are not counted) */
 int kvr_dev_time_attention(kvr_dev *d, uint32_t iters, double *ms_per_launch);
 int kvr_dev_time_gather(kvr_dev *d, uint32_t iters, double *ms_per_launch);
 /* diagnostic kernel timeline (only when KVR_TIMELINE=1 was set at kvr_dev_open): for each
  * kernel id (0 apply, 1 queries, 2 K-scan, 3 hot K-write, 4 K-far/map/prime, 5 K-gather,
- * 6 K-attn, 7 cold K-write, 8 K-presum) the %globaltimer ns of its first CTA start and
+ * 6 K-attn, 7 cold K-write, 8 K-presum, 9 tensor-core K-attn's CTA entry before its prologue) the %globaltimer ns of its first CTA start and
  * last warp exit since the previous call, out[2 id], out[2 id + 1] (~0 / 0: not run);
  * synchronises the step stream and resets */
 #define KVR_TIMELINE_IDS 16

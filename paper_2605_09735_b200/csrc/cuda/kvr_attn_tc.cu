@@ -360,6 +360,9 @@ constexpr uint32_t kQ = 64;     // queue entries (roles lag the claimer by < ~10
 #define KVR_TC_AHEADQ 4
 #endif
 constexpr uint32_t kAheadQ = KVR_TC_AHEADQ; // items claimed ahead of the claimer's own position
+#ifndef KVR_TC_FIRST_CLAIM
+#define KVR_TC_FIRST_CLAIM 1
+#endif
 struct ItemQueue {
     uint32_t item[kQ];
     uint32_t tail; // items published
@@ -495,6 +498,7 @@ template <typename T, int G>
 __global__ void __launch_bounds__(kThreads, 1)
     k_attn_tc(DevCtx c, const __grid_constant__ TcMaps maps) {
     using SP = Splits<T, G>;
+    TlScopeT<1> tl_entry_(c, kTlAttnEntry); // (diagnostic: CTA entry, before the prologue)
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t *kbuf = smem;                                    // kKStages x 32 KiB
@@ -543,7 +547,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         queue->tail = 0;
         queue->end = ~0u;
-        claim_to(queue, kAheadQ, c, slots, n_items); // the first items, before any role reads
+        // the first item only: each claim is an atomic round trip plus a slot-state load,
+        // serial — claiming kAheadQ here held every CTA's start ~2 us per item after
+        // K-gather (timeline); warp 0 tops the queue up as its tile stream advances
+        claim_to(queue, KVR_TC_FIRST_CLAIM, c, slots, n_items);
     }
     fence_async_smem();
     if (warp == 1) {

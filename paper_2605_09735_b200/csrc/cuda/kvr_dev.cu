@@ -163,6 +163,15 @@ int query_fork() {
     return k;
 }
 
+// KVR_QJOIN=gather: the queries branch joins before K-gather instead of before K-attn (A/B)
+bool query_join_at_gather() {
+    static const bool v = [] {
+        const char *e = getenv("KVR_QJOIN");
+        return e && std::string(e) == "gather";
+    }();
+    return v;
+}
+
 DevCtx ctx_for(const kvr_dev *d, int slot) {
     DevCtx c = d->base;
     c.desc = d->d_desc[slot];
@@ -222,9 +231,13 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     launch_far_map_prime(c, s, d->sms, pdl);
     mark(3);
     ck(cudaStreamWaitEvent(s, d->ev_join, 0), "join wait");
+    const bool qjoin_gather = query_join_at_gather();
+    if (qjoin_gather) // K-attn's only dependency is then K-gather's PDL edge
+        ck(cudaStreamWaitEvent(s, d->ev_join2, 0), "join wait");
     mark(4);
     launch_gather(c, s, d->sms, pdl);
-    ck(cudaStreamWaitEvent(s, d->ev_join2, 0), "join wait");
+    if (!qjoin_gather)
+        ck(cudaStreamWaitEvent(s, d->ev_join2, 0), "join wait");
     mark(5);
     if (d->g.attention && d->attn)
         launch_attn(d->attn, c, s, pdl);
@@ -644,7 +657,9 @@ int kvr_dev_wait(kvr_dev *d, uint32_t k, kvr_step_stats *out) {
                 ck(cudaEventElapsedTime(&t, d->ev_phase[k][j], d->ev_phase[k][j + 1]), "elapsed");
             out->phase_ms[j] = t;
         }
-        out->gather_ms = out->phase_ms[4];
+        // K-gather's own span (first-CTA start to last exit) unless phase events bracket it
+        out->gather_ms = d->phase_events ? out->phase_ms[4]
+                         : sc.gather_t1 > sc.gather_t0 ? double(sc.gather_t1 - sc.gather_t0) * 1e-6 : 0.0;
         // K-attn's own span (first CTA start to last exit) unless phase events bracket it
         out->attn_ms = d->phase_events ? out->phase_ms[5]
                        : sc.attn_t1 > sc.attn_t0 ? double(sc.attn_t1 - sc.attn_t0) * 1e-6 : 0.0;
@@ -752,6 +767,10 @@ int kvr_dev_fault(kvr_dev *d, int what, uint64_t arg) {
     });
 }
 
+// `iters` launches of K-attn / K-gather alone on the last launched step's descriptor;
+// each launch's own span (first-CTA start to last exit, the kernel's %globaltimer stamps —
+// ncu's gpu__time_duration), averaged: launch gaps between back-to-back launches are
+// not the kernel's time.
 static int time_kernel(kvr_dev *d, uint32_t iters, double *ms, bool attn) {
     return guard([&] {
         ck(cudaStreamSynchronize(d->stream), "sync");
@@ -760,21 +779,22 @@ static int time_kernel(kvr_dev *d, uint32_t iters, double *ms, bool attn) {
         const DevCtx c = ctx_for(d, k);
         if (attn && !d->attn)
             throw std::runtime_error("attention disabled");
-        auto once = [&] {
+        uint64_t *span = attn ? &c.scan->attn_t0 : &c.scan->gather_t0;
+        const uint64_t reset[2] = {~0ull, 0ull};
+        double total = 0.0;
+        for (uint32_t i = 0; i <= iters; ++i) { // (the first launch warms up, untimed)
+            ck(cudaMemcpyAsync(span, reset, sizeof(reset), cudaMemcpyHostToDevice, d->stream), "span reset");
             if (attn)
                 launch_attn(d->attn, c, d->stream);
             else
                 launch_gather(c, d->stream, d->sms);
-        };
-        once();
-        ck(cudaEventRecord(d->ev_attn[0], d->stream), "event");
-        for (uint32_t i = 0; i < iters; ++i)
-            once();
-        ck(cudaEventRecord(d->ev_attn[1], d->stream), "event");
-        ck(cudaEventSynchronize(d->ev_attn[1]), "sync");
-        float t = 0.f;
-        ck(cudaEventElapsedTime(&t, d->ev_attn[0], d->ev_attn[1]), "elapsed");
-        *ms = iters ? t / iters : 0.0;
+            uint64_t got[2];
+            ck(cudaMemcpyAsync(got, span, sizeof(got), cudaMemcpyDeviceToHost, d->stream), "span read");
+            ck(cudaStreamSynchronize(d->stream), "sync");
+            if (i > 0 && got[1] > got[0])
+                total += double(got[1] - got[0]) * 1e-6;
+        }
+        *ms = iters ? total / iters : 0.0;
     });
 }
 

@@ -158,6 +158,7 @@ template <int kStages, int kAhead>
 __global__ void __launch_bounds__(32) k_gather(DevCtx c) {
     pdl_wait();
     pdl_trigger();
+    GatherSpan span_(c);
     TlScope tl_(c, kTlGather);
     extern __shared__ __align__(128) uint8_t stage[];
     __shared__ __align__(8) uint64_t full[kStages];
@@ -257,6 +258,7 @@ template <int kSt>
 __global__ void __launch_bounds__(64) k_gather2(DevCtx c) {
     pdl_wait();
     pdl_trigger();
+    GatherSpan span_(c);
     TlScope tl_(c, kTlGather);
     extern __shared__ __align__(128) uint8_t stage[];
     __shared__ __align__(8) uint64_t full[kSt], empty[kSt];
@@ -370,6 +372,7 @@ template <int kUnit, int kFly, bool kInterleave>
 __global__ void __launch_bounds__(32 * kVecWarps) k_gather_vec(DevCtx c) {
     pdl_wait();
     pdl_trigger();
+    GatherSpan span_(c);
     TlScope tl_(c, kTlGather);
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);

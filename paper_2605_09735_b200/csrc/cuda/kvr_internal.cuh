@@ -31,6 +31,7 @@ struct ScanCounters {
     uint64_t train_bytes;
     uint64_t end_ns; // %globaltimer when the step's last kernel ran (inter-token latency)
     uint64_t attn_t0, attn_t1; // K-attn's first CTA start / last warp exit (%globaltimer; reset by K-scan)
+    uint64_t gather_t0, gather_t1; // the same for K-gather
 };
 
 /// Everything a kernel needs: geometry + device buffers. Passed by value.
@@ -71,7 +72,8 @@ struct DevCtx {
 /// Diagnostic timeline (KVR_TIMELINE=1): per kernel of the step, the first CTA's start
 /// and the last warp's exit on %globaltimer (min / max over CTAs) — the step graph's
 /// real schedule without event nodes. Ids: kvr_dev_timeline in kvr_cuda.h.
-enum TlId : uint32_t { kTlApply, kTlQuery, kTlScan, kTlWriteHot, kTlFmp, kTlGather, kTlAttn, kTlWriteCold, kTlPresum };
+enum TlId : uint32_t { kTlApply, kTlQuery, kTlScan, kTlWriteHot, kTlFmp, kTlGather, kTlAttn, kTlWriteCold, kTlPresum,
+                      kTlAttnEntry };
 __device__ inline unsigned long long gtimer() {
     unsigned long long t;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -107,18 +109,27 @@ struct AttnSpan : SpanStamp {
     }
     __device__ ~AttnSpan() { close(); }
 };
-struct TlScope : SpanStamp {
-    __device__ TlScope(const DevCtx &c, uint32_t id) {
+struct GatherSpan : SpanStamp {
+    __device__ explicit GatherSpan(const DevCtx &c) {
+        __shared__ unsigned cnt;
+        open(reinterpret_cast<unsigned long long *>(&c.scan->gather_t0), &cnt);
+    }
+    __device__ ~GatherSpan() { close(); }
+};
+/// (kTag: each scope live at the same time in one kernel needs its own exit counter)
+template <int kTag> struct TlScopeT : SpanStamp {
+    __device__ TlScopeT(const DevCtx &c, uint32_t id) {
         __shared__ unsigned cnt;
         t = nullptr;
         if (c.tl) // (uniform)
             open(c.tl + 2 * id, &cnt);
     }
-    __device__ ~TlScope() {
+    __device__ ~TlScopeT() {
         if (t)
             close();
     }
 };
+using TlScope = TlScopeT<0>;
 
 /// Token `tok` of a slot is written into the ring by K-write / K-prime only when it
 /// lies in the live window after this step and K-gather does not deliver it (near

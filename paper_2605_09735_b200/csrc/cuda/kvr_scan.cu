@@ -383,8 +383,10 @@ template <int kScanThreads> __global__ void __launch_bounds__(kScanThreads, 1) k
         c.scan->status = s_status;
         c.scan->total_tokens = ok ? carry_t : 0;
         c.scan->train_bytes = bytes;
-        c.scan->attn_t0 = ~0ull; // K-attn (after the join) stamps its span
+        c.scan->attn_t0 = ~0ull; // K-attn and K-gather (after the join) stamp their spans
         c.scan->attn_t1 = 0;
+        c.scan->gather_t0 = ~0ull;
+        c.scan->gather_t1 = 0;
     }
 }
 

@@ -648,7 +648,7 @@ class Device:
         return ms.value
 
     TIMELINE_NAMES = ("apply", "queries", "scan", "write_hot", "far_map_prime", "gather", "attention",
-                      "write_cold", "presum")
+                      "write_cold", "presum", "attention_entry")
 
     def timeline(self) -> dict:
         """Diagnostic (KVR_TIMELINE=1 at open): {kernel: (start_ns, end_ns)} since the last
