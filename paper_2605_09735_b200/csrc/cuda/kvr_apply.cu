@@ -242,6 +242,15 @@ __device__ __forceinline__ void write_body(const DevCtx &c, int cold) {
 
 // Decode queries for live slots: [slot][L][Hq][hd], exact in the KV element type
 // (kvo_fill_query in the oracle). One CTA per (slot, layer); one hash per 8 lanes.
+/// Two values exact in the element type (<= 8 significant bits), packed: bf16 = the upper
+/// halves of the fp32 bits, fp16 = the conversion (exact).
+__device__ __forceinline__ uint32_t pack_exact2(const DevCtx &c, float a, float b) {
+    if (c.elem_kind == KVR_ELEM_BF16)
+        return __byte_perm(__float_as_uint(a), __float_as_uint(b), 0x7632);
+    const __half2 h = __floats2half2_rn(a, b);
+    return *reinterpret_cast<const uint32_t *>(&h);
+}
+
 __global__ void __launch_bounds__(256) k_query(DevCtx c) {
     pdl_trigger();
     TlScope tl_(c, kTlQuery);
@@ -259,6 +268,7 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
         const uint64_t base = c.seed ^ (0x51ull << 56) ^ (uint64_t(slots[s].session) << 32) ^
                               (h->step << 20) ^ (uint64_t(l) << 12);
         float4 *q = reinterpret_cast<float4 *>(c.q + uint64_t(sl) * per_layer);
+        int4 *q16 = reinterpret_cast<int4 *>(reinterpret_cast<uint16_t *>(c.q) + uint64_t(sl) * per_layer);
         const uint32_t hd_shift = __ffs(c.hd) - 1; // head_dim is a power of two (32/64/128)
         if (c.query_mode == KVR_QUERY_F32) { // two 24-bit lanes per hash (kvo_fill_query_mode)
             const uint64_t fbase = base ^ (0x52ull << 56) ^ (0x51ull << 56);
@@ -288,8 +298,15 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
                 if (i >= n8)
                     break;
                 const uint32_t lo = uint32_t(x[u]), hi = uint32_t(x[u] >> 32);
-                q[2 * i] = make_float4(val(lo, 0), val(lo, 1), val(lo, 2), val(lo, 3));
-                q[2 * i + 1] = make_float4(val(hi, 0), val(hi, 1), val(hi, 2), val(hi, 3));
+                const float4 a = make_float4(val(lo, 0), val(lo, 1), val(lo, 2), val(lo, 3));
+                const float4 b = make_float4(val(hi, 0), val(hi, 1), val(hi, 2), val(hi, 3));
+                if (c.q_esz == 4) {
+                    q[2 * i] = a;
+                    q[2 * i + 1] = b;
+                } else { // exact in the element type: 16 bytes per 8 lanes instead of 32
+                    q16[i] = make_int4(int(pack_exact2(c, a.x, a.y)), int(pack_exact2(c, a.z, a.w)),
+                                       int(pack_exact2(c, b.x, b.y)), int(pack_exact2(c, b.z, b.w)));
+                }
             }
         }
     }

@@ -133,7 +133,7 @@ template <typename T, int HD, int QG, int R> struct Attn {
     float q[QG][DPL];
     float m[QG], lsum[QG], acc[QG][DPL];
 
-    __device__ void init(const float *qsrc) { // qsrc: [QG][HD] floats
+    __device__ void init(const DevCtx &c, uint64_t q0) { // queries [QG][HD] from element q0
         const int lane = threadIdx.x & 31;
 #pragma unroll
         for (int g = 0; g < QG; ++g) {
@@ -141,7 +141,7 @@ template <typename T, int HD, int QG, int R> struct Attn {
             lsum[g] = 0.f;
 #pragma unroll
             for (int k = 0; k < DPL; ++k) {
-                q[g][k] = qsrc[g * HD + DPL * lane + k];
+                q[g][k] = load_q(c, q0 + g * HD + DPL * lane + k);
                 acc[g][k] = 0.f;
             }
         }
@@ -334,7 +334,7 @@ __global__ void __launch_bounds__(32 * (warps_per_head<QG>() * kMaxG + 1), 1)
         window(slot, lo, t0, n_tiles);
         const uint64_t w = st.written;
         A at;
-        at.init(c.q + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD);
+        at.init(c, ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * QG) * HD);
         // far summaries: rows straight from global memory
         const T *far_base = reinterpret_cast<const T *>(c.far) +
                             (uint64_t(slot) * c.L + l) * c.max_chunks * c.row_elems + uint64_t(kvh) * HD;

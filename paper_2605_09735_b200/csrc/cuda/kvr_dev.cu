@@ -399,9 +399,15 @@ int kvr_dev_open(const kvr_geometry *geo, kvr_dev **out) {
                                                             "presum stash"))
                             : nullptr;
         const uint64_t qn = uint64_t(c.n_slots) * c.L * c.Hq * c.hd;
-        c.q = static_cast<float *>(dalloc(d.get(), qn * 4, "q"));
+        // exact queries (multiples of 1/128 in [-1, 1)) are stored in the KV element type:
+        // half the query bytes K-attn reads per item (C3: 67 -> 34 MB per step)
+#ifndef KVR_Q16
+#define KVR_Q16 1
+#endif
+        c.q_esz = KVR_Q16 && c.query_mode == KVR_QUERY_EXACT && c.esz == 2 ? 2u : 4u;
+        c.q = static_cast<float *>(dalloc(d.get(), qn * c.q_esz, "q"));
         c.out = static_cast<float *>(dalloc(d.get(), qn * 4, "out"));
-        ck(cudaMemsetAsync(c.q, 0, qn * 4, d->stream), "q zero");
+        ck(cudaMemsetAsync(c.q, 0, qn * c.q_esz, d->stream), "q zero");
         ck(cudaMemsetAsync(c.out, 0, qn * 4, d->stream), "out zero");
         c.trains = static_cast<kvr_train *>(dalloc(d.get(), sizeof(kvr_train) * c.max_trains, "trains"));
         c.descs = static_cast<kvr_descriptor *>(dalloc(d.get(), sizeof(kvr_descriptor) * c.max_scan, "descs"));
@@ -692,8 +698,8 @@ int kvr_dev_buffer_bytes(kvr_dev *d, int buffer, uint64_t *out) {
         case KVR_BUF_ARENA: *out = uint64_t(c.arena_pages) * c.page_bytes; break;
         case KVR_BUF_RING: *out = uint64_t(c.n_slots) * c.L * c.Rp * c.row_elems * c.esz; break;
         case KVR_BUF_TMAP: *out = uint64_t(c.n_slots) * c.max_tokens * 4; break;
-        case KVR_BUF_OUT:
-        case KVR_BUF_QUERY: *out = uint64_t(c.n_slots) * c.L * c.Hq * c.hd * 4; break;
+        case KVR_BUF_OUT: *out = uint64_t(c.n_slots) * c.L * c.Hq * c.hd * 4; break;
+        case KVR_BUF_QUERY: *out = uint64_t(c.n_slots) * c.L * c.Hq * c.hd * c.q_esz; break;
         case KVR_BUF_FAR: *out = uint64_t(c.n_slots) * c.L * c.max_chunks * c.row_elems * c.esz; break;
         case KVR_BUF_TRAINS: *out = sizeof(kvr_train) * c.max_trains; break;
         case KVR_BUF_DESCS: *out = sizeof(kvr_descriptor) * c.max_scan; break;

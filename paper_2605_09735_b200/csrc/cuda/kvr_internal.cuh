@@ -50,7 +50,8 @@ struct DevCtx {
     uint32_t *smap;   // [slot][smap_cap]
     uint8_t *far;     // [slot][L][max_chunks][row_elems] elements
     uint8_t *stash;   // [slot][max_chunks][token_bytes]: K-presum chunk means (far view only)
-    float *q;         // [slot][L][Hq][hd]
+    float *q;         // [slot][L][Hq][hd]: fp32, or the KV element type when q_esz == 2 (load_q)
+    uint32_t q_esz;   // 2: exact queries stored as bf16/fp16 (exact: multiples of 1/128); 4: fp32
     float *out;       // [slot][L][Hq][hd]
     const uint8_t *desc; // device copy of the step descriptor
     kvr_train *trains;
@@ -130,6 +131,14 @@ template <int kTag> struct TlScopeT : SpanStamp {
     }
 };
 using TlScope = TlScopeT<0>;
+
+/// Query element i of the query buffer as fp32 (exact either way).
+__device__ __forceinline__ float load_q(const DevCtx &c, uint64_t i) {
+    if (c.q_esz == 4)
+        return c.q[i];
+    const uint16_t b = reinterpret_cast<const uint16_t *>(c.q)[i];
+    return c.elem_kind == KVR_ELEM_BF16 ? __uint_as_float(uint32_t(b) << 16) : __half2float(__ushort_as_half(b));
+}
 
 /// Token `tok` of a slot is written into the ring by K-write / K-prime only when it
 /// lies in the live window after this step and K-gather does not deliver it (near

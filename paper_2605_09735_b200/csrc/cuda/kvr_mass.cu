@@ -89,7 +89,7 @@ __global__ void __launch_bounds__(1024) k_mass_rows(DevCtx c) {
     const uint32_t ring0 = uint32_t(lo % c.R); // ring row of view row n_far
     static_assert(kSplitRows == 8, "the butterfly below reduces 8 rows");
     for (uint32_t kvh = threadIdx.x >> 5; kvh < c.Hkv; kvh += blockDim.x >> 5) {
-        const float *q = c.q + ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * G) * HD + DPL * lane;
+        const uint64_t q0 = ((uint64_t(slot) * c.L + l) * c.Hq + uint64_t(kvh) * G) * HD + DPL * lane;
         const T *ring = reinterpret_cast<const T *>(c.ring) + ring_row(c, slot, l, 0) + uint64_t(kvh) * HD + DPL * lane;
         const T *far = reinterpret_cast<const T *>(c.far) +
                        (uint64_t(slot) * c.L + l) * c.max_chunks * c.row_elems + uint64_t(kvh) * HD + DPL * lane;
@@ -117,7 +117,7 @@ __global__ void __launch_bounds__(1024) k_mass_rows(DevCtx c) {
                 float a = 0.f;
 #pragma unroll
                 for (int d = 0; d < DPL; ++d)
-                    a = fmaf(q[g * HD + d], k[r][d], a);
+                    a = fmaf(load_q(c, q0 + g * HD + d), k[r][d], a);
                 part[r] = a;
             }
             // halving butterfly: lane ends with row lane >> 2 summed over 8 lanes, then

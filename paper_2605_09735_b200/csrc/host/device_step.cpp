@@ -20,6 +20,7 @@
 #include <stdexcept>
 #include <unordered_map>
 #include <unordered_set>
+#include <vector>
 
 #include "kvrail/device_step.hpp"
 
@@ -894,10 +895,41 @@ void DeviceStep::read_attention(uint32_t slot, float *out) {
     ck(kvr_dev_read(impl_->dev, KVR_BUF_OUT, uint64_t(slot) * n * 4, n * 4, out));
 }
 
+namespace {
+float bits_to_float(uint32_t b) {
+    float f;
+    std::memcpy(&f, &b, 4);
+    return f;
+}
+/// IEEE binary16 -> binary32 (exact; the device's exact queries are normal or zero)
+float half_to_float(uint16_t h) {
+    const uint32_t sign = uint32_t(h & 0x8000u) << 16, exp = (h >> 10) & 0x1fu, man = h & 0x3ffu;
+    if (exp == 0 && man == 0)
+        return bits_to_float(sign);
+    if (exp == 0) { // subnormal
+        float v = float(man) * (1.0f / 16777216.0f); // man * 2^-24
+        return sign ? -v : v;
+    }
+    if (exp == 31)
+        return bits_to_float(sign | 0x7f800000u | (man << 13));
+    return bits_to_float(sign | ((exp + 112u) << 23) | (man << 13));
+}
+} // namespace
+
 void DeviceStep::read_query(uint32_t slot, float *out) {
     const kvr_geometry &g = impl_->g;
     const uint64_t n = uint64_t(g.layers) * g.q_heads * g.head_dim;
-    ck(kvr_dev_read(impl_->dev, KVR_BUF_QUERY, uint64_t(slot) * n * 4, n * 4, out));
+    // exact queries live in the KV element type on the device (kvr_dev.cu: q_esz)
+    uint64_t qbytes = 0;
+    ck(kvr_dev_buffer_bytes(impl_->dev, KVR_BUF_QUERY, &qbytes));
+    if (qbytes == uint64_t(g.n_slots) * n * 4) { // fp32 queries
+        ck(kvr_dev_read(impl_->dev, KVR_BUF_QUERY, uint64_t(slot) * n * 4, n * 4, out));
+        return;
+    }
+    std::vector<uint16_t> h(n);
+    ck(kvr_dev_read(impl_->dev, KVR_BUF_QUERY, uint64_t(slot) * n * 2, n * 2, h.data()));
+    for (uint64_t i = 0; i < n; ++i)
+        out[i] = g.elem_kind == KVR_ELEM_BF16 ? bits_to_float(uint32_t(h[i]) << 16) : half_to_float(h[i]);
 }
 
 void DeviceStep::read_far_row(uint32_t slot, uint64_t chunk, void *out) {
