@@ -96,6 +96,10 @@ constexpr bool kUseTile5d = KVR_TC_TILE5D != 0;
 #define KVR_TC_LAZY_T 8
 #endif
 constexpr float kLazy = KVR_TC_LAZY_T; // (0: flip on every raise — a test build exercising the flips)
+// lazy mode: a barrier OR-vote per tile replaces the tile-max exchange unless a row raises
+#ifndef KVR_TC_VOTE
+#define KVR_TC_VOTE 1
+#endif
 constexpr int kThreads = 384; // warp 0 K TMA, 1 S MMA, 2 V TMA, 3 PV MMA, warps 4-7 / 8-11 softmax
 
 __device__ inline uint32_t smem_u32(const void *p) { return uint32_t(__cvta_generic_to_shared(p)); }
@@ -937,6 +941,64 @@ __global__ void __launch_bounds__(kThreads, 1)
                 __syncwarp();
                 if (lane == 0)
                     mbar_arrive(&B.sempty[b]);
+#if KVR_TC_VOTE
+                float sc[G], mx[G];
+                float scl[G], pv[G];
+                // One barrier reduction decides whether any row of the tile raises a held
+                // maximum past kLazy (always on an item's first tile: m = -inf); only then
+                // are the tile maxima exchanged through shared memory.
+                bool mine = false;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    float s_small = sv[G + g];
+                    if constexpr (SP::QS == 3)
+                        s_small += sv[2 * G + g];
+                    sc[g] = valid ? (sv[g] + s_small) * scale_log2 : -INFINITY;
+                    mine = mine || sc[g] > m[g] + kLazy;
+                }
+                uint32_t any_raise;
+                asm volatile("{\n\t.reg .pred q, r;\n\tsetp.ne.u32 q, %1, 0;\n\t"
+                             "bar.red.or.pred r, %2, 128, q;\n\tselp.u32 %0, 1, 0, r;\n\t}"
+                             : "=r"(any_raise)
+                             : "r"(uint32_t(mine)), "r"(bar_id)
+                             : "memory");
+                const bool need = any_raise != 0;
+                if (need) {
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        float v = sc[g];
+#pragma unroll
+                        for (int off = 16; off; off >>= 1)
+                            v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, off));
+                        mx[g] = v;
+                    }
+                    if (lane == 0)
+#pragma unroll
+                        for (int g = 0; g < G; ++g)
+                            rd[(b * 4 + wq) * 8 + g] = mx[g];
+                    asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
+#pragma unroll
+                    for (int g = 0; g < G; ++g) {
+                        const float tm = fmaxf(fmaxf(rd[(b * 4 + 0) * 8 + g], rd[(b * 4 + 1) * 8 + g]),
+                                               fmaxf(rd[(b * 4 + 2) * 8 + g], rd[(b * 4 + 3) * 8 + g]));
+                        const float mn = fmaxf(m[g], tm);
+                        scl[g] = m[g] == -INFINITY ? 1.f : exp2f(m[g] - mn);
+                        l[g] *= scl[g];
+                        m[g] = mn;
+                    }
+                } else {
+#pragma unroll
+                    for (int g = 0; g < G; ++g)
+                        scl[g] = 1.f;
+                }
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const float p = valid ? exp2f(sc[g] - m[g]) : 0.f;
+                    l[g] += p;
+                    pv[g] = p;
+                }
+#else
+                float scl[G], pv[G];
                 float sc[G], mx[G];
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
@@ -957,7 +1019,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 asm volatile("bar.sync %0, 128;" ::"r"(bar_id) : "memory");
                 // tile maxima (identical in every thread of the warpgroup: uniform decision)
                 bool need = false;
-                float scl[G], pv[G];
 #pragma unroll
                 for (int g = 0; g < G; ++g) {
                     const float tm = fmaxf(fmaxf(rd[(b * 4 + 0) * 8 + g], rd[(b * 4 + 1) * 8 + g]),
@@ -975,6 +1036,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     l[g] += p;
                     pv[g] = p;
                 }
+#endif
                 const bool flip = need && ep > 0;
                 uint8_t *pb = qb + kQBytes + b * kOpBytes;
                 if (n >= 2) // P buffer b: the PV of this warpgroup's tile n - 2 has read it
