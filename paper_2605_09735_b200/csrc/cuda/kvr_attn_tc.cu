@@ -21,9 +21,11 @@
 //           sub-partition: C5 0.4478 -> 0.4467 -> 0.4409 ms, S then PV);
 //   warps 4-7, 8-11  two softmax/correction warpgroups, items alternating between
 //           them: thread t owns TMEM lane t, i.e. token row t of S and head dim t
-//           of O. Online softmax in base 2 per q-head column (cross-warp tile max
-//           through shared memory), P written back as bf16/fp16 for the PV MMA, O
-//           folded into fp32 registers; the next item's Q is fetched ahead.
+//           of O. Online softmax in base 2 per q-head column with a held maximum:
+//           O accumulates in TMEM across the item's tiles and is read back only when
+//           a tile raises the maximum by more than 2^8 (one barrier OR-vote per tile
+//           decides; only then are the tile maxima exchanged), P written back as
+//           bf16/fp16 for the PV MMA; the next item's Q is fetched ahead.
 // Precision: the MMA operands are 16-bit, so q and p are split into 16-bit terms
 // (x = x_0 + x_1 [+ x_2], each the rounding of the remainder) in column blocks
 // [s*g, (s+1)*g) of the operand, and S / O are the sums of the column blocks. fp16
@@ -87,7 +89,7 @@ constexpr bool kUseTile5d = KVR_TC_TILE5D != 0;
 // lazy O rescaling (needs the in-order PV issuer): rescale only when a tile's maximum
 // exceeds the held one by more than kLazy (log2 units: p <= 256)
 #ifndef KVR_TC_LAZY
-#define KVR_TC_LAZY 0
+#define KVR_TC_LAZY 1
 #endif
 #if KVR_TC_LAZY && !KVR_TC_PVWAIT
 #error "KVR_TC_LAZY needs KVR_TC_PVWAIT"
