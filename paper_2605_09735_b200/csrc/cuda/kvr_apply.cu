@@ -162,7 +162,7 @@ __device__ __forceinline__ int4 payload16(const DevCtx &c, const LaneTable &tab,
 // `cold`: 0 = the hot write ops (rows read later in this step), 1 = the cold ops
 // (older prompt rows nothing in this step reads; launched after K-attn).
 template <uint32_t kPer, int kKind> // chunks per thread per unit; payload kind
-__device__ __forceinline__ void write_body(const DevCtx &c, int cold) {
+__device__ __forceinline__ void write_body(const DevCtx &c, int cold, uint32_t bid, uint32_t nblk) {
     __shared__ LaneTable tab;
     const kvr_step_header *h = hdr(c);
     const uint32_t n_hot = h->n_write - h->n_far_jobs - h->n_cold;
@@ -182,8 +182,8 @@ __device__ __forceinline__ void write_body(const DevCtx &c, int cold) {
     const uint64_t units = total * slices;
     // each CTA walks a contiguous run of units: one binary search, then the op
     // cursor only moves forward (ops are sorted by token prefix)
-    const uint64_t per = (units + gridDim.x - 1) / gridDim.x;
-    const uint64_t u0 = blockIdx.x * per, u1 = min(units, u0 + per);
+    const uint64_t per = (units + nblk - 1) / nblk;
+    const uint64_t u0 = bid * per, u1 = min(units, u0 + per);
     uint32_t cur = 0;
     if (u0 < u1) // last op with prefix <= j0 (every warp searches: 2-3 rounds of parallel probes)
         cur = warp_last_le(n, u0 / slices, [&](uint32_t i) { return ops[i].prefix; });
@@ -251,9 +251,7 @@ __device__ __forceinline__ uint32_t pack_exact2(const DevCtx &c, float a, float 
     return *reinterpret_cast<const uint32_t *>(&h);
 }
 
-__global__ void __launch_bounds__(256) k_query(DevCtx c) {
-    pdl_trigger();
-    TlScope tl_(c, kTlQuery);
+__device__ __forceinline__ void query_body(const DevCtx &c, uint32_t bid, uint32_t nblk) {
     // byte k of x -> (b - 128) / 128, exactly: b placed in the mantissa of 2^23 + b
     auto val = [](uint32_t x, uint32_t k) {
         return fmaf(__uint_as_float(__byte_perm(x, 0x4B000000u, 0x7440 | k)), 0.0078125f, -65537.f);
@@ -261,7 +259,7 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
     const kvr_step_header *h = hdr(c);
     const kvr_slot_state *slots = section<kvr_slot_state>(c, h->off_slots);
     const uint32_t per_layer = c.Hq * c.hd;
-    for (uint32_t sl = blockIdx.x; sl < c.n_slots * c.L; sl += gridDim.x) {
+    for (uint32_t sl = bid; sl < c.n_slots * c.L; sl += nblk) {
         const uint32_t s = sl / c.L, l = sl - s * c.L;
         if (!slots[s].live)
             continue;
@@ -310,6 +308,12 @@ __global__ void __launch_bounds__(256) k_query(DevCtx c) {
             }
         }
     }
+}
+
+__global__ void __launch_bounds__(256) k_query(DevCtx c) {
+    pdl_trigger();
+    TlScope tl_(c, kTlQuery);
+    query_body(c, blockIdx.x, gridDim.x);
 }
 
 // ---------------------------------------------------------------------------
@@ -625,11 +629,17 @@ template <int kKind> __global__ void __launch_bounds__(256) k_write_cols(DevCtx 
         stamp_if_last(c);
 }
 
-template <uint32_t kPer, int kKind> __global__ void __launch_bounds__(256) k_write(DevCtx c, int cold, int stamp) {
+// nq > 0: the last nq CTAs generate the decode queries instead (KVR_QMERGE: the queries
+// ride in the hot K-write's launch, no forked branch and no join before K-attn)
+template <uint32_t kPer, int kKind>
+__global__ void __launch_bounds__(256) k_write(DevCtx c, int cold, int stamp, uint32_t nq) {
     pdl_wait();
     pdl_trigger();
     TlScope tl_(c, cold ? kTlWriteCold : kTlWriteHot);
-    write_body<kPer, kKind>(c, cold);
+    if (nq && blockIdx.x >= gridDim.x - nq)
+        query_body(c, blockIdx.x - (gridDim.x - nq), nq);
+    else
+        write_body<kPer, kKind>(c, cold, blockIdx.x, gridDim.x - nq);
     if (stamp)
         stamp_if_last(c);
 }
@@ -724,16 +734,17 @@ int hot_kind() {
 } // namespace
 
 // cold: 0 hot writes, 1 cold writes (both over the whole GPU)
-void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp, bool pdl) {
+void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp, bool pdl, bool with_queries) {
     // hot writes (few decode tokens + window rows): one chunk per thread for
     // spread; cold prompt rows: two chunks per thread for generator ILP
     const int kind = c.esz == 4 ? kLanes32 : c.payload_mode == KVR_PAYLOAD_LANES ? kLanes16 : kBytes;
     const unsigned g = unsigned(sms) * (cold ? 8 : 4 * grid_scale());
+    const uint32_t nq = with_queries ? uint32_t(sms) * 2 * grid_scale() : 0u;
     auto go = [&](auto per, auto kk) {
-        launch_ex(k_write<decltype(per)::value, decltype(kk)::value>, g, 256, 0, s, pdl, c, cold, stamp);
+        launch_ex(k_write<decltype(per)::value, decltype(kk)::value>, g + nq, 256, 0, s, pdl, c, cold, stamp, nq);
     };
     using std::integral_constant;
-    if (cold ? cold_kind() == 1 : hot_kind() == 1) {
+    if (cold ? cold_kind() == 1 : (hot_kind() == 1 && !with_queries)) {
         if (kind == kLanes16)
             launch_ex(k_write_cols<kLanes16>, g, 256, 0, s, pdl, c, cold, stamp);
         else if (kind == kLanes32)

@@ -163,6 +163,15 @@ int query_fork() {
     return k;
 }
 
+// KVR_QMERGE=1: the decode queries are extra CTAs of the hot K-write launch (no branch)
+bool query_merge() {
+    static const bool v = [] {
+        const char *e = getenv("KVR_QMERGE");
+        return e && e[0] == '1';
+    }();
+    return v;
+}
+
 // KVR_QJOIN=gather: the queries branch joins before K-gather instead of before K-attn (A/B)
 bool query_join_at_gather() {
     static const bool v = [] {
@@ -207,7 +216,8 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     // writes): a fork edge after K-apply cost ~11 us before they started (timeline).
     const bool pdl = pdl_enabled() && !d->phase_events;
     cudaStream_t side = d->side, side2 = d->side2;
-    const int qfork = query_fork(); // 0 root, 1 after K-apply, 2 after the hot K-write
+    const bool qmerge = query_merge(); // queries generated inside the hot K-write launch
+    const int qfork = qmerge ? -1 : query_fork(); // 0 root, 1 after K-apply, 2 after the hot K-write
     auto fork_queries = [&] {
         ck(cudaEventRecord(d->ev_fork2, s), "fork");
         ck(cudaStreamWaitEvent(side2, d->ev_fork2, 0), "fork wait");
@@ -224,19 +234,19 @@ void run_step_kernels(kvr_dev *d, const DevCtx &c, bool full_step, int k = -1, b
     if (qfork == 1)
         fork_queries();
     mark(1);
-    launch_write(c, s, d->sms, 0, 0, pdl);
+    launch_write(c, s, d->sms, 0, 0, pdl, qmerge);
     if (qfork == 2)
         fork_queries();
     mark(2);
     launch_far_map_prime(c, s, d->sms, pdl);
     mark(3);
     ck(cudaStreamWaitEvent(s, d->ev_join, 0), "join wait");
-    const bool qjoin_gather = query_join_at_gather();
+    const bool qjoin_gather = !qmerge && query_join_at_gather();
     if (qjoin_gather) // K-attn's only dependency is then K-gather's PDL edge
         ck(cudaStreamWaitEvent(s, d->ev_join2, 0), "join wait");
     mark(4);
     launch_gather(c, s, d->sms, pdl);
-    if (!qjoin_gather)
+    if (!qjoin_gather && !qmerge)
         ck(cudaStreamWaitEvent(s, d->ev_join2, 0), "join wait");
     mark(5);
     if (d->g.attention && d->attn)

@@ -230,7 +230,9 @@ inline void launch_ex(void (*k)(P...), unsigned grid, unsigned block, size_t sme
 // pdl: the launch's stream predecessor is a kernel of the same step (PDL edge)
 void launch_apply(const DevCtx &c, cudaStream_t s, int sms);   // zero, cow, blob
 /// stamp: this launch is the step's last kernel and writes the step-end timestamp
-void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp = 0, bool pdl = false); // generated payloads
+/// with_queries: the decode queries are generated by extra CTAs of this (hot) launch
+void launch_write(const DevCtx &c, cudaStream_t s, int sms, int cold, int stamp = 0, bool pdl = false,
+                  bool with_queries = false); // generated payloads
 void launch_query(const DevCtx &c, cudaStream_t s, int sms);   // decode queries
 void launch_far_map_prime(const DevCtx &c, cudaStream_t s, int sms, bool pdl = false); // K-far + K-map + K-prime
 void launch_stamp(const DevCtx &c, cudaStream_t s); // step-end timestamp
