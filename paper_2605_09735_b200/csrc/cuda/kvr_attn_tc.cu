@@ -363,9 +363,12 @@ __device__ inline bool elect_one() {
 /// every role reads the CTA's j-th item from it (item j -> softmax warpgroup j % 2).
 constexpr uint32_t kQ = 64;     // queue entries (roles lag the claimer by < ~10 items)
 #ifndef KVR_TC_AHEADQ
-#define KVR_TC_AHEADQ 4
+#define KVR_TC_AHEADQ 2
 #endif
-constexpr uint32_t kAheadQ = KVR_TC_AHEADQ; // items claimed ahead of the claimer's own position
+// items claimed ahead of the claimer's own position: fewer keeps the end of a launch
+// balanced (A/B, K-attn ms: 8 -> C5 0.4348 / C3 1.2415, 4 -> 0.4306 / 1.2344, 2 -> 0.4286 /
+// 1.2307)
+constexpr uint32_t kAheadQ = KVR_TC_AHEADQ;
 #ifndef KVR_TC_FIRST_CLAIM
 #define KVR_TC_FIRST_CLAIM 1
 #endif
